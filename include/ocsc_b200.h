@@ -1,0 +1,167 @@
+/*
+ * ocsc_b200.h -- C-ABI of libocsc_b200.so, the B200 (sm_100a) hot path of
+ * online convolutional sparse coding (arXiv 1706.06972).
+ *
+ * The reference (`ocsc`, pure Python/numpy) has no FFI; its boundary is the
+ * Python API of pkg/src/ocsc/__init__.py.  Each entry point below replaces
+ * the numpy arithmetic of one reference function (cited file:line, relative to
+ * the reference's pkg/src/ocsc/).  The Python package paper_1706_06972_b200
+ * binds these with ctypes and keeps the reference's
+ * names, signatures and exceptions on top.
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer owned by the caller unless noted;
+ *     everything is enqueued on `stream` (a cudaStream_t, NULL = legacy
+ *     default) and returns without a host sync unless noted.
+ *   - dtype: OCSC_F32 (float / complex64) or OCSC_F64 (double / complex128).
+ *     Complex arrays are interleaved (re, im) pairs.
+ *   - Grids are H x W (a 1-D signal of length W is H = 1).  Half spectra
+ *     ("rfft2 layout") are H x Wh with Wh = W/2 + 1, nfreq = H*Wh; planes are
+ *     stored (plane, H, W) / (plane, H, Wh), row-major.
+ *   - Forward transforms are unnormalised; inverse transforms carry 1/P
+ *     (transforms.py:1-8).
+ *   - Packed Hermitian matrices store the lower triangle row by row:
+ *     entry (i, j), j <= i, at i*(i+1)/2 + j; one matrix per frequency.
+ *   - Return value: OCSC_OK or a negative status; ocsc_last_error() gives
+ *     the message of the last failure on the calling thread.
+ */
+#ifndef OCSC_B200_H
+#define OCSC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OCSC_ABI_VERSION 1
+
+#define OCSC_F32 4
+#define OCSC_F64 8
+
+#define OCSC_OK 0
+#define OCSC_ESHAPE (-1)    /* errors.py:4-5  ShapeMismatchError            */
+#define OCSC_EDIVERGED (-2) /* errors.py:12-13 DivergenceError              */
+#define OCSC_EUNINIT (-3)   /* errors.py:16-17 UninitializedHistoryError    */
+#define OCSC_ECUDA (-4)     /* CUDA / cuFFT failure                         */
+#define OCSC_EARG (-6)      /* bad dtype / unsupported size                 */
+
+const char* ocsc_last_error(void);
+int ocsc_abi_version(void);
+
+/* ------------------------------------------------------------ transforms --
+ * transforms.py:82-87, 148-158 (forward_dft[_cols]); :90-109, 161-176
+ * (inverse_dft[_cols] + the imaginary-residue guard). */
+
+/* xh[n] = rfft2(x[n]) for n < nplanes; x (nplanes,H,W) real -> xh (nplanes,H,Wh). */
+int ocsc_rfft2(int dtype, int H, int W, int nplanes, const void* x, void* xh, void* stream);
+/* x[n] = irfft2(xh[n]) / P.  xh is CLOBBERED (cuFFT C2R). */
+int ocsc_irfft2(int dtype, int H, int W, int nplanes, void* xh, void* x, void* stream);
+/* Full complex DFT of reference columns (P, ncols), K fastest, row-major (H, W) pixels.
+ * in_complex = 0: `in` is real (P, ncols); 1: complex.  inverse = 1 uses e^{+i}; no scaling. */
+int ocsc_dft_cols(int dtype, int H, int W, int ncols, const void* in, int in_complex, void* out,
+                  int inverse, void* stream);
+/* stats[0] = max |Im spatial|, stats[1] = max |spec| over n complex entries each
+ * (atomic max; caller zeroes stats).  transforms.py:102-109 */
+int ocsc_residue_stats(int dtype, int64_t n, const void* spatial, const void* spec, double* stats,
+                       void* stream);
+/* out[i] = scale * Re(in[i]) */
+int ocsc_real_part(int dtype, int64_t n, const void* in, double scale, void* out, void* stream);
+/* half spectra (nplanes, H, Wh) -> full spectrum columns (P, nplanes) by Hermitian extension */
+int ocsc_half_to_cols(int dtype, int H, int W, int nplanes, const void* half, void* cols, void* stream);
+/* full spectrum columns (P, ncols) -> half spectra (ncols, H, Wh) (gather) */
+int ocsc_cols_to_half(int dtype, int H, int W, int ncols, const void* cols, void* half, void* stream);
+/* stats[0] = max |X[p] - conj X[-p]|, stats[1] = max |X| over columns (P, ncols) (caller zeroes) */
+int ocsc_hermitian_defect(int dtype, int H, int W, int ncols, const void* cols, double* stats,
+                          void* stream);
+
+/* ---------------------------------------------------------------- coding --
+ * coding.py:45-134 */
+
+/* coding.py:45-48 */
+int ocsc_soft_threshold(int dtype, int64_t n, const void* in, double kappa, void* out, void* stream);
+/* coding.py:51-64, rows (nrows, K) complex, x (nrows) complex */
+int ocsc_solve_code_rows(int dtype, int nrows, int K, const void* d, const void* x, const void* t,
+                         double rho, void* out, void* stream);
+/* den[p] = rho + sum_k |Wh[k][p]|^2, Wh (K, nfreq) */
+int ocsc_code_den(int dtype, int K, int nfreq, const void* Wh, double rho, void* den, void* stream);
+/* Bytes of scratch ocsc_code_admm needs for (H, W, K, B); want_z adds the z buffer. */
+size_t ocsc_code_workspace_bytes(int dtype, int H, int W, int K, int B, int want_z);
+/* Batched ADMM sparse coding, coding.py:67-119, for B samples against one dictionary.
+ *   xh   (B, nfreq)       sample spectra (ocsc_rfft2 of the samples)
+ *   Wh   (K, nfreq)       dictionary spectrum;  den (nfreq) from ocsc_code_den
+ *   u, t (B, K, H, W)     in: code U and U - Gamma (zeros = cold start); out: final values
+ *   zh   (B, K, nfreq)    optional (NULL): spectrum of the last ADMM iterate z
+ *   iters, status (B)     int32: iterations run; 0 = hit max_iters, 1 = converged,
+ *                         2 = diverged (non-finite code) at iteration iters[b]
+ * Each sample stops at exactly the iteration the reference would (the
+ * two-part test of coding.py:113-118); converged samples are frozen on device.
+ * poll > 0: the host checks the all-converged flag every `poll` iterations,
+ * one chunk behind the device (no pipeline bubble); poll = 0 never syncs. */
+int ocsc_code_admm(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
+                   const void* den, double beta, double rho, int max_iters, double rel_tol,
+                   void* u, void* t, void* zh, void* work, int32_t* iters, int32_t* status,
+                   int poll, void* stream);
+/* coding.py:122-134 for B codes: uh = rfft2(u) (B, K, nfreq) and
+ * obj[b] = 0.5 ||x_b - sum_k w_k (*) u_bk||^2 + beta ||u_b||_1 (double, device);
+ * resid[b] (optional) = ||x_b - reconstruction||^2 (evaluate.py:55-62 PSNR input). */
+int ocsc_code_objective(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
+                        const void* u, double beta, void* uh, double* obj, double* resid,
+                        void* stream);
+/* out[b][p] = sum_k Wh[k][p] zh[b][k][p]  (reconstruct, coding.py:122-126, in frequency) */
+int ocsc_synthesize(int dtype, int K, int nfreq, int B, const void* Wh, const void* zh, void* out,
+                    void* stream);
+
+/* --------------------------------------------------------------- history --
+ * dictionary.py:30-131.  State is kept as SUMS: S_p = sum z z^H (packed),
+ * c_p = sum conj(x) z, with the count t on the host; the reference's averaged
+ * cross = c/t and inv_gram = t (S + t rho P I)^-1 are the same quantities. */
+
+/* S (nfreq, K(K+1)/2), c (nfreq, K) += rank-B update; z element (b,k,p) at
+ * z[b*z_sb + k*z_sk + p*z_sp], x element (b,p) at x[b*x_sb + p*x_sp]. */
+int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int nfreq, int B, const void* z,
+                            int64_t z_sb, int64_t z_sk, int64_t z_sp, const void* x, int64_t x_sb,
+                            int64_t x_sp, void* S, void* c, void* stream);
+/* inv_p = scale * (S_p + ridge I)^-1 via per-frequency Cholesky (packed in/out).
+ * info (device int32): 0, or 1 + first frequency whose matrix was not positive definite. */
+int ocsc_history_invert(int dtype_hist, int K, int nfreq, const void* S, double ridge, double scale,
+                        void* inv, int32_t* info, void* stream);
+/* packed (nfreq, K(K+1)/2) Hermitian -> full (nfreq, K, K), times scale */
+int ocsc_packed_to_full(int dtype, int K, int nfreq, const void* packed, double scale, void* full,
+                        void* stream);
+/* flag (device int32) |= 1 if any of n values (complex: 2n reals) is non-finite */
+int ocsc_nonfinite(int dtype, int64_t n_reals, const void* a, int32_t* flag, void* stream);
+
+/* ------------------------------------------------------------ dictionary --
+ * dictionary.py:134-215 */
+
+/* Row solve, dictionary.py:134-142, in sum form:
+ * conj(D_p) = inv_p (c_p + ridge conj(V_p - Theta_p)), inv from ocsc_history_invert
+ * with scale 1, ridge = t rho P.  V/Theta/D element (k,p) at [k*sk + p*sp]. */
+int ocsc_dict_rowsolve(int dtype, int dtype_hist, int K, int nfreq, const void* inv, const void* c,
+                       double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
+                       void* Dh, void* stream);
+/* One fused projection round on half spectra (K, H, Wh), dictionary.py:145-154 + :205-207:
+ * alpha_k = crop(irfft2(D_k + Theta_k)) / max(||.||, 1); V_k = rfft2(pad(alpha_k));
+ * Theta_k += D_k - V_k.  Pruned separable DFTs: only the M0 x M1 support is touched.
+ * alpha (K, M0*M1) row-major support. */
+int ocsc_dict_project(int dtype, int H, int W, int M0, int M1, int K, const void* Dh, void* Th,
+                      void* Vh, void* alpha, void* stream);
+/* alpha_k = crop(irfft2(X_k)) without normalisation (training.py:165-169 final_filters). */
+int ocsc_crop_irfft(int dtype, int H, int W, int M0, int M1, int K, const void* Xh, void* alpha,
+                    void* stream);
+/* Full-spectrum projection tail on reference columns: spatial (P, K) real ->
+ * padded (P, K) real with the support scaled into the unit ball. */
+int ocsc_crop_normalize_cols(int dtype, int H, int W, int M0, int M1, int K, const void* spatial,
+                             void* padded, void* stream);
+/* Support (K, M0*M1) -> spectra (K, H, Wh) via the pruned forward DFT (dict_state_from_filters). */
+int ocsc_support_rfft(int dtype, int H, int W, int M0, int M1, int K, const void* alpha, void* Vh,
+                      void* stream);
+/* out[0] += sum (a-b)^2, out[1] += sum a^2 over n reals (b may be NULL: treated as 0) */
+int ocsc_norms2(int dtype, int64_t n, const void* a, const void* b, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCSC_B200_H */

@@ -1,0 +1,119 @@
+// Shared device helpers for libocsc_b200 (sm_100a).
+//
+// Complex values are float2 / double2 (interleaved re, im) -- the layout
+// cuFFT and torch.complex64/complex128 use, so spectra cross the C-ABI as
+// plain pointers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/ocsc_b200.h"
+
+namespace ocsc {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define OCSC_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e__ = (call);                             \
+    if (e__ != cudaSuccess) return ::ocsc::cuda_fail(e__, #call); \
+  } while (0)
+
+#define OCSC_LAUNCHED(name)                                              \
+  do {                                                                   \
+    cudaError_t e__ = cudaGetLastError();                                \
+    if (e__ != cudaSuccess) return ::ocsc::cuda_fail(e__, name);         \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// --------------------------------------------------------------- complex --
+template <typename T> struct Cx;
+template <> struct Cx<float> { using type = float2; };
+template <> struct Cx<double> { using type = double2; };
+template <typename T> using cx = typename Cx<T>::type;
+
+template <typename C> __host__ __device__ __forceinline__ C mkc(decltype(C::x) r, decltype(C::x) i) {
+  C c; c.x = r; c.y = i; return c;
+}
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return mkc<C>(a.x + b.x, a.y + b.y); }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return mkc<C>(a.x - b.x, a.y - b.y); }
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
+  return mkc<C>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// conj(a) * b
+template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
+  return mkc<C>(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+template <typename C> __device__ __forceinline__ C cconj(C a) { return mkc<C>(a.x, -a.y); }
+template <typename C, typename S> __device__ __forceinline__ C cscale(C a, S s) { return mkc<C>(a.x * s, a.y * s); }
+template <typename C> __device__ __forceinline__ decltype(C::x) cabs2(C a) { return a.x * a.x + a.y * a.y; }
+// acc += a * b
+template <typename C> __device__ __forceinline__ void cfma(C& acc, C a, C b) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+}
+// acc += conj(a) * b
+template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) {
+  acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+}
+
+template <typename To, typename From> __device__ __forceinline__ cx<To> ccast(From a) {
+  return mkc<cx<To>>((To)a.x, (To)a.y);
+}
+
+// ------------------------------------------------------------ reductions --
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum of NV doubles; result valid in thread 0. `scratch` holds 32*NV doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) scratch[i * 32 + warp] = v[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double s = lane < nwarps ? scratch[i * 32 + lane] : 0.0;
+      v[i] = warp_sum(s);
+    }
+  }
+  __syncthreads();
+}
+
+// atomic max for non-negative doubles (bit pattern order == value order)
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  if (!(v >= 0.0)) v = __longlong_as_double(0x7ff8000000000000ULL);  // NaN -> propagate as huge
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// Half-spectrum (rfft2 along W) Hermitian weight of column v: the number of
+// full-spectrum points the stored value stands for in a real sum.
+__device__ __forceinline__ int herm_weight(int v, int W) {
+  return (v == 0 || (2 * v == W)) ? 1 : 2;
+}
+
+__host__ __device__ __forceinline__ int64_t packed_index(int i, int j) {  // j <= i
+  return (int64_t)i * (i + 1) / 2 + j;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace ocsc

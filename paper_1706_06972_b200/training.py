@@ -1,0 +1,386 @@
+"""Online training driver -- drop-in for the reference training.py, device-resident.
+
+`OnlineTrainer` keeps every piece of learner state on the GPU in the half
+spectrum of the real-signal FFT (H x Wh frequencies):
+
+    Wh (K, H, Wh)        working dictionary spectrum F(V) the codes are solved against
+    den (H*Wh)           rho_code + sum_k |Wh_k|^2, the rank-one solve denominator
+    Dh, Th (K, H, Wh)    dictionary ADMM spectrum and dual
+    alpha (K, M)         feasible filters crop(V) (unit ball, support M0 x M1)
+    S, c                 history sums, packed per frequency (dictionary.py docstring)
+
+`partial_fit(X)` is one mini-batch of the composed reference semantics
+(SURVEY.md 8(c)); with B = 1 it is exactly `OnlineTrainer.step`
+(training.py:128-155): code every sample against Wh (cold start), objective,
+fold F(U) into the history, J rounds of dictionary ADMM, Wh <- F(V).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .coding import CodeBuffers, CodeState, CodingConfig, code_den, code_objectives, infer_codes
+from .dictionary import DictState, HistoryState
+from .errors import DivergenceError, ShapeMismatchError
+from .transforms import SignalShape, _np, half_to_cols_dev, rfft2_dev
+
+_REAL = {"float32": torch.float32, "float64": torch.float64}
+_CPLX = {torch.float32: torch.complex64, torch.float64: torch.complex128}
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """Training knobs (training.py:39-64) plus the B200 build's mini-batch/precision fields."""
+
+    n_filters: int = 100
+    beta: float = 1.0
+    rho_code: float = 1.0
+    rho_dict: float = 10.0
+    inner_iters: int = 10
+    max_passes: int = 10
+    stop_tol: float = 1e-3
+    seed: int = 0
+    code_max_iters: int = 300
+    code_rel_tol: float = 1e-3
+    batch_dict_iters: int = 200
+    batch_dict_tol: float = 1e-4
+    fista_iters: int = 100
+    mode: str = "online"
+    # --- B200 build ---
+    batch_size: int = 1            # samples per partial_fit mini-batch
+    dtype: str = "float64"         # code/dictionary arithmetic: float64 (parity) or float32
+    history_dtype: str = "float64" # history sums and Cholesky
+    poll: int = 16                 # code-ADMM convergence poll interval (iterations)
+
+    def coding(self) -> CodingConfig:
+        return CodingConfig(beta=self.beta, rho=self.rho_code, max_iters=self.code_max_iters,
+                            rel_tol=self.code_rel_tol)
+
+
+@dataclass
+class PassRecord:
+    """One training-log row per pass (training.py:67-77)."""
+
+    index: int
+    time_s: float
+    train_obj: float
+    test_obj: float | None
+    psnr: float | None
+    history_bytes: int
+    snapshot_id: str
+
+
+@dataclass
+class TrainReport:
+    """Run output (training.py:80-88) plus the per-sample objective trace."""
+
+    config: TrainConfig
+    shape: SignalShape
+    records: list[PassRecord] = field(default_factory=list)
+    filters: np.ndarray | None = None
+    stopped_early: bool = False
+    objectives: list[float] = field(default_factory=list)
+    codes: list[np.ndarray] | None = None
+
+
+@dataclass
+class BatchResult:
+    """What one partial_fit returns: per-sample objectives and iteration counts (host)."""
+
+    objectives: np.ndarray
+    iterations: np.ndarray
+    codes: torch.Tensor | None = None   # device (B, K, H, W) view, valid until the next call
+
+
+def init_dictionary(shape: SignalShape, n_filters: int, seed: int) -> np.ndarray:
+    """Seeded Gaussian (M, K) filters with unit columns (training.py:91-95).
+
+    Drawn on the host with numpy's generator so the start point is bit-identical
+    to the reference's for the same seed.
+    """
+    f = np.random.default_rng(seed).normal(size=(shape.filter_size, n_filters))
+    return f / np.linalg.norm(f, axis=0)
+
+
+def _snapshot_id(filters: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(filters).tobytes()).hexdigest()[:12]
+
+
+class _HalfHistory(HistoryState):
+    """Trainer history over the half spectrum; `cross`/`inv_gram` materialise the full one."""
+
+    def _full_index(self):
+        H, W = self.shape.grid
+        Wh = W // 2 + 1
+        u, v = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+        stored = v < Wh
+        uu = np.where(stored, u, (H - u) % H)
+        vv = np.where(stored, v, W - v)
+        return (uu * Wh + vv).ravel(), ~stored.ravel()
+
+    def _extend(self, half: torch.Tensor) -> torch.Tensor:
+        idx, conj = self._full_index()
+        full = half[torch.as_tensor(idx, device=half.device)]
+        mask = torch.as_tensor(conj, device=half.device).reshape((-1,) + (1,) * (full.dim() - 1))
+        return torch.where(mask, full.conj(), full)
+
+    @property
+    def cross(self) -> np.ndarray:
+        if self.count == 0:
+            return np.zeros((self.shape.size, self.K), dtype=np.complex128)
+        return _np(self._extend(self.c / self.count)).astype(np.complex128)
+
+    @property
+    def inv_gram(self) -> np.ndarray:
+        if self.count == 0:
+            return np.zeros((self.shape.size, self.K, self.K), dtype=np.complex128)
+        full = torch.empty((self.nfreq, self.K, self.K), dtype=self.S.dtype, device=self.S.device)
+        _lib.call("ocsc_packed_to_full", _lib.code(self.S.dtype), self.K, self.nfreq, _lib.ptr(self.inverse()),
+                  float(self.count), _lib.ptr(full), _lib.stream())
+        return _np(self._extend(full)).astype(np.complex128)
+
+
+class OnlineTrainer:
+    """Streaming trainer (training.py:102-169); `step` = one sample, `partial_fit` = one mini-batch."""
+
+    def __init__(self, shape: SignalShape, config: TrainConfig):
+        self.shape = shape
+        self.config = config
+        self.coding_config = config.coding()
+        if config.dtype not in _REAL or config.history_dtype not in _REAL:
+            raise ValueError("dtype/history_dtype must be 'float32' or 'float64'")
+        self.dtype = _REAL[config.dtype]
+        self.cdtype = _CPLX[self.dtype]
+        hist_cdtype = _CPLX[_REAL[config.history_dtype]]
+        if self.dtype == torch.float64 and hist_cdtype == torch.complex64:
+            raise ValueError("history_dtype must be at least as wide as dtype")
+        self.dev = _lib.device()
+        H, W = shape.grid
+        self.H, self.W = H, W
+        self.M0, self.M1 = shape.support
+        self.K = K = config.n_filters
+        self.nf = shape.half_size
+        filters = init_dictionary(shape, K, config.seed)
+        self.initial_filters = filters
+        self.alpha = torch.as_tensor(filters.T.copy(), dtype=self.dtype).to(self.dev)        # (K, M)
+        self.Wh = torch.empty((K, H, W // 2 + 1), dtype=self.cdtype, device=self.dev)
+        self._support_rfft(self.alpha, self.Wh)
+        self.Dh = self.Wh.clone()
+        self.Th = torch.zeros_like(self.Wh)
+        self.den = code_den(self.Wh, self.coding_config.rho)
+        self.history = _HalfHistory(shape, K, config.rho_dict, nfreq=self.nf, dtype=hist_cdtype)
+        self.rng = np.random.default_rng(config.seed)
+        self._prev_code = None
+        self._prev_alpha = self.alpha.clone()
+        self._metrics = torch.zeros(4, dtype=torch.float64, device=self.dev)
+        self.code_change = np.inf
+        self.dict_change = np.inf
+        self.last_objective = np.nan
+        self._buf = None
+        self._uh = None
+        self._x = None
+
+    # ---------------------------------------------------------- internals --
+    def _support_rfft(self, alpha: torch.Tensor, out: torch.Tensor) -> None:
+        _lib.call("ocsc_support_rfft", _lib.code(self.dtype), self.H, self.W, self.M0, self.M1, self.K,
+                  _lib.ptr(alpha), _lib.ptr(out), _lib.stream())
+
+    def _buffers(self, B: int, want_z: bool) -> CodeBuffers:
+        if self._buf is None or self._buf.B < B or (want_z and not self._buf.want_z):
+            self._buf = CodeBuffers(self.shape, self.K, B, self.dtype, want_z=want_z)
+            self._uh = torch.empty((B, self.K, self.H, self.W // 2 + 1), dtype=self.cdtype, device=self.dev)
+            self._x = torch.empty((B, self.H, self.W), dtype=self.dtype, device=self.dev)
+        return self._buf
+
+    def _load(self, X) -> tuple[torch.Tensor, int]:
+        P = self.shape.size
+        if isinstance(X, torch.Tensor):
+            if X.numel() % P or X.numel() == 0:
+                raise ShapeMismatchError(f"sample has {X.numel()} entries, expected a multiple of {P}")
+            B = X.numel() // P
+            return X.reshape(B, self.H, self.W), B
+        arr = np.asarray(X, dtype=np.float64)
+        if arr.size % P or arr.size == 0:
+            raise ShapeMismatchError(f"sample has {arr.size} entries, expected {P}")
+        B = arr.size // P
+        return torch.from_numpy(np.ascontiguousarray(arr.reshape(B, self.H, self.W))), B
+
+    def _dictionary_update(self) -> None:
+        """J rounds of DictOCSC (dictionary.py:176-215) on device state; Wh <- F(V)."""
+        J = self.config.inner_iters
+        if J == 0:
+            return
+        h = self.history
+        inv = h.inverse(check=False)
+        ridge = h.count * h.ridge
+        dt, ht = _lib.code(self.dtype), _lib.code(h.S.dtype)
+        s = _lib.stream()
+        self.Th.zero_()
+        for _ in range(J):
+            _lib.call("ocsc_dict_rowsolve", dt, ht, self.K, self.nf, _lib.ptr(inv), _lib.ptr(h.c), ridge,
+                      _lib.ptr(self.Wh), _lib.ptr(self.Th), self.nf, 1, _lib.ptr(self.Dh), s)
+            _lib.call("ocsc_dict_project", dt, self.H, self.W, self.M0, self.M1, self.K, _lib.ptr(self.Dh),
+                      _lib.ptr(self.Th), _lib.ptr(self.Wh), _lib.ptr(self.alpha), s)
+        _lib.call("ocsc_code_den", dt, self.K, self.nf, _lib.ptr(self.Wh), self.coding_config.rho,
+                  _lib.ptr(self.den), s)
+
+    # -------------------------------------------------------------- API --
+    def partial_fit(self, X, want_z: bool = False, check: bool = True) -> BatchResult:
+        """One mini-batch of B samples (rows of X, each P entries) through the hot path.
+
+        check=True syncs once after coding to raise DivergenceError before the
+        history is touched (the reference's order, coding.py:105-106); the
+        per-sample objectives/iterations come back to the host at the end.
+        """
+        xs, B = self._load(X)
+        buf = self._buffers(B, want_z)
+        x = self._x[:B]
+        x.copy_(xs, non_blocking=True)
+        xh = rfft2_dev(x, self.shape)
+        infer_codes(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
+        if check:
+            status = buf.status[:B].cpu()
+            if bool((status == 2).any()):
+                it = int(buf.iters[:B][status.to(buf.iters.device) == 2].min().cpu())
+                raise DivergenceError(f"code solver diverged at iteration {it}")
+        uh = self._uh[:B]
+        obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
+        nf = self.nf
+        self.history.accumulate(uh, (self.K * nf, nf, 1), xh, (nf, 1), B)
+        self._dictionary_update()
+        track = self.config.stop_tol > 0
+        if track:
+            self._metrics.zero_()
+            last = buf.u[B - 1]
+            if self._prev_code is not None:
+                _lib.call("ocsc_norms2", _lib.code(self.dtype), last.numel(), _lib.ptr(last),
+                          _lib.ptr(self._prev_code), _lib.ptr(self._metrics), _lib.stream())
+                self._prev_code.copy_(last)
+            else:
+                self._prev_code = last.clone()
+            _lib.call("ocsc_norms2", _lib.code(self.dtype), self.alpha.numel(), _lib.ptr(self.alpha),
+                      _lib.ptr(self._prev_alpha), _lib.ptr(self._metrics[2:]), _lib.stream())
+            self._prev_alpha.copy_(self.alpha)
+        host = torch.cat([obj, buf.iters[:B].double(), self._metrics]).cpu().numpy()
+        objectives, iterations = host[:B], host[B:2 * B].astype(np.int64)
+        if track:
+            m = host[2 * B:]
+            if self.history.count > B:
+                self.code_change = float(np.sqrt(m[0]) / max(np.sqrt(m[1]), 1e-12))
+            self.dict_change = float(np.sqrt(m[2]) / max(np.sqrt(m[3]), 1e-12))
+        self.last_objective = float(objectives[-1])
+        return BatchResult(objectives=objectives, iterations=iterations, codes=buf.u[:B])
+
+    def step(self, x) -> CodeState:
+        """Code one sample, absorb it, refresh the dictionary (training.py:128-155)."""
+        arr = np.asarray(x, dtype=np.float64).ravel() if not isinstance(x, torch.Tensor) else x
+        n = arr.numel() if isinstance(arr, torch.Tensor) else arr.size
+        if n != self.shape.size:
+            raise ShapeMismatchError(f"sample has {n} entries, expected {self.shape.size}")
+        res = self.partial_fit(arr, want_z=True)
+        buf = self._buf
+        K, P = self.K, self.shape.size
+        u = buf.u[0].reshape(K, P)
+        dual = (buf.u[0] - buf.t[0]).reshape(K, P)
+        z_freq = half_to_cols_dev(buf.zh[0], self.shape)
+        return CodeState(z_freq=_np(z_freq).astype(np.complex128), code=_np(u.T).astype(np.float64),
+                         dual=_np(dual.T).astype(np.float64), iterations=int(res.iterations[0]))
+
+    def converged(self) -> bool:
+        tol = self.config.stop_tol
+        return self.code_change < tol and self.dict_change < tol
+
+    def coding_filters(self) -> np.ndarray:
+        """Feasible filters coding uses, (M, K) (training.py:161-163)."""
+        return _np(self.alpha.T).astype(np.float64)
+
+    def final_filters(self) -> np.ndarray:
+        """crop(F^-1(D)), (M, K) (training.py:165-169)."""
+        out = torch.empty_like(self.alpha)
+        _lib.call("ocsc_crop_irfft", _lib.code(self.dtype), self.H, self.W, self.M0, self.M1, self.K,
+                  _lib.ptr(self.Dh), _lib.ptr(out), _lib.stream())
+        return _np(out.T).astype(np.float64)
+
+    # reference attribute views (host copies, full spectra)
+    @property
+    def working_freq(self) -> np.ndarray:
+        return _np(half_to_cols_dev(self.Wh, self.shape)).astype(np.complex128)
+
+    @property
+    def dict_state(self) -> DictState:
+        H, W = self.shape.grid
+        v = torch.zeros((self.K, H, W), dtype=self.dtype, device=self.dev)
+        v[:, :self.M0, :self.M1] = self.alpha.reshape(self.K, self.M0, self.M1)
+        return DictState(freq=_np(half_to_cols_dev(self.Dh, self.shape)).astype(np.complex128),
+                         v=_np(v.reshape(self.K, -1).T).astype(np.float64),
+                         dual=_np(half_to_cols_dev(self.Th, self.shape)).astype(np.complex128))
+
+
+def _evaluate_pass(filters, test_samples, shape, coding, config):
+    if test_samples is None:
+        return None
+    from .evaluate import evaluate_dictionary
+    return evaluate_dictionary(filters, test_samples, shape, coding, dtype=config.dtype)
+
+
+def train_online(samples, shape: SignalShape, config: TrainConfig, test_samples=None,
+                 return_codes: bool = False) -> TrainReport:
+    """Shuffled passes of mini-batches until both change metrics settle (training.py:178-223)."""
+    samples = np.atleast_2d(np.asarray(samples, dtype=np.float64))
+    trainer = OnlineTrainer(shape, config)
+    report = TrainReport(config=config, shape=shape, codes=[] if return_codes else None)
+    if samples.size == 0:
+        report.filters = trainer.coding_filters()
+        return report
+    if samples.shape[1] != shape.size:
+        raise ShapeMismatchError(f"samples must be (N, {shape.size}), got {samples.shape}")
+    B = max(1, int(config.batch_size))
+    train_seconds = 0.0
+    for pass_idx in range(1, config.max_passes + 1):
+        order = trainer.rng.permutation(samples.shape[0])
+        objectives = []
+        tic = time.perf_counter()
+        stopped = False
+        for start in range(0, len(order), B):
+            res = trainer.partial_fit(samples[order[start:start + B]])
+            objectives.extend(res.objectives.tolist())
+            if return_codes:
+                report.codes.append(_np(res.codes.reshape(res.codes.shape[0], trainer.K, -1)).transpose(0, 2, 1))
+            if trainer.converged():
+                stopped = True
+                break
+        train_seconds += time.perf_counter() - tic
+        filters = trainer.final_filters()
+        result = _evaluate_pass(trainer.coding_filters(), test_samples, shape, config.coding(), config)
+        report.objectives.extend(objectives)
+        report.records.append(PassRecord(
+            index=pass_idx, time_s=train_seconds, train_obj=float(np.mean(objectives)),
+            test_obj=None if result is None else result.test_objective,
+            psnr=None if result is None else result.psnr,
+            history_bytes=trainer.history.nbytes, snapshot_id=_snapshot_id(filters)))
+        if stopped:
+            report.stopped_early = True
+            break
+    report.filters = trainer.final_filters()
+    return report
+
+
+def fit(samples, shape: SignalShape, config: TrainConfig, test_samples=None, return_codes: bool = False
+        ) -> TrainReport:
+    """North-star name for `train_online`: filters, objective trace and (optionally) codes."""
+    return train_online(samples, shape, config, test_samples, return_codes=return_codes)
+
+
+def train(mode: str, samples, shape, config, test_samples=None) -> TrainReport:
+    """Mode dispatch (training.py:374-383).  Only the online path is built for B200."""
+    if mode == "online":
+        return train_online(samples, shape, replace(config, mode=mode), test_samples)
+    if mode in ("batch", "fista-dict"):
+        raise NotImplementedError(f"training mode {mode!r} is outside the B200 hot path (SURVEY.md 2.1 rows 4, 7)")
+    raise ValueError(f"unknown training mode: {mode!r}")

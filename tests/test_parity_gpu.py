@@ -1,0 +1,323 @@
+"""Parity of the B200 path (libocsc_b200.so via the drop-in API) with the reference.
+
+Checked against golden vectors the reference produced (tests/golden/) and,
+for the larger / float32 cases, against the CPU oracle (oracle/ocsc_oracle.py).
+float64 bar: 1e-9 relative (north_star); float32 bar: objective trace 1e-4,
+filters 1e-3 relative Frobenius.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1706_06972_b200 as ob  # noqa: E402
+from oracle import ocsc_oracle as O  # noqa: E402
+from tests._layout import cols_to_planes, hw, planes_to_cols, rel  # noqa: E402
+
+TOL64 = 1e-9
+
+
+def _shape(g):
+    return ob.SignalShape(tuple(int(d) for d in g["dims"]), tuple(int(d) for d in g["fdims"]))
+
+
+def test_native_library_is_loaded():
+    from paper_1706_06972_b200 import _lib
+    lib = _lib.load()
+    assert lib.ocsc_abi_version() == 1
+    maps = open("/proc/self/maps").read()
+    assert "libocsc_b200.so" in maps
+
+
+# ------------------------------------------------------------- transforms --
+
+def test_transform_primitives(golden):
+    g = golden("primitives")
+    shape = _shape(g)
+    assert rel(ob.forward_dft_cols(g["cols"], shape), g["fcols"]) < 1e-13
+    back = ob.inverse_dft_cols(g["fcols"], shape)
+    assert np.abs(back - g["cols"]).max() < 1e-12
+    assert np.array_equal(ob.pad_filter_cols(g["filt"], shape), g["padded"])
+    assert np.array_equal(ob.crop_filter_cols(g["padded"], shape), g["filt"])
+    proj = ob.project_filter_cols(ob.forward_dft_cols(g["padded"] * 3.0, shape), shape)
+    assert np.abs(proj - g["proj"]).max() < 1e-12
+    x = np.random.default_rng(0).normal(size=shape.size)
+    assert np.abs(ob.inverse_dft(ob.forward_dft(x, shape), shape) - x).max() < 1e-12
+
+
+def test_residue_guard_rejects_non_hermitian():
+    shape = ob.SignalShape((4, 4), (2, 2))
+    spec = np.zeros(16, complex)
+    spec[1] = 1j
+    with pytest.raises(ob.NumericalConsistencyError):
+        ob.inverse_dft(spec, shape)
+
+
+def test_shape_errors():
+    shape = ob.SignalShape((8,), (3,))
+    with pytest.raises(ob.ShapeMismatchError):
+        ob.forward_dft(np.zeros(7), shape)
+    with pytest.raises(ob.ShapeMismatchError):
+        ob.forward_dft_cols(np.zeros((7, 2)), shape)
+
+
+# ------------------------------------------------------------------ coding --
+
+def test_solve_code_rows_and_soft_threshold(golden):
+    g = golden("primitives")
+    assert np.abs(ob.solve_code_rows(g["d"], g["x"], g["t"], float(g["rho"])) - g["rows"]).max() < 1e-12
+    assert np.array_equal(ob.soft_threshold(g["v"], float(g["kappa"])), g["st"])
+    assert ob.soft_threshold(np.array([0.3, -0.5, 0.0]), 0.5).tolist() == [0.0, 0.0, 0.0]
+
+
+@pytest.mark.parametrize("name", ["code_2d", "code_1d", "code_odd"])
+def test_infer_code_matches_reference(golden, name):
+    g = golden(name)
+    shape = _shape(g)
+    cfg = ob.CodingConfig(beta=float(g["beta"]), rho=float(g["rho"]), max_iters=int(g["max_iters"]),
+                          rel_tol=float(g["rel_tol"]))
+    st = ob.infer_code(g["x"], g["dict_freq"], shape, cfg)
+    assert st.iterations == int(g["iterations"])
+    assert rel(st.code, g["code"]) < TOL64
+    assert rel(st.dual, g["dual"]) < TOL64
+    assert rel(st.z_freq, g["z_freq"]) < TOL64
+    obj = ob.coding_objective(g["x"], g["dict_freq"], st.code, shape, cfg.beta)
+    assert abs(obj - float(g["objective"])) <= TOL64 * abs(float(g["objective"]))
+
+
+def test_infer_code_monitor_trace(golden):
+    g = golden("code_2d")
+    shape = _shape(g)
+    cfg = ob.CodingConfig(beta=float(g["beta"]), rho=float(g["rho"]), max_iters=int(g["max_iters"]),
+                          rel_tol=float(g["rel_tol"]))
+    trace = []
+    st = ob.infer_code(g["x"], g["dict_freq"], shape, cfg,
+                       monitor=lambda it, c: trace.append(np.abs(c).sum()))
+    assert st.iterations == int(g["iterations"]) == len(trace)
+    assert rel(st.code, g["code"]) < TOL64
+
+
+def test_infer_code_divergence_reports_iteration():
+    rng = np.random.default_rng(46)
+    shape = ob.SignalShape((8,), (3,))
+    f = rng.normal(size=(3, 2))
+    d = ob.forward_dft_cols(ob.pad_filter_cols(f / np.linalg.norm(f, axis=0), shape), shape)
+    x = rng.normal(size=8)
+    x[0] = np.nan
+    with pytest.raises(ob.DivergenceError, match="iteration"):
+        ob.infer_code(x, d, shape)
+
+
+def test_zero_signal_and_huge_beta_give_zero_code():
+    rng = np.random.default_rng(30)
+    shape = ob.SignalShape((8,), (3,))
+    f = rng.normal(size=(3, 2))
+    d = ob.forward_dft_cols(ob.pad_filter_cols(f / np.linalg.norm(f, axis=0), shape), shape)
+    assert np.all(ob.infer_code(np.zeros(8), d, shape).code == 0.0)
+    assert np.all(ob.infer_code(rng.normal(size=8), d, shape, ob.CodingConfig(beta=1e6)).code == 0.0)
+
+
+def test_reconstruct_matches_oracle(golden):
+    g = golden("code_2d")
+    shape = _shape(g)
+    rec = ob.reconstruct(g["dict_freq"], g["code"], shape)
+    H, W = hw(g["dims"])
+    want = O.reconstruction(cols_to_planes(g["dict_freq"], g["dims"]), cols_to_planes(g["code"], g["dims"]))
+    assert np.abs(rec - want.ravel()).max() < 1e-12
+
+
+# ----------------------------------------------------------------- history --
+
+def test_history_sequence_matches_reference(golden):
+    g = golden("history")
+    shape = _shape(g)
+    h = ob.empty_history(shape, int(g["K"]), rho=float(g["rho"]))
+    for i in range(len(g["z"])):
+        ob.update_history(h, g["z"][i], g["x"][i])
+        assert h.count == i + 1
+        assert np.abs(h.cross - g["cross"][i]).max() < 1e-13
+        assert np.abs(h.inv_gram - g["inv"][i]).max() < 1e-12
+    h2 = ob.empty_history(ob.SignalShape((5,), (2,)), 2, rho=0.8)
+    for zc, xc in zip(g["zc"], g["xc"]):
+        ob.update_history(h2, zc, xc)
+    assert np.abs(h2.inv_gram - g["inv_c"]).max() < 1e-12
+    assert np.abs(h2.cross - g["cross_c"]).max() < 1e-13
+
+
+def test_history_first_update_zero_code_and_nonfinite_rejection():
+    shape = ob.SignalShape((4,), (2,))
+    h = ob.empty_history(shape, 3, rho=2.0)
+    ob.update_history(h, np.zeros((4, 3), complex), ob.forward_dft(np.ones(4), shape))
+    assert np.abs(h.inv_gram - np.eye(3) / 8.0).max() < 1e-14
+    before, nbytes = h.cross.copy(), h.nbytes
+    bad = np.ones((4, 3), complex)
+    bad[0, 0] = np.nan
+    with pytest.raises(ob.DivergenceError):
+        ob.update_history(h, bad, np.ones(4, complex))
+    assert h.count == 1 and np.array_equal(h.cross, before) and h.nbytes == nbytes
+
+
+def test_batch_history_equals_streaming(golden):
+    g = golden("history")
+    shape = _shape(g)
+    hb = ob.batch_history(g["z"], g["x"], shape, rho=float(g["rho"]))
+    assert hb.count == len(g["z"])
+    assert np.abs(hb.inv_gram - g["inv"][-1]).max() < 1e-12
+
+
+# -------------------------------------------------------------- dictionary --
+
+def test_update_dictionary_matches_reference(golden):
+    g = golden("dictionary")
+    shape = _shape(g)
+    h = ob.empty_history(shape, int(g["K"]), rho=float(g["rho"]))
+    for z, x in zip(g["z"], g["x"]):
+        ob.update_history(h, z, x)
+    d0 = ob.dict_state_from_filters(g["filters"], shape)
+    rounds = []
+    d1 = ob.update_dictionary(d0, h, 5, monitor=lambda t, f, v: rounds.append(f))
+    assert rel(d1.freq, g["freq"]) < TOL64
+    assert rel(d1.v, g["v"]) < TOL64
+    assert rel(d1.dual, g["dual"]) < TOL64
+    for a, b in zip(rounds, g["rounds"]):
+        assert rel(a, b) < TOL64
+    rows = ob.solve_dict_rows(h, g["rows_v"], g["rows_dual"])
+    assert rel(rows, g["rows"]) < TOL64
+    assert ob.update_dictionary(d0, h, 0) is d0
+    with pytest.raises(ob.UninitializedHistoryError):
+        ob.update_dictionary(d0, ob.empty_history(shape, int(g["K"])), 3)
+
+
+# ----------------------------------------------------------------- trainer --
+
+def _cfg(g, **kw):
+    return ob.TrainConfig(n_filters=int(g["K"]), beta=float(g["beta"]), rho_code=float(g["rho_code"]),
+                          rho_dict=float(g["rho_dict"]), inner_iters=int(g["inner_iters"]),
+                          seed=int(g["seed"]), code_max_iters=int(g["code_max_iters"]),
+                          code_rel_tol=float(g["code_rel_tol"]), **kw)
+
+
+@pytest.mark.parametrize("name", ["train_2d", "train_odd"])
+def test_trainer_steps_match_reference(golden, name):
+    g = golden(name)
+    shape = _shape(g)
+    tr = ob.OnlineTrainer(shape, _cfg(g))
+    for i, x in enumerate(g["X"]):
+        st = tr.step(x)
+        assert st.iterations == int(g["iterations"][i])
+        assert abs(tr.last_objective - g["objectives"][i]) <= TOL64 * abs(g["objectives"][i])
+        assert rel(st.code, g["codes"][i]) < TOL64
+    assert rel(tr.final_filters(), g["final_filters"]) < TOL64
+    assert rel(tr.coding_filters(), g["coding_filters"]) < TOL64
+    assert rel(tr.working_freq, g["working_freq"]) < TOL64
+    assert rel(tr.history.cross, g["cross"]) < TOL64
+    assert rel(tr.history.inv_gram, g["inv_gram"]) < TOL64
+    assert abs(tr.dict_change - float(g["dict_change"])) <= 1e-9 * max(1.0, abs(float(g["dict_change"])))
+
+
+def test_minibatch_matches_composed_reference(golden):
+    g = golden("minibatch")
+    shape = _shape(g)
+    tr = ob.OnlineTrainer(shape, _cfg(g, batch_size=int(g["B"])))
+    B = int(g["B"])
+    objs, codes = [], []
+    for m in range(len(g["X"]) // B):
+        res = tr.partial_fit(g["X"][m * B:(m + 1) * B])
+        objs.extend(res.objectives)
+        codes.extend(res.codes.reshape(B, tr.K, -1).cpu().numpy().transpose(0, 2, 1))
+    assert np.allclose(objs, g["objectives"], rtol=TOL64, atol=0)
+    for a, b in zip(codes, g["codes"]):
+        assert rel(a, b) < TOL64
+    assert rel(tr.final_filters(), g["final_filters"]) < TOL64
+
+
+def test_train_online_matches_reference(golden):
+    g = golden("train_online")
+    shape = _shape(g)
+    cfg = ob.TrainConfig(n_filters=2, beta=0.5, seed=3, max_passes=3, stop_tol=1e-12, inner_iters=5,
+                         code_max_iters=100)
+    rep = ob.train_online(g["X"], shape, cfg)
+    assert np.allclose([r.train_obj for r in rep.records], g["train_obj"], rtol=TOL64)
+    assert rel(rep.filters, g["filters"]) < TOL64
+    cfg2 = ob.TrainConfig(n_filters=2, beta=0.5, seed=3, max_passes=5, stop_tol=0.5, inner_iters=5,
+                          code_max_iters=100)
+    rep2 = ob.train_online(g["X"], shape, cfg2)
+    assert rep2.stopped_early == bool(g["stopped2"])
+    assert np.allclose([r.train_obj for r in rep2.records], g["train_obj2"], rtol=TOL64)
+    assert len(set(r.history_bytes for r in rep.records)) == 1
+
+
+def test_empty_stream_returns_init():
+    shape = ob.SignalShape((16,), (3,))
+    cfg = ob.TrainConfig(n_filters=2, seed=5)
+    rep = ob.train_online(np.empty((0, 16)), shape, cfg)
+    assert rep.records == [] and not rep.stopped_early
+    assert np.array_equal(rep.filters, ob.init_dictionary(shape, 2, 5))
+
+
+def test_online_bitwise_repeatable():
+    shape = ob.SignalShape((12, 12), (3, 3))
+    X = O.synth_images(4, (12, 12), (12, 12), 2, filter_dims=(3, 3), seed=4, density=0.05).reshape(4, -1)
+    cfg = ob.TrainConfig(n_filters=3, beta=0.5, seed=3, max_passes=2, stop_tol=1e-12, inner_iters=3,
+                         code_max_iters=40, batch_size=2)
+    a, b = ob.train_online(X, shape, cfg), ob.train_online(X, shape, cfg)
+    assert [r.train_obj for r in a.records] == [r.train_obj for r in b.records]
+    assert np.array_equal(a.filters, b.filters)
+
+
+# ------------------------------------------------------- BASELINE configs --
+
+@pytest.mark.slow
+def test_config0_full_size_float64(golden):
+    """BASELINE config 0 at full size: 100x100, K=100, f64, B=1 -- 1e-9 vs the reference."""
+    g = golden("cfg0")
+    shape = ob.SignalShape((100, 100), (11, 11))
+    cfg = ob.TrainConfig(n_filters=100, beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0)
+    tr = ob.OnlineTrainer(shape, cfg)
+    st = tr.step(g["X"][0])
+    assert st.iterations == int(g["iterations"][0])
+    assert abs(tr.last_objective - g["objectives"][0]) <= TOL64 * abs(g["objectives"][0])
+    code = np.zeros(shape.size * 100)
+    code[g["code_idx"]] = g["code_val"]
+    assert rel(st.code.ravel(), code) < TOL64
+    assert rel(tr.final_filters(), g["final_filters"]) < TOL64
+    assert rel(tr.coding_filters(), g["coding_filters"]) < TOL64
+
+
+def test_float32_prefix_config1_shape():
+    """Config-1 geometry (32x32 padded to 42x42, K=100) in float32 vs the float64 oracle on a prefix."""
+    c = O.CONFIGS[1]
+    B, nb = 4, 2
+    X = O.synth_images(B * nb, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B * nb, -1)
+    kw = dict(beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0, code_max_iters=300)
+    ora = O.Trainer(c["grid"], (11, 11), K=100, **kw)
+    shape = ob.SignalShape(c["grid"], (11, 11))
+    tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=100, dtype="float32", history_dtype="float64",
+                                                batch_size=B, stop_tol=0.0, **kw))
+    for m in range(nb):
+        want = [o for _, o in ora.step_batch(X[m * B:(m + 1) * B])]
+        got = tr.partial_fit(X[m * B:(m + 1) * B]).objectives
+        assert np.max(np.abs(np.asarray(got) - want) / np.abs(want)) < 1e-4
+    assert rel(tr.final_filters(), ora.final_filters()) < 1e-3
+    assert rel(tr.coding_filters(), ora.coding_filters()) < 1e-3
+
+
+def test_evaluate_dictionary_psnr():
+    shape = ob.SignalShape((16, 16), (3, 3))
+    X = O.synth_images(3, (16, 16), (16, 16), 2, filter_dims=(3, 3), seed=2, density=0.05).reshape(3, -1)
+    f = ob.init_dictionary(shape, 4, 1)
+    res = ob.evaluate_dictionary(f, X, shape, ob.CodingConfig(beta=0.2))
+    dh = O.fwd(O.pad(f, 16, 16, 3, 3))
+    objs, ps = [], []
+    for x in X:
+        st = O.code_admm(x, dh, 0.2, 1.0, 300, 1e-3)
+        objs.append(O.objective(x, dh, st["code"], 0.2))
+        err = ((x.reshape(16, 16) - O.reconstruction(dh, st["code"])) ** 2).sum()
+        ps.append(10 * np.log10(255.0 ** 2 * 256 / err))
+    assert abs(res.test_objective - np.mean(objs)) < 1e-9 * abs(np.mean(objs))
+    assert abs(res.psnr - np.mean(ps)) < 1e-9 * abs(np.mean(ps))
