@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py -- OCSC training images/sec on B200 (BASELINE.json metric), one JSON line.
+
+Workload (BASELINE.json configs[1]): seeded synthetic 32x32
+images zero-padded to 42x42, K = 100 filters of 11x11, beta = 1,
+rho_code = rho_dict = 1, J = 10 dictionary rounds, <= 300 code iterations,
+float32 arithmetic (float64 history), mini-batch 50 per GPU.  A step is one
+mini-batch through the whole hot path: batched code ADMM -> objective ->
+history fold -> Cholesky -> J dictionary rounds.
+
+    python bench.py [--gpus N --steps K --warmup W]            # this build
+    python bench.py --impl reference [--steps K --warmup W]    # CPU reference arm
+    torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1: sample-sharded
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events
+on the trainer's stream, L2 flushed (256 MiB write) between steps outside the
+events, barrier + synchronize around the block, max over ranks.  `value` has
+the inputs already resident in HBM; `e2e` runs the public API
+(`OnlineTrainer.partial_fit`) on pinned host arrays, H2D of the images and
+D2H of the per-sample objectives inside the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "OCSC training images/sec at 1/2/4/8 B200; % of HBM/FP32 roofline per kernel"
+UNIT = "images/s"
+CFG = dict(dims0=(32, 32), grid=(42, 42), fdims=(11, 11), K0=20, K=100, beta=1.0, rho_code=1.0, rho_dict=1.0,
+           J=10, max_iters=300, rel_tol=1e-3, B=50)
+WORKLOAD = ("BASELINE config 1: seeded synthetic 32x32 images zero-padded to 42x42, K=100 filters 11x11, "
+            "beta=1, rho=1, J=10, <=300 code iterations, float32 (history float64), mini-batch 50 per GPU")
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def make_images(n, start, seed=0):
+    from oracle import ocsc_oracle as O  # bench input generator; not the measured path
+    return O.synth_images(n, CFG["dims0"], CFG["grid"], CFG["K0"], filter_dims=CFG["fdims"], seed=seed,
+                          start=start).reshape(n, -1)
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- CPU legs --
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_oracle_rate(n_images, budget_s=None, warmup=0):
+    """Images/s of the CPU reference algorithm (oracle port, composed mini-batch of 1) on config 1."""
+    from oracle import ocsc_oracle as O
+    tr = O.Trainer(CFG["grid"], CFG["fdims"], K=CFG["K"], beta=CFG["beta"], rho_code=CFG["rho_code"],
+                   rho_dict=CFG["rho_dict"], inner_iters=CFG["J"], seed=0, code_max_iters=CFG["max_iters"],
+                   code_rel_tol=CFG["rel_tol"], stop_tol=0.0)
+    X = make_images(n_images + warmup, start=10_000_000)
+    for i in range(warmup):
+        tr.step_batch(X[i:i + 1])
+    done, t0 = 0, time.perf_counter()
+    for i in range(warmup, warmup + n_images):
+        tr.step_batch(X[i:i + 1])
+        done += 1
+        if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return done / dt, done, dt
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    budget = float(os.environ.get("OCSC_REF_BUDGET_S", "150"))
+    rate, done, dt = cpu_oracle_rate(args.steps, budget_s=budget, warmup=min(args.warmup, 1))
+    cores = cpu_threads()
+    sample = (f"{done} timed step(s) of 1 image each of config 1 (reference OnlineTrainer.step semantics, "
+              f"oracle/ocsc_oracle.py numpy port), {dt:.1f} s; warm-up {min(args.warmup, 1)} step")
+    line = {"metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * dt / max(done, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded planted-dictionary images, SURVEY.md 8(d))",
+            "config": {"workload": WORKLOAD, "global_batch": 1, "parallelism": "cpu"},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU legs --
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1706_06972_b200 as ob
+    from paper_1706_06972_b200 import _lib
+    from paper_1706_06972_b200.coding import infer_codes
+    from paper_1706_06972_b200.parallel import DistributedTrainer
+    from paper_1706_06972_b200.transforms import rfft2_dev
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    lib = _lib.load()
+    B = args.batch
+    shape = ob.SignalShape(CFG["grid"], CFG["fdims"])
+    cfg = ob.TrainConfig(n_filters=CFG["K"], beta=CFG["beta"], rho_code=CFG["rho_code"], rho_dict=CFG["rho_dict"],
+                         inner_iters=CFG["J"], seed=0, code_max_iters=CFG["max_iters"], code_rel_tol=CFG["rel_tol"],
+                         dtype="float32", history_dtype="float64", batch_size=B, stop_tol=0.0, poll=16)
+    Trainer = (lambda: DistributedTrainer(shape, cfg)) if world > 1 else (lambda: ob.OnlineTrainer(shape, cfg))
+    nsteps = args.warmup + args.steps
+    P = shape.size
+    # rank r owns rows [r*B, (r+1)*B) of each global mini-batch of world*B images
+    X = np.stack([make_images(B, start=(s * world + rank) * B) for s in range(nsteps)]).astype(np.float32)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+
+    # ---- value: inputs resident in HBM, device-timed --------------------------------
+    trainer = Trainer()
+    Xd = torch.as_tensor(X).to(dev)
+    for s in range(args.warmup):
+        trainer.partial_fit(Xd[s])
+    torch.cuda.synchronize()
+    barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.4)
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = lib.ocsc_kernel_launches()
+    torch.cuda.synchronize()
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        evs[i][0].record(stream)
+        res = trainer.partial_fit(Xd[args.warmup + i])
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = lib.ocsc_kernel_launches() - launches0
+    clocks = sampler.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    total_ms = max_over_ranks(total_ms)
+    value = world * B * args.steps / (total_ms / 1e3)
+    iters_mean = float(np.mean(res.iterations))
+
+    # ---- roofline of the dominant kernel: one code-ADMM iteration over the batch ----
+    buf = trainer._buf
+    xh = rfft2_dev(Xd[0].reshape(B, *CFG["grid"]), shape)
+    reps = 3
+    durs = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        infer_codes(xh, trainer.Wh, trainer.den, shape, trainer.coding_config, buf, B, poll=0)
+        b.record(stream)
+        torch.cuda.synchronize()
+        durs.append(a.elapsed_time(b) / max(int(buf.iters[:B].max().item()), 1))
+    it_ms = min(durs)
+    H, W = CFG["grid"]
+    Pf, Ph, K, s = H * W, H * (W // 2 + 1), CFG["K"], 4
+    bytes_per_img_iter = 8 * Pf * K * s + 8 * Ph * K * s          # SURVEY.md 8(d) G1-G4, algorithmic
+    achieved = B * bytes_per_img_iter / (it_ms / 1e3) / 1e9       # GB/s
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get("code_admm_iter_bytes")
+    except (OSError, ValueError):
+        pass
+
+    # ---- e2e: public API, pinned host input, objectives back to host -----------------
+    trainer2 = Trainer()
+    Xh = torch.as_tensor(X).pin_memory()
+    for s in range(args.warmup):
+        trainer2.partial_fit(Xh[s])
+    torch.cuda.synchronize()
+    barrier()
+    e2e_s = 0.0
+    for i in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r2 = trainer2.partial_fit(Xh[args.warmup + i])
+        _ = float(r2.objectives.sum())
+        e2e_s += time.perf_counter() - t0
+    barrier()
+    e2e_s = max_over_ranks(e2e_s)
+    e2e = world * B * args.steps / e2e_s
+
+    # ---- CPU baseline (rank 0, N = 1 only) -------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n = int(os.environ.get("OCSC_CPU_SAMPLE_IMAGES", "2"))
+        rate, done, dt = cpu_oracle_rate(n)
+        cpu = {"value": rate, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+               "sample": f"{done} images of config 1 through oracle/ocsc_oracle.py (reference algorithm, "
+                         f"OnlineTrainer.step semantics, float64), {dt:.1f} s on host cores"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded planted-dictionary images, SURVEY.md 8(d))",
+                "config": {"workload": WORKLOAD, "global_batch": world * B, "per_gpu_batch": B,
+                           "code_iterations_mean": iters_mean,
+                           "l2": "flushed between timed steps (256 MiB device write outside the events)",
+                           "parallelism": f"dp{world} (sample-sharded coding, all-gathered code spectra, "
+                                          f"replicated dictionary)"},
+                "roofline": {"bound": "hbm", "kernel": "code-ADMM iteration (R2C + residual + C2R + update "
+                                                       "+ decide) over the mini-batch",
+                             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                             "traffic": traffic, "iter_ms": it_ms,
+                             "algorithmic_bytes_per_image_iter": bytes_per_img_iter,
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * P * 4,
+                        "d2h_bytes_per_step": (2 * B + 4) * 8},
+                "gpu_launches": int(launches), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=CFG["B"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

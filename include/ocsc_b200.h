@@ -49,6 +49,8 @@ extern "C" {
 
 const char* ocsc_last_error(void);
 int ocsc_abi_version(void);
+/* Number of this library's own kernels enqueued so far in the process (cuFFT's excluded). */
+int64_t ocsc_kernel_launches(void);
 
 /* ------------------------------------------------------------ transforms --
  * transforms.py:82-87, 148-158 (forward_dft[_cols]); :90-109, 161-176

@@ -29,6 +29,7 @@ _I, _I64, _D, _P, _SZ = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_
 SIGNATURES = {
     "ocsc_last_error": [],
     "ocsc_abi_version": [],
+    "ocsc_kernel_launches": [],
     "ocsc_rfft2": [_I, _I, _I, _I, _P, _P, _P],
     "ocsc_irfft2": [_I, _I, _I, _I, _P, _P, _P],
     "ocsc_dft_cols": [_I, _I, _I, _I, _P, _I, _P, _I, _P],
@@ -55,7 +56,8 @@ SIGNATURES = {
     "ocsc_support_rfft": [_I, _I, _I, _I, _I, _I, _P, _P, _P],
     "ocsc_norms2": [_I, _I64, _P, _P, _P, _P],
 }
-_RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ}
+_RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ,
+             "ocsc_kernel_launches": ctypes.c_int64}
 
 _lib = None
 

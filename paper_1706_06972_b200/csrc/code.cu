@@ -292,6 +292,7 @@ static int code_admm_impl(int dtype, int H, int W, int K, int B, const void* xh,
       k_update<T, false><<<ugrid, 256, 0, s>>>(n, invP, kappa, (T*)u, (T*)t, (const T*)w.cbuf, nullptr, flags,
                                                 flags + B, flags + 2 * B, w.acc);
     k_decide<<<1, 256, 0, s>>>(B, rel_tol, w.acc, flags, iters, status);
+    count_launches(3);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { rc = cuda_fail(e, "code ADMM launch"); break; }
     if (host && it % poll == 0 && it < max_iters) {
@@ -379,6 +380,7 @@ extern "C" int ocsc_code_objective(int dtype, int H, int W, int K, int B, const 
   } else {
     return fail(OCSC_EARG, "dtype must be 4 or 8");
   }
+  count_launches(1);  // two kernels above
   OCSC_LAUNCHED("k_obj");
   return OCSC_OK;
 }

@@ -18,6 +18,7 @@ namespace ocsc {
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
+void count_launches(int n);  // kernels of this library enqueued (ocsc_kernel_launches)
 
 #define OCSC_CUDA(call)                                   \
   do {                                                    \
@@ -27,6 +28,7 @@ int cuda_fail(cudaError_t e, const char* where);
 
 #define OCSC_LAUNCHED(name)                                              \
   do {                                                                   \
+    ::ocsc::count_launches(1);                                           \
     cudaError_t e__ = cudaGetLastError();                                \
     if (e__ != cudaSuccess) return ::ocsc::cuda_fail(e__, name);         \
   } while (0)

@@ -231,6 +231,24 @@ class OnlineTrainer:
                   _lib.ptr(self.den), s)
 
     # -------------------------------------------------------------- API --
+    def _fold(self, uh: torch.Tensor, xh: torch.Tensor, B: int) -> None:
+        """History += this mini-batch (overridden by the distributed trainer)."""
+        nf = self.nf
+        self.history.accumulate(uh, (self.K * nf, nf, 1), xh, (nf, 1), B)
+
+    def _track_changes(self, last: torch.Tensor) -> None:
+        """Device partial sums of code_change / dict_change (training.py:146-154)."""
+        self._metrics.zero_()
+        if self._prev_code is not None:
+            _lib.call("ocsc_norms2", _lib.code(self.dtype), last.numel(), _lib.ptr(last),
+                      _lib.ptr(self._prev_code), _lib.ptr(self._metrics), _lib.stream())
+            self._prev_code.copy_(last)
+        else:
+            self._prev_code = last.clone()
+        _lib.call("ocsc_norms2", _lib.code(self.dtype), self.alpha.numel(), _lib.ptr(self.alpha),
+                  _lib.ptr(self._prev_alpha), _lib.ptr(self._metrics[2:]), _lib.stream())
+        self._prev_alpha.copy_(self.alpha)
+
     def partial_fit(self, X, want_z: bool = False, check: bool = True) -> BatchResult:
         """One mini-batch of B samples (rows of X, each P entries) through the hot path.
 
@@ -251,31 +269,22 @@ class OnlineTrainer:
                 raise DivergenceError(f"code solver diverged at iteration {it}")
         uh = self._uh[:B]
         obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
-        nf = self.nf
-        self.history.accumulate(uh, (self.K * nf, nf, 1), xh, (nf, 1), B)
+        self._fold(uh, xh, B)
         self._dictionary_update()
         track = self.config.stop_tol > 0
         if track:
-            self._metrics.zero_()
-            last = buf.u[B - 1]
-            if self._prev_code is not None:
-                _lib.call("ocsc_norms2", _lib.code(self.dtype), last.numel(), _lib.ptr(last),
-                          _lib.ptr(self._prev_code), _lib.ptr(self._metrics), _lib.stream())
-                self._prev_code.copy_(last)
-            else:
-                self._prev_code = last.clone()
-            _lib.call("ocsc_norms2", _lib.code(self.dtype), self.alpha.numel(), _lib.ptr(self.alpha),
-                      _lib.ptr(self._prev_alpha), _lib.ptr(self._metrics[2:]), _lib.stream())
-            self._prev_alpha.copy_(self.alpha)
+            self._track_changes(buf.u[B - 1])
         host = torch.cat([obj, buf.iters[:B].double(), self._metrics]).cpu().numpy()
         objectives, iterations = host[:B], host[B:2 * B].astype(np.int64)
         if track:
-            m = host[2 * B:]
-            if self.history.count > B:
-                self.code_change = float(np.sqrt(m[0]) / max(np.sqrt(m[1]), 1e-12))
-            self.dict_change = float(np.sqrt(m[2]) / max(np.sqrt(m[3]), 1e-12))
+            self._set_changes(host[2 * B:], B)
         self.last_objective = float(objectives[-1])
         return BatchResult(objectives=objectives, iterations=iterations, codes=buf.u[:B])
+
+    def _set_changes(self, m: np.ndarray, B: int) -> None:
+        if self.history.count > B:
+            self.code_change = float(np.sqrt(m[0]) / max(np.sqrt(m[1]), 1e-12))
+        self.dict_change = float(np.sqrt(m[2]) / max(np.sqrt(m[3]), 1e-12))
 
     def step(self, x) -> CodeState:
         """Code one sample, absorb it, refresh the dictionary (training.py:128-155)."""
