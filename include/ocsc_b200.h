@@ -105,6 +105,18 @@ int ocsc_code_admm(int dtype, int H, int W, int K, int B, const void* xh, const 
                    const void* den, double beta, double rho, int max_iters, double rel_tol,
                    void* u, void* t, void* zh, void* work, int32_t* iters, int32_t* status,
                    int poll, void* stream);
+/* Fused on-chip code ADMM (cold start) + objective for grids with an instantiated
+ * kernel: one thread-block cluster per sample keeps the ADMM state in shared memory
+ * for every iteration; the cluster exchanges the partial synthesis through DSMEM.
+ * Outputs u (B,K,H,W) = code U, t (optional) = U - Gamma, uh (B,K,nfreq) = rfft2(U),
+ * obj/resid as ocsc_code_objective, iters/status as ocsc_code_admm.  Same
+ * stopping semantics as ocsc_code_admm.  ocsc_code_fused_cluster returns the cluster
+ * size the launch would use, or 0 when (dtype, H, W, K) is not supported. */
+int ocsc_code_fused_cluster(int dtype, int H, int W, int K, int B);
+int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
+                    const void* den, double beta, double rho, int max_iters, double rel_tol,
+                    void* u, void* t, void* uh, double* obj, double* resid, int32_t* iters,
+                    int32_t* status, void* stream);
 /* coding.py:122-134 for B codes: uh = rfft2(u) (B, K, nfreq) and
  * obj[b] = 0.5 ||x_b - sum_k w_k (*) u_bk||^2 + beta ||u_b||_1 (double, device);
  * resid[b] (optional) = ||x_b - reconstruction||^2 (evaluate.py:55-62 PSNR input). */

@@ -1,0 +1,162 @@
+// Register-resident small FFTs with compile-time length and compile-time twiddles.
+//
+// fft<C, N, INV>(x) transforms x[0..N) held in registers (N known at compile
+// time): mixed-radix decimation in time on the smallest prime factor, prime
+// lengths by the symmetric direct DFT.  Every index and every twiddle is a
+// compile-time constant, so after unrolling the transform is straight-line
+// FFMA code with immediate operands -- no shared-memory twiddle loads.
+// Forward uses e^{-2 pi i jk/N}, inverse e^{+2 pi i jk/N}, both unnormalised.
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace ocsc {
+namespace sfft {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+__host__ __device__ constexpr double reduce_angle(double x) {
+  // to [-pi, pi]
+  const double two_pi = 2.0 * kPi;
+  long long n = (long long)(x / two_pi + (x >= 0 ? 0.5 : -0.5));
+  return x - (double)n * two_pi;
+}
+
+__host__ __device__ constexpr double ce_sin(double x) {
+  x = reduce_angle(x);
+  double term = x, sum = x;
+  for (int n = 1; n < 30; ++n) {
+    term *= -x * x / ((2.0 * n) * (2.0 * n + 1.0));
+    sum += term;
+  }
+  return sum;
+}
+
+__host__ __device__ constexpr double ce_cos(double x) {
+  x = reduce_angle(x);
+  double term = 1.0, sum = 1.0;
+  for (int n = 1; n < 30; ++n) {
+    term *= -x * x / ((2.0 * n - 1.0) * (2.0 * n));
+    sum += term;
+  }
+  return sum;
+}
+
+__host__ __device__ constexpr int smallest_factor(int n) {
+  for (int f = 2; f * f <= n; ++f)
+    if (n % f == 0) return f;
+  return n;
+}
+
+template <int Begin, int End, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (Begin < End) {
+    f(std::integral_constant<int, Begin>{});
+    static_for<Begin + 1, End>(f);
+  }
+}
+
+// v * e^{(INV ? +1 : -1) 2 pi i E / N}
+template <typename C, int N, int E, bool INV>
+__device__ __forceinline__ C twiddle(C v) {
+  using T = decltype(C::x);
+  constexpr int e = E % N;
+  if constexpr (e == 0) {
+    return v;
+  } else if constexpr (4 * e == N) {  // -i (fwd) / +i (inv)
+    return INV ? mkc<C>(-v.y, v.x) : mkc<C>(v.y, -v.x);
+  } else if constexpr (2 * e == N) {
+    return mkc<C>(-v.x, -v.y);
+  } else if constexpr (4 * e == 3 * N) {
+    return INV ? mkc<C>(v.y, -v.x) : mkc<C>(-v.y, v.x);
+  } else {
+    constexpr T c = (T)ce_cos(2.0 * kPi * e / N);
+    constexpr T s = (T)((INV ? 1.0 : -1.0) * ce_sin(2.0 * kPi * e / N));
+    return mkc<C>(v.x * c - v.y * s, v.x * s + v.y * c);
+  }
+}
+
+// direct DFT of prime length R (R = 2 butterfly; odd R with the j <-> R-j pairing)
+template <typename C, int R, bool INV>
+__device__ __forceinline__ void dft_prime(C (&x)[R]) {
+  using T = decltype(C::x);
+  if constexpr (R == 1) {
+    return;
+  } else if constexpr (R == 2) {
+    const C a = x[0], b = x[1];
+    x[0] = mkc<C>(a.x + b.x, a.y + b.y);
+    x[1] = mkc<C>(a.x - b.x, a.y - b.y);
+  } else {
+    constexpr int Hh = (R - 1) / 2;
+    C s[Hh], d[Hh];
+    const C x0 = x[0];
+    C sum = x0;
+    static_for<1, Hh + 1>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      s[j - 1] = mkc<C>(x[j].x + x[R - j].x, x[j].y + x[R - j].y);
+      d[j - 1] = mkc<C>(x[j].x - x[R - j].x, x[j].y - x[R - j].y);
+      sum.x += s[j - 1].x;
+      sum.y += s[j - 1].y;
+    });
+    static_for<1, Hh + 1>([&](auto Kk) {
+      constexpr int k = decltype(Kk)::value;
+      C a = x0;
+      T bx = 0, by = 0;
+      static_for<1, Hh + 1>([&](auto J) {
+        constexpr int j = decltype(J)::value;
+        constexpr T c = (T)ce_cos(2.0 * kPi * ((j * k) % R) / R);
+        constexpr T sn = (T)ce_sin(2.0 * kPi * ((j * k) % R) / R);
+        a.x = fma(s[j - 1].x, c, a.x);
+        a.y = fma(s[j - 1].y, c, a.y);
+        bx = fma(d[j - 1].x, sn, bx);
+        by = fma(d[j - 1].y, sn, by);
+      });
+      // forward: X[k] = a - i*b, X[R-k] = a + i*b (b = sum d_j sin); inverse swaps
+      if constexpr (!INV) {
+        x[k] = mkc<C>(a.x + by, a.y - bx);
+        x[R - k] = mkc<C>(a.x - by, a.y + bx);
+      } else {
+        x[k] = mkc<C>(a.x - by, a.y + bx);
+        x[R - k] = mkc<C>(a.x + by, a.y - bx);
+      }
+    });
+    x[0] = sum;
+  }
+}
+
+template <typename C, int N, bool INV>
+__device__ __forceinline__ void fft(C (&x)[N]) {
+  constexpr int R = smallest_factor(N);
+  if constexpr (R == N) {
+    dft_prime<C, N, INV>(x);
+  } else {
+    constexpr int M = N / R;
+    C sub[R][M];
+    static_for<0, R>([&](auto Rr) {
+      constexpr int r = decltype(Rr)::value;
+      static_for<0, M>([&](auto Mm) {
+        constexpr int m = decltype(Mm)::value;
+        sub[r][m] = x[m * R + r];
+      });
+      fft<C, M, INV>(sub[r]);
+    });
+    static_for<0, M>([&](auto Kk) {
+      constexpr int k = decltype(Kk)::value;
+      C tmp[R];
+      static_for<0, R>([&](auto Rr) {
+        constexpr int r = decltype(Rr)::value;
+        tmp[r] = twiddle<C, N, r * k, INV>(sub[r][k]);
+      });
+      dft_prime<C, R, INV>(tmp);
+      static_for<0, R>([&](auto Q) {
+        constexpr int q = decltype(Q)::value;
+        x[k + M * q] = tmp[q];
+      });
+    });
+  }
+}
+
+}  // namespace sfft
+}  // namespace ocsc

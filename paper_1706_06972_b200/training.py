@@ -57,6 +57,7 @@ class TrainConfig:
     dtype: str = "float64"         # code/dictionary arithmetic: float64 (parity) or float32
     history_dtype: str = "float64" # history sums and Cholesky
     poll: int = 16                 # code-ADMM convergence poll interval (iterations)
+    fused: bool = True             # on-chip cluster kernel when the grid has one (else cuFFT path)
 
     def coding(self) -> CodingConfig:
         return CodingConfig(beta=self.beta, rho=self.rho_code, max_iters=self.code_max_iters,
@@ -185,6 +186,8 @@ class OnlineTrainer:
         self._buf = None
         self._uh = None
         self._x = None
+        self._obj = None
+        self._fused_ok = {}
 
     # ---------------------------------------------------------- internals --
     def _support_rfft(self, alpha: torch.Tensor, out: torch.Tensor) -> None:
@@ -196,7 +199,18 @@ class OnlineTrainer:
             self._buf = CodeBuffers(self.shape, self.K, B, self.dtype, want_z=want_z)
             self._uh = torch.empty((B, self.K, self.H, self.W // 2 + 1), dtype=self.cdtype, device=self.dev)
             self._x = torch.empty((B, self.H, self.W), dtype=self.dtype, device=self.dev)
+            self._obj = torch.empty(B, dtype=torch.float64, device=self.dev)
         return self._buf
+
+    def use_fused(self, B: int) -> bool:
+        """True when the on-chip cluster kernel covers this grid/dtype (ocsc_code_fused_cluster)."""
+        if not self.config.fused:
+            return False
+        key = (B,)
+        if key not in self._fused_ok:
+            self._fused_ok[key] = _lib.load().ocsc_code_fused_cluster(_lib.code(self.dtype), self.H, self.W,
+                                                                      self.K, B) > 0
+        return self._fused_ok[key]
 
     def _load(self, X) -> tuple[torch.Tensor, int]:
         P = self.shape.size
@@ -261,14 +275,24 @@ class OnlineTrainer:
         x = self._x[:B]
         x.copy_(xs, non_blocking=True)
         xh = rfft2_dev(x, self.shape)
-        infer_codes(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
+        uh = self._uh[:B]
+        fused = self.use_fused(B) and not want_z
+        if fused:
+            obj = self._obj[:B]
+            cc = self.coding_config
+            _lib.call("ocsc_code_fused", _lib.code(self.dtype), self.H, self.W, self.K, B, _lib.ptr(xh),
+                      _lib.ptr(self.Wh), _lib.ptr(self.den), cc.beta, cc.rho, cc.max_iters, cc.rel_tol,
+                      _lib.ptr(buf.u), None, _lib.ptr(uh), _lib.ptr(obj), None, _lib.ptr(buf.iters),
+                      _lib.ptr(buf.status), _lib.stream())
+        else:
+            infer_codes(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
         if check:
             status = buf.status[:B].cpu()
             if bool((status == 2).any()):
                 it = int(buf.iters[:B][status.to(buf.iters.device) == 2].min().cpu())
                 raise DivergenceError(f"code solver diverged at iteration {it}")
-        uh = self._uh[:B]
-        obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
+        if not fused:
+            obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
         self._fold(uh, xh, B)
         self._dictionary_update()
         track = self.config.stop_tol > 0

@@ -321,3 +321,87 @@ def test_evaluate_dictionary_psnr():
         ps.append(10 * np.log10(255.0 ** 2 * 256 / err))
     assert abs(res.test_objective - np.mean(objs)) < 1e-9 * abs(np.mean(objs))
     assert abs(res.psnr - np.mean(ps)) < 1e-9 * abs(np.mean(ps))
+
+
+# ------------------------------------------------------ fused cluster kernel --
+
+def test_fused_kernel_is_selected_for_config1():
+    shape = ob.SignalShape((42, 42), (11, 11))
+    tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=100, dtype="float32", batch_size=50))
+    assert tr.use_fused(50)
+    from paper_1706_06972_b200 import _lib
+    assert _lib.load().ocsc_code_fused_cluster(4, 42, 42, 100, 50) in (2, 4, 8, 16)
+
+
+def test_fused_minibatch_matches_composed_reference(golden):
+    g = golden("minibatch")
+    shape = _shape(g)
+    B = int(g["B"])
+    tr = ob.OnlineTrainer(shape, _cfg(g, batch_size=B, fused=True))
+    assert tr.use_fused(B)
+    objs, codes = [], []
+    for m in range(len(g["X"]) // B):
+        res = tr.partial_fit(g["X"][m * B:(m + 1) * B])
+        objs.extend(res.objectives)
+        codes.extend(res.codes.reshape(B, tr.K, -1).cpu().numpy().transpose(0, 2, 1))
+    assert np.allclose(objs, g["objectives"], rtol=TOL64, atol=0)
+    for a, b in zip(codes, g["codes"]):
+        assert rel(a, b) < TOL64
+    assert rel(tr.final_filters(), g["final_filters"]) < TOL64
+
+
+def test_fused_single_sample_steps_match_reference(golden):
+    g = golden("train_2d")
+    shape = _shape(g)
+    tr = ob.OnlineTrainer(shape, _cfg(g, fused=True))
+    assert tr.use_fused(1)
+    for i, x in enumerate(g["X"]):
+        res = tr.partial_fit(x)
+        assert int(res.iterations[0]) == int(g["iterations"][i])
+        assert abs(res.objectives[0] - g["objectives"][i]) <= TOL64 * abs(g["objectives"][i])
+        assert rel(res.codes[0].reshape(tr.K, -1).cpu().numpy().T, g["codes"][i]) < TOL64
+    assert rel(tr.final_filters(), g["final_filters"]) < TOL64
+    assert rel(tr.working_freq, g["working_freq"]) < TOL64
+
+
+@pytest.mark.parametrize("dims,K,B", [((16, 16), 7, 5), ((24, 24), 12, 3), ((12, 9), 4, 4), ((20, 20), 33, 2)])
+def test_fused_equals_cufft_path(dims, K, B):
+    shape = ob.SignalShape(dims, (3, 3))
+    X = O.synth_images(2 * B, dims, dims, 3, filter_dims=(3, 3), seed=9, density=0.05).reshape(2 * B, -1)
+    kw = dict(n_filters=K, beta=0.3, rho_code=1.0, rho_dict=1.0, inner_iters=3, seed=2, code_max_iters=80,
+              batch_size=B, stop_tol=0.0)
+    a = ob.OnlineTrainer(shape, ob.TrainConfig(fused=True, **kw))
+    b = ob.OnlineTrainer(shape, ob.TrainConfig(fused=False, **kw))
+    assert a.use_fused(B) and not b.use_fused(B)
+    for m in range(2):
+        ra, rb = a.partial_fit(X[m * B:(m + 1) * B]), b.partial_fit(X[m * B:(m + 1) * B])
+        assert np.array_equal(ra.iterations, rb.iterations)
+        assert np.allclose(ra.objectives, rb.objectives, rtol=1e-11, atol=0)
+        assert rel(ra.codes.cpu().numpy(), rb.codes.cpu().numpy()) < 1e-10
+    assert rel(a.final_filters(), b.final_filters()) < 1e-11
+
+
+def test_fused_float32_matches_oracle_42x42():
+    c = O.CONFIGS[1]
+    B = 6
+    X = O.synth_images(B, c["dims0"], c["grid"], c["K0"], seed=3).reshape(B, -1)
+    kw = dict(beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0, code_max_iters=300)
+    ora = O.Trainer(c["grid"], (11, 11), K=100, **kw)
+    tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)),
+                          ob.TrainConfig(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, **kw))
+    assert tr.use_fused(B)
+    got = tr.partial_fit(X).objectives
+    want = [o for _, o in ora.step_batch(X)]
+    assert np.max(np.abs(np.asarray(got) - want) / np.abs(want)) < 1e-4
+    assert rel(tr.final_filters(), ora.final_filters()) < 1e-3
+
+
+def test_fused_divergence_raises():
+    shape = ob.SignalShape((12, 12), (3, 3))
+    tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=4, batch_size=2))
+    X = np.random.default_rng(0).normal(size=(2, 144))
+    X[1, 5] = np.nan
+    assert tr.use_fused(2)
+    with pytest.raises(ob.DivergenceError, match="iteration"):
+        tr.partial_fit(X)
+    assert tr.history.count == 0
