@@ -113,6 +113,10 @@ int ocsc_code_admm(int dtype, int H, int W, int K, int B, const void* xh, const 
  * stopping semantics as ocsc_code_admm.  ocsc_code_fused_cluster returns the cluster
  * size the launch would use, or 0 when (dtype, H, W, K) is not supported. */
 int ocsc_code_fused_cluster(int dtype, int H, int W, int K, int B);
+/* Launch plan of ocsc_code_fused (host array of 6 int32): cluster size, threads per CTA,
+ * dynamic shared memory bytes, registers per thread, max threads per block, max active
+ * clusters.  Returns the cluster size (0 = unsupported). */
+int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32_t* info);
 int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
                     const void* den, double beta, double rho, int max_iters, double rel_tol,
                     void* u, void* t, void* uh, double* obj, double* resid, int32_t* iters,

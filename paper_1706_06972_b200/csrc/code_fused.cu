@@ -46,38 +46,51 @@ struct FusedArgs {
   int32_t* status;  // (B)
 };
 
-template <int H, int W>
+// Grid N x N with N = 2M, M odd (42 = 2 * 21 for BASELINE config 1).
+//  * a real row of N pixels is one M-point complex FFT of (even, odd) pixel pairs plus a
+//    twiddled real pre/post-processing step: one thread per row, the update of w runs on
+//    the row's values in registers between the inverse and the forward row transform;
+//  * a column (N complex) is the Good-Thomas split N = 2 x M (no twiddles): lanes l and
+//    l^16 each run the M-point FFT of one index parity and finish the 2-point stage with
+//    one butterfly shuffle.
+// Every transform goes through ONE call site of the M-point FFT (inverse = conj o FFT o conj),
+// which keeps the kernel's instruction footprint inside the instruction caches.
+template <int N>
 struct Geo {
-  static constexpr int Wh = W / 2 + 1;
-  static constexpr int WP = (W % 2 == 0) ? W + 1 : W;   // odd row stride of w (bank-conflict free)
-  static constexpr int WhP = (Wh % 2 == 0) ? Wh + 1 : Wh;  // odd complex row stride of the workspace
-  static constexpr int NF = H * Wh;
-  static constexpr int H2 = H / 2;
-  static_assert(H % 2 == 0, "fused path pairs rows: H must be even");
+  static constexpr int M = N / 2;
+  static constexpr int Wh = M + 1;
+  static constexpr int WP = N + 1;  // odd float row stride of w
+  static constexpr int NF = N * Wh;
+  // complex row stride of the workspace: odd, >= Wh, and N*RS == Wh (mod 16) when possible,
+  // so the row tasks (lane -> row) and the column half-warps (lane -> column, running across
+  // plane boundaries) both hit 16 distinct 8-byte bank pairs
+  static constexpr int pick_rs() {
+    for (int r = Wh | 1; r < Wh + 17; r += 2)
+      if (((N * r - Wh) % 16 + 16) % 16 == 0) return r;
+    return Wh | 1;
+  }
+  static constexpr int RS = pick_rs();
+  static constexpr int PS = N * RS + (((Wh - N * RS) % 16) + 16) % 16;  // == Wh (mod 16)
+  static_assert(N % 2 == 0 && (N / 2) % 2 == 1, "fused grid must be N = 2 * odd");
 };
 
-template <typename T>
-__device__ __forceinline__ T soft(T a, T k) {
-  return a > k ? a - k : (a < -k ? a + k : (a == a ? (T)0 : a));
-}
-template <typename T>
-__device__ __forceinline__ T clipk(T a, T k) {
-  return a > k ? k : (a < -k ? -k : a);
-}
-
 // shared-memory carve-up (all offsets 16-byte aligned)
-template <typename T, int H, int W>
+template <typename T, int N>
 struct Smem {
-  using G = Geo<H, W>;
-  static __host__ __device__ size_t w_bytes(int nk) { return align16(sizeof(T) * (size_t)nk * H * G::WP); }
-  static __host__ __device__ size_t x_bytes(int nk) { return align16(sizeof(cx<T>) * (size_t)nk * H * G::WhP); }
-  static __host__ __device__ size_t g_bytes() { return align16(sizeof(cx<T>) * (size_t)H * G::WhP); }
-  static __host__ __device__ size_t p_bytes() { return align16(sizeof(cx<T>) * (size_t)G::NF); }
-  static __host__ __device__ size_t n_bytes(int cs) { return align16(sizeof(double) * 8 * (size_t)cs); }
+  using G = Geo<N>;
+  static __host__ __device__ size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
+  static __host__ __device__ size_t w_bytes(int nk) { return al(sizeof(T) * (size_t)nk * N * G::WP); }
+  static __host__ __device__ size_t x_bytes(int nk) { return al(sizeof(cx<T>) * (size_t)nk * G::PS); }
+  static __host__ __device__ size_t g_bytes() { return al(sizeof(cx<T>) * (size_t)N * G::RS); }
+  static __host__ __device__ size_t p_bytes() { return al(sizeof(cx<T>) * (size_t)G::NF); }
+  static __host__ __device__ size_t n_bytes(int cs) { return al(sizeof(double) * 8 * (size_t)cs); }
   static __host__ __device__ size_t total(int nk, int cs) {
-    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes() + n_bytes(cs) + 6 * 32 * sizeof(double);  // + block_allsum scratch
+    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes() + n_bytes(cs) + 6 * 32 * sizeof(double);
   }
-  static __host__ __device__ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+  static __host__ __device__ int threads(int nk) {
+    const int wc = (nk * G::Wh + 15) / 16, wr = (nk * N + 31) / 32;
+    return 32 * (wc > wr ? wc : wr);
+  }
 };
 
 // block-wide sum of NV doubles, result broadcast to every thread
@@ -100,12 +113,57 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch) {
   __syncthreads();
 }
 
-template <typename T, int H, int W>
-__global__ void __launch_bounds__(384, 1) k_code_fused(FusedArgs<T> a) {
+template <typename T>
+__device__ __forceinline__ T clampk(T w, T k) {
+  return fmin(fmax(w, -k), k);  // Gamma = clip(w); NaN maps to -k so U = w - Gamma stays NaN
+}
+
+// half spectrum row[0..M] of a real row  ->  z = conj(Ze + i Zo) (inverse through the forward FFT)
+template <typename C, int N>
+__device__ __forceinline__ void row_inverse_pre(const C* row, C (&z)[N / 2]) {
+  using T = decltype(C::x);
+  constexpr int M = N / 2;
+  sfft::static_for<0, M>([&](auto Kk) {
+    constexpr int k = decltype(Kk)::value;
+    C A_ = row[k], B_ = row[M - k];
+    if constexpr (k == 0) {  // DC and Nyquist are real for a real row
+      A_.y = 0;
+      B_.y = 0;
+    }
+    const T zex = (T)0.5 * (A_.x + B_.x), zey = (T)0.5 * (A_.y - B_.y);
+    const T dx = (T)0.5 * (A_.x - B_.x), dy = (T)0.5 * (A_.y + B_.y);
+    constexpr T c = (T)sfft::ce_cos(2.0 * sfft::kPi * k / N);
+    constexpr T s = (T)sfft::ce_sin(2.0 * sfft::kPi * k / N);
+    const T zox = c * dx - s * dy, zoy = c * dy + s * dx;  // Zo = D e^{+2 pi i k/N}
+    z[k] = mkc<C>(zex - zoy, -(zey + zox));                // conj(Ze + i Zo)
+  });
+}
+
+// Z = FFT_M(even + i odd)  ->  half spectrum row[0..M] of the real row
+template <typename C, int N>
+__device__ __forceinline__ void row_forward_post(const C (&Z)[N / 2], C* row) {
+  using T = decltype(C::x);
+  constexpr int M = N / 2;
+  sfft::static_for<0, M + 1>([&](auto Kk) {
+    constexpr int k = decltype(Kk)::value;
+    const C a = Z[k % M], bb = Z[(M - k) % M];
+    const T zex = (T)0.5 * (a.x + bb.x), zey = (T)0.5 * (a.y - bb.y);
+    const T zox = (T)0.5 * (a.y + bb.y), zoy = (T)0.5 * (bb.x - a.x);  // Zo = -i (a - conj bb)/2
+    constexpr T c = (T)sfft::ce_cos(2.0 * sfft::kPi * k / N);
+    constexpr T s = (T)sfft::ce_sin(2.0 * sfft::kPi * k / N);
+    row[k] = mkc<C>(zex + c * zox + s * zoy, zey + c * zoy - s * zox);  // Ze + e^{-2 pi i k/N} Zo
+  });
+}
+
+enum ColMode : int { COL_F = 0, COL_I = 1, COL_FE = 2 };
+
+template <typename T, int N>
+__global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   using C = cx<T>;
-  using G = Geo<H, W>;
-  using S = Smem<T, H, W>;
-  constexpr int Wh = G::Wh, WP = G::WP, WhP = G::WhP, NF = G::NF, H2 = G::H2;
+  using G = Geo<N>;
+  using S = Smem<T, N>;
+  using A = T;  // norm accumulators follow the arithmetic precision
+  constexpr int M = G::M, Wh = G::Wh, WP = G::WP, RS = G::RS, PS = G::PS, NF = G::NF;
 
   cg::cluster_group cl = cg::this_cluster();
   const int CS = (int)cl.num_blocks();
@@ -117,80 +175,91 @@ __global__ void __launch_bounds__(384, 1) k_code_fused(FusedArgs<T> a) {
   const int nkmax = (K + CS - 1) / CS;
 
   extern __shared__ __align__(16) unsigned char smem[];
-  T* wS = reinterpret_cast<T*>(smem);
-  C* Xf = reinterpret_cast<C*>(smem + S::w_bytes(nkmax));
-  C* gS = reinterpret_cast<C*>(smem + S::w_bytes(nkmax) + S::x_bytes(nkmax));
-  C* part = reinterpret_cast<C*>(smem + S::w_bytes(nkmax) + S::x_bytes(nkmax) + S::g_bytes());
-  double* norms = reinterpret_cast<double*>(smem + S::w_bytes(nkmax) + S::x_bytes(nkmax) + S::g_bytes() +
-                                            S::p_bytes());
+  size_t off = 0;
+  T* wS = reinterpret_cast<T*>(smem + off);   off += S::w_bytes(nkmax);
+  C* X = reinterpret_cast<C*>(smem + off);    off += S::x_bytes(nkmax);
+  C* gS = reinterpret_cast<C*>(smem + off);   off += S::g_bytes();
+  C* part = reinterpret_cast<C*>(smem + off); off += S::p_bytes();
+  double* norms = reinterpret_cast<double*>(smem + off);
   double* scratch = norms + 8 * CS;
 
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const T kappa = a.kappa;
-  const T invP = (T)(1.0 / ((double)H * W));
+  const T cscl = (T)(2.0 / ((double)N * N));  // c = (2/P) IFFT_M(z): the M-point inverse covers half a row
   const C* Dg = a.Wh + (int64_t)k0 * NF;
-  const int nrow_tasks = nk * H2, ncol_tasks = nk * Wh;
 
-  // cold start: w = 0, so t = 0 and its row transforms are 0
-  for (int i = tid; i < nk * H * WP; i += nt) wS[i] = (T)0;
-  for (int i = tid; i < nk * H * WhP; i += nt) Xf[i] = mkc<C>(0, 0);
+  // column task of this lane: item (plane cj, column cv) shared by lanes l and l^16, index parity h
+  const int citem = warp * 16 + (lane & 15);
+  const int hpar = lane >> 4;
+  const bool cvalid = citem < nk * Wh;
+  const int cj = cvalid ? citem / Wh : 0, cv = cvalid ? citem % Wh : 0;
+  C* colp = X + cj * PS + cv;
+  const C* dcol = Dg + (int64_t)cj * NF + cv;
+  // row task of this thread: plane rj, row rq
+  const bool rvalid = tid < nk * N;
+  const int rj = rvalid ? tid / N : 0, rq = rvalid ? tid % N : 0;
+  C* xrow = X + rj * PS + rq * RS;
+  T* wrow = wS + (rj * N + rq) * WP;
+
+  for (int i = tid; i < nk * N * WP; i += nt) wS[i] = (T)0;
+  for (int i = tid; i < nk * PS; i += nt) X[i] = mkc<C>(0, 0);
   __syncthreads();
 
-  // ---------------------------------------------------------------- pieces --
-  // forward column FFT of the row-transformed plane j, column v; optionally emit it; Xf <- D * col
-  auto col_forward = [&](int j, int v, C* emit) {
-    C col[H];
+  // ---- column transform of item (cj, cv): Good-Thomas 2 x M across lanes l, l^16 ----------
+  auto col_phase = [&](auto mode_c, C* emit) {
+    constexpr int mode = decltype(mode_c)::value;
+    C z[M];
+    int u = hpar ? M : 0;  // input map n = (M h + 2 n2) mod N
 #pragma unroll
-    for (int u = 0; u < H; ++u) col[u] = Xf[(j * H + u) * WhP + v];
-    sfft::fft<C, H, false>(col);
+    for (int n2 = 0; n2 < M; ++n2) {
+      if constexpr (mode == COL_I) {
+        const C g = gS[u * RS + cv];
+        z[n2] = cmul(dcol[u * Wh], mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
+      } else {
+        z[n2] = colp[u * RS];
+      }
+      u = u + 2 >= N ? u + 2 - N : u + 2;
+    }
+    sfft::fft<C, M, false>(z);
+    int k = hpar ? M : 0;  // output map k = (M h + (M+1) k2) mod N
 #pragma unroll
-    for (int u = 0; u < H; ++u) {
-      if (emit) emit[u * Wh + v] = col[u];
-      Xf[(j * H + u) * WhP + v] = cmul(Dg[(int64_t)j * NF + u * Wh + v], col[u]);
+    for (int k2 = 0; k2 < M; ++k2) {
+      const C p = mkc<C>(__shfl_xor_sync(0xffffffffu, z[k2].x, 16), __shfl_xor_sync(0xffffffffu, z[k2].y, 16));
+      const C o = hpar ? csub(p, z[k2]) : cadd(z[k2], p);
+      if (cvalid) {
+        if constexpr (mode == COL_I) {
+          colp[k * RS] = mkc<C>(o.x, -o.y);
+        } else {
+          if constexpr (mode == COL_FE) emit[(int64_t)cj * NF + k * Wh + cv] = o;
+          colp[k * RS] = cmul(dcol[k * Wh], o);
+        }
+      }
+      k = k + M + 1 >= N ? k + M + 1 - N : k + M + 1;
     }
   };
-  // sum over own filters -> part (the CTA's share of sum_k D_k T_k)
   auto reduce_part = [&]() {
     for (int f = tid; f < NF; f += nt) {
-      const int u = f / Wh, v = f % Wh;
+      const int o = (f / Wh) * RS + f % Wh;
       C s = mkc<C>(0, 0);
-      for (int j = 0; j < nk; ++j) s = cadd(s, Xf[(j * H + u) * WhP + v]);
+      for (int j = 0; j < nk; ++j) s = cadd(s, X[j * PS + o]);
       part[f] = s;
     }
   };
-  // rows q and q+H/2 of plane j: value(w) of the stored w -> packed forward row FFT -> Xf rows
-  auto row_forward_store = [&](int j, int q, auto value) {
-    const T* wa = wS + (j * H + q) * WP;
-    const T* wb = wS + (j * H + q + H2) * WP;
-    C z[W];
-#pragma unroll
-    for (int n = 0; n < W; ++n) z[n] = mkc<C>(value(wa[n]), value(wb[n]));
-    sfft::fft<C, W, false>(z);
-    C* xa = Xf + (j * H + q) * WhP;
-    C* xb = Xf + (j * H + q + H2) * WhP;
-#pragma unroll
-    for (int k = 0; k < Wh; ++k) {
-      const C p = z[k], m = z[(W - k) % W];
-      // A = (Z[k] + conj Z[-k]) / 2 ;  B = -i (Z[k] - conj Z[-k]) / 2
-      xa[k] = mkc<C>((T)0.5 * (p.x + m.x), (T)0.5 * (p.y - m.y));
-      xb[k] = mkc<C>((T)0.5 * (p.y + m.y), (T)0.5 * (m.x - p.x));
-    }
-  };
-  auto t_of = [kappa](T wv) { const T uv = soft(wv, kappa); return uv - (wv - uv); };
-  auto u_of = [kappa](T wv) { return soft(wv, kappa); };
 
   int it = 0, stat = 0;
   for (;;) {
-    // ---- A: forward column transforms, multiply by D, partial synthesis -------------------
-    for (int task = tid; task < ncol_tasks; task += nt) col_forward(task / Wh, task % Wh, nullptr);
+    // ---- A: forward column transforms times D, partial synthesis ------------------------
+    col_phase(std::integral_constant<int, COL_F>{}, nullptr);
     __syncthreads();
     reduce_part();
-    cl.sync();  // #1: partials and the previous iteration's norms are visible cluster-wide
+    cl.sync();  // #1: partials and the previous iteration's norms are visible
     bool stop = false;
     if (it > 0) {
       double n4[5] = {0, 0, 0, 0, 0};
-      for (int q = 0; q < CS; ++q)
-        for (int i = 0; i < 5; ++i) n4[i] += norms[8 * q + i];
+      for (int qq = 0; qq < CS; ++qq)
+#pragma unroll
+        for (int i = 0; i < 5; ++i) n4[i] += norms[8 * qq + i];
       if (n4[4] > 0.0) {
         stat = 2;
         stop = true;
@@ -205,110 +274,88 @@ __global__ void __launch_bounds__(384, 1) k_code_fused(FusedArgs<T> a) {
     if (!stop && it == a.max_iters) stop = true;
     if (stop) break;
     ++it;
-    // ---- reduce-scatter y over the cluster, g = (X - y) / den on my slice, all-gather g ---
+    // ---- reduce-scatter y over the cluster; g = (X - y)/den on my slice; all-gather g ----
     {
       const int f0 = (int)((int64_t)r * NF / CS), f1 = (int)((int64_t)(r + 1) * NF / CS);
       for (int f = f0 + tid; f < f1; f += nt) {
         C y = mkc<C>(0, 0);
-        for (int q = 0; q < CS; ++q) y = cadd(y, cl.map_shared_rank(part, q)[f]);
+        for (int qq = 0; qq < CS; ++qq) y = cadd(y, cl.map_shared_rank(part, qq)[f]);
         const T inv = (T)1 / a.den[f];
         const C g = cscale(csub(a.xh[(int64_t)b * NF + f], y), inv);
-        const int u = f / Wh, v = f % Wh;
-        for (int q = 0; q < CS; ++q) cl.map_shared_rank(gS, q)[u * WhP + v] = g;
+        const int o = (f / Wh) * RS + f % Wh;
+        for (int qq = 0; qq < CS; ++qq) cl.map_shared_rank(gS, qq)[o] = g;
       }
     }
     cl.sync();  // #2: g complete in every CTA
-    // ---- B: C_k = conj(D_k) g, inverse column transforms ----------------------------------
-    for (int task = tid; task < ncol_tasks; task += nt) {
-      const int j = task / Wh, v = task % Wh;
-      C col[H];
-#pragma unroll
-      for (int u = 0; u < H; ++u) col[u] = cmulc(Dg[(int64_t)j * NF + u * Wh + v], gS[u * WhP + v]);
-      sfft::fft<C, H, true>(col);
-#pragma unroll
-      for (int u = 0; u < H; ++u) Xf[(j * H + u) * WhP + v] = col[u];
-    }
+    // ---- B: inverse column transforms of conj(D) g ---------------------------------------
+    col_phase(std::integral_constant<int, COL_I>{}, nullptr);
     __syncthreads();
-    // ---- rows: inverse row FFT -> c, update w, norms, next t, forward row FFT -------------
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    // ---- C: row IFFT -> c -> update w (registers) -> t -> row FFT --------------------------
+    A s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     bool bad = false;
-    for (int task = tid; task < nrow_tasks; task += nt) {
-      const int j = task / H2, q = task % H2;
-      C z[W];
-      {
-        const C* xa = Xf + (j * H + q) * WhP;
-        const C* xb = Xf + (j * H + q + H2) * WhP;
+    if (rvalid) {
+      C z[M];
+      row_inverse_pre<C, N>(xrow, z);
+      sfft::fft<C, M, false>(z);
 #pragma unroll
-        for (int k = 0; k < Wh; ++k) {
-          C A = xa[k], Bv = xb[k];
-          if (k == 0 || 2 * k == W) {
-            A.y = 0;
-            Bv.y = 0;
-          }
-          z[k] = mkc<C>(A.x - Bv.y, A.y + Bv.x);            // A + iB
-          if (k > 0 && 2 * k != W) z[W - k] = mkc<C>(A.x + Bv.y, Bv.x - A.y);  // conj A + i conj B
-        }
-      }
-      sfft::fft<C, W, true>(z);
-      T* wa = wS + (j * H + q) * WP;
-      T* wb = wS + (j * H + q + H2) * WP;
+      for (int m = 0; m < M; ++m) {
+        T tv[2];
 #pragma unroll
-      for (int n = 0; n < W; ++n) {
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          T* wp = half ? wb : wa;
-          const T c = (half ? z[n].y : z[n].x) * invP;
-          const T wo = wp[n];
-          const T uo = soft(wo, kappa), go = wo - uo;
+        for (int e = 0; e < 2; ++e) {
+          const T c = (e ? -z[m].y : z[m].x) * cscl;
+          const T wo = wrow[2 * m + e];
+          const T go = clampk(wo, kappa), uo = wo - go;
           const T wn = uo + c;
-          const T un = soft(wn, kappa), gn = wn - un;
-          bad |= !isfinite(un);
-          const float d0 = (float)(un - uo), d2 = (float)(gn - go);
-          s0 = fmaf(d0, d0, s0);
-          s1 = fmaf((float)un, (float)un, s1);
-          s2 = fmaf(d2, d2, s2);
-          s3 = fmaf((float)gn, (float)gn, s3);
-          wp[n] = wn;
+          const T gn = clampk(wn, kappa), un = wn - gn;
+          bad |= !(fabs(un) <= (T)3.0e38);
+          const A d0 = (A)(un - uo), d2 = (A)(gn - go);
+          s0 = fma(d0, d0, s0);
+          s1 = fma((A)un, (A)un, s1);
+          s2 = fma(d2, d2, s2);
+          s3 = fma((A)gn, (A)gn, s3);
+          wrow[2 * m + e] = wn;
+          tv[e] = un - gn;
         }
+        z[m] = mkc<C>(tv[0], tv[1]);
       }
-      row_forward_store(j, q, t_of);
+      sfft::fft<C, M, false>(z);
+      row_forward_post<C, N>(z, xrow);
     }
-    double nv[5] = {s0, s1, s2, s3, bad ? 1.0 : 0.0};
-    block_allsum<5>(nv, scratch);
+    double nv[5] = {(double)s0, (double)s1, (double)s2, (double)s3, bad ? 1.0 : 0.0};
+    block_allsum<5>(nv, scratch);  // (contains the barrier that ends the row phase)
     if (tid < CS) {
       double* dst = cl.map_shared_rank(norms, tid) + 8 * r;
+#pragma unroll
       for (int i = 0; i < 5; ++i) dst[i] = nv[i];
     }
-    __syncthreads();
   }
 
-  // ---- outputs: U = S(w) (and t), F(U), objective -----------------------------------------
-  const int64_t plane0 = ((int64_t)b * K + k0) * H * W;
+  // ---- outputs: U = S(w) (and t), F(U), objective -------------------------------------------
   double l1 = 0.0;
-  for (int task = tid; task < nrow_tasks; task += nt) {
-    const int j = task / H2, q = task % H2;
+  if (rvalid) {
+    const int64_t rowoff = (((int64_t)b * K + k0 + rj) * N + rq) * N;
+    T* uo = a.u_out + rowoff;
+    T* to = a.t_out ? a.t_out + rowoff : nullptr;
+    C z[M];
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int row = q + half * H2;
-      const T* wp = wS + (j * H + row) * WP;
-      T* uo = a.u_out + plane0 + ((int64_t)j * H + row) * W;
-      T* to = a.t_out ? a.t_out + plane0 + ((int64_t)j * H + row) * W : nullptr;
-      for (int n = 0; n < W; ++n) {
-        const T wv = wp[n];
-        const T uv = soft(wv, kappa);
-        l1 += fabs((double)uv);
-        uo[n] = uv;
-        if (to) to[n] = uv - (wv - uv);
+    for (int m = 0; m < M; ++m) {
+      const T va = wrow[2 * m], vb = wrow[2 * m + 1];
+      const T ga = clampk(va, kappa), gb = clampk(vb, kappa);
+      const T ua = va - ga, ub = vb - gb;
+      uo[2 * m] = ua;
+      uo[2 * m + 1] = ub;
+      if (to) {
+        to[2 * m] = ua - ga;
+        to[2 * m + 1] = ub - gb;
       }
+      l1 += fabs((double)ua) + fabs((double)ub);
+      z[m] = mkc<C>(ua, ub);
     }
-    row_forward_store(j, q, u_of);
+    sfft::fft<C, M, false>(z);
+    row_forward_post<C, N>(z, xrow);
   }
   __syncthreads();
-  C* uh = a.uh_out + ((int64_t)b * K + k0) * NF;
-  for (int task = tid; task < ncol_tasks; task += nt) {
-    const int j = task / Wh, v = task % Wh;
-    col_forward(j, v, uh + (int64_t)j * NF);
-  }
+  col_phase(std::integral_constant<int, COL_FE>{}, a.uh_out + ((int64_t)b * K + k0) * NF);
   __syncthreads();
   reduce_part();
   cl.sync();
@@ -317,9 +364,9 @@ __global__ void __launch_bounds__(384, 1) k_code_fused(FusedArgs<T> a) {
     const int f0 = (int)((int64_t)r * NF / CS), f1 = (int)((int64_t)(r + 1) * NF / CS);
     for (int f = f0 + tid; f < f1; f += nt) {
       C y = mkc<C>(0, 0);
-      for (int q = 0; q < CS; ++q) y = cadd(y, cl.map_shared_rank(part, q)[f]);
+      for (int qq = 0; qq < CS; ++qq) y = cadd(y, cl.map_shared_rank(part, qq)[f]);
       const C res = csub(a.xh[(int64_t)b * NF + f], y);
-      e += herm_weight(f % Wh, W) * ((double)res.x * res.x + (double)res.y * res.y);
+      e += herm_weight(f % Wh, N) * ((double)res.x * res.x + (double)res.y * res.y);
     }
   }
   double ev[2] = {e, l1};
@@ -332,11 +379,11 @@ __global__ void __launch_bounds__(384, 1) k_code_fused(FusedArgs<T> a) {
   cl.sync();
   if (r == 0 && tid == 0) {
     double energy = 0.0, l1s = 0.0;
-    for (int q = 0; q < CS; ++q) {
-      energy += norms[8 * q + 5];
-      l1s += norms[8 * q + 6];
+    for (int qq = 0; qq < CS; ++qq) {
+      energy += norms[8 * qq + 5];
+      l1s += norms[8 * qq + 6];
     }
-    const double invPd = 1.0 / ((double)H * W);
+    const double invPd = 1.0 / ((double)N * N);
     a.obj[b] = 0.5 * invPd * energy + a.beta * l1s;
     if (a.resid) a.resid[b] = invPd * energy;
     a.iters[b] = it;
@@ -350,31 +397,29 @@ struct FusedPlan {
   size_t smem = 0;
 };
 
-template <typename T, int H, int W>
+template <typename T, int N>
 static FusedPlan plan_for(int K, int B) {
-  using G = Geo<H, W>;
   FusedPlan best;
   int dev = 0, max_smem = 0, sms = 148;
-  cudaGetDevice(&dev);
+  if (cudaGetDevice(&dev) != cudaSuccess) return best;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_code_fused<T, N>) != cudaSuccess) return best;
   double best_cost = 1e300;
   for (int cs : {2, 4, 8, 16}) {
     if (cs > K) break;
     const int nk = (K + cs - 1) / cs;
-    const size_t smem = Smem<T, H, W>::total(nk, cs);
+    const size_t smem = Smem<T, N>::total(nk, cs);
     if (smem > (size_t)max_smem) continue;
-    int work = nk * (G::Wh > G::H2 ? G::Wh : G::H2);
-    int threads = ((work + 31) / 32) * 32;
-    if (threads > 384) threads = 384;
-    if (threads < 64) threads = 64;
-    // clusters resident at once (1 CTA per SM for these footprints), then waves over B samples
+    const int threads = Smem<T, N>::threads(nk);
+    if (threads > fa.maxThreadsPerBlock) continue;  // registers x threads must fit the SM
     int per_sm = (int)(228 * 1024 / (smem + 1024));
     if (per_sm < 1) per_sm = 1;
     const int resident = (sms * per_sm) / cs;
     if (resident < 1) continue;
     const int waves = (B + resident - 1) / resident;
-    const double cost = (double)waves * nk * (1.0 + 0.05 * cs);  // mild penalty for cluster sync width
+    const double cost = (double)waves * nk * (1.0 + 0.05 * cs);
     if (cost < best_cost) {
       best_cost = cost;
       best.cs = cs;
@@ -385,11 +430,11 @@ static FusedPlan plan_for(int K, int B) {
   return best;
 }
 
-template <typename T, int H, int W>
+template <typename T, int N>
 static int launch_fused(const FusedArgs<T>& a, cudaStream_t s) {
-  FusedPlan p = plan_for<T, H, W>(a.K, a.B);
+  FusedPlan p = plan_for<T, N>(a.K, a.B);
   if (!p.cs) return fail(OCSC_EARG, "fused code ADMM: no cluster shape fits shared memory");
-  auto kern = k_code_fused<T, H, W>;
+  auto kern = k_code_fused<T, N>;
   OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   if (p.cs > 8) OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
@@ -409,18 +454,47 @@ static int launch_fused(const FusedArgs<T>& a, cudaStream_t s) {
   return OCSC_OK;
 }
 
-template <typename T, int H, int W>
-static int query_fused(int K, int B) {
-  return plan_for<T, H, W>(K, B).cs;
+template <typename T, int N>
+static int query_fused(int K, int B, int* info) {
+  FusedPlan p = plan_for<T, N>(K, B);
+  if (info) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_code_fused<T, N>);
+    info[0] = p.cs;
+    info[1] = p.threads;
+    info[2] = (int)p.smem;
+    info[3] = fa.numRegs;
+    info[4] = fa.maxThreadsPerBlock;
+    int clusters = 0;
+    if (p.cs) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(B * p.cs, 1, 1);
+      cfg.blockDim = dim3(p.threads, 1, 1);
+      cfg.dynamicSmemBytes = p.smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = p.cs;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaFuncSetAttribute(k_code_fused<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      if (p.cs > 8) cudaFuncSetAttribute(k_code_fused<T, N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaOccupancyMaxActiveClusters(&clusters, k_code_fused<T, N>, &cfg);
+    }
+    info[5] = clusters;
+  }
+  return p.cs;
 }
 
 // the grids the fused kernel is instantiated for (BASELINE config 1 is 42 x 42)
-#define OCSC_FUSED_SIZES(X) X(42, 42) X(12, 12) X(10, 10) X(16, 16) X(24, 24) X(20, 20) X(8, 8) X(12, 9)
+#define OCSC_FUSED_SIZES(X) X(42) X(10) X(14) X(18) X(30)
 
 template <typename T>
-static int fused_dispatch(int H, int W, bool query, const FusedArgs<T>* a, int K, int B, cudaStream_t s) {
-#define OCSC_CASE(HH, WW) \
-  if (H == HH && W == WW) return query ? query_fused<T, HH, WW>(K, B) : launch_fused<T, HH, WW>(*a, s);
+static int fused_dispatch(int H, int W, bool query, const FusedArgs<T>* a, int K, int B, cudaStream_t s,
+                          int* info = nullptr) {
+#define OCSC_CASE(NN) \
+  if (H == NN && W == NN) return query ? query_fused<T, NN>(K, B, info) : launch_fused<T, NN>(*a, s);
   OCSC_FUSED_SIZES(OCSC_CASE)
 #undef OCSC_CASE
   return query ? 0 : fail(OCSC_EARG, "fused code ADMM: grid not instantiated");
@@ -429,6 +503,14 @@ static int fused_dispatch(int H, int W, bool query, const FusedArgs<T>* a, int K
 }  // namespace ocsc
 
 using namespace ocsc;
+
+extern "C" int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32_t* info) {
+  for (int i = 0; i < 6; ++i) info[i] = 0;
+  if (K <= 0 || B <= 0) return 0;
+  if (dtype == OCSC_F32) return fused_dispatch<float>(H, W, true, nullptr, K, B, nullptr, info);
+  if (dtype == OCSC_F64) return fused_dispatch<double>(H, W, true, nullptr, K, B, nullptr, info);
+  return 0;
+}
 
 extern "C" int ocsc_code_fused_cluster(int dtype, int H, int W, int K, int B) {
   if (K <= 0 || B <= 0) return 0;

@@ -50,6 +50,21 @@ __host__ __device__ constexpr int smallest_factor(int n) {
   return n;
 }
 
+// p^e exactly dividing n for the smallest prime p | n
+__host__ __device__ constexpr int prime_power_factor(int n) {
+  const int p = smallest_factor(n);
+  int q = p;
+  while (n % (q * p) == 0) q *= p;
+  return q;
+}
+
+__host__ __device__ constexpr int modinv(int a, int m) {
+  a %= m;
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return 1;  // m == 1
+}
+
 template <int Begin, int End, typename F>
 __device__ __forceinline__ void static_for(F&& f) {
   if constexpr (Begin < End) {
@@ -127,34 +142,79 @@ __device__ __forceinline__ void dft_prime(C (&x)[R]) {
 }
 
 template <typename C, int N, bool INV>
-__device__ __forceinline__ void fft(C (&x)[N]) {
+__device__ __forceinline__ void fft(C (&x)[N]);
+
+// Cooley-Tukey decimation in time on the smallest prime (prime powers)
+template <typename C, int N, bool INV>
+__device__ __forceinline__ void fft_ct(C (&x)[N]) {
   constexpr int R = smallest_factor(N);
-  if constexpr (R == N) {
-    dft_prime<C, N, INV>(x);
-  } else {
-    constexpr int M = N / R;
-    C sub[R][M];
+  constexpr int M = N / R;
+  C sub[R][M];
+  static_for<0, R>([&](auto Rr) {
+    constexpr int r = decltype(Rr)::value;
+    static_for<0, M>([&](auto Mm) {
+      constexpr int m = decltype(Mm)::value;
+      sub[r][m] = x[m * R + r];
+    });
+    fft<C, M, INV>(sub[r]);
+  });
+  static_for<0, M>([&](auto Kk) {
+    constexpr int k = decltype(Kk)::value;
+    C tmp[R];
     static_for<0, R>([&](auto Rr) {
       constexpr int r = decltype(Rr)::value;
-      static_for<0, M>([&](auto Mm) {
-        constexpr int m = decltype(Mm)::value;
-        sub[r][m] = x[m * R + r];
-      });
-      fft<C, M, INV>(sub[r]);
+      tmp[r] = twiddle<C, N, r * k, INV>(sub[r][k]);
     });
-    static_for<0, M>([&](auto Kk) {
-      constexpr int k = decltype(Kk)::value;
-      C tmp[R];
-      static_for<0, R>([&](auto Rr) {
-        constexpr int r = decltype(Rr)::value;
-        tmp[r] = twiddle<C, N, r * k, INV>(sub[r][k]);
-      });
-      dft_prime<C, R, INV>(tmp);
-      static_for<0, R>([&](auto Q) {
-        constexpr int q = decltype(Q)::value;
-        x[k + M * q] = tmp[q];
-      });
+    dft_prime<C, R, INV>(tmp);
+    static_for<0, R>([&](auto Q) {
+      constexpr int q = decltype(Q)::value;
+      x[k + M * q] = tmp[q];
     });
+  });
+}
+
+// Good-Thomas prime-factor algorithm for N = N1 * N2 with gcd(N1, N2) = 1: no twiddles.
+// input  n = (N2 n1 + N1 n2) mod N ;  output k = (N2 t2 k1 + N1 t1 k2) mod N,
+// t2 = N2^-1 mod N1, t1 = N1^-1 mod N2.
+template <typename C, int N, bool INV>
+__device__ __forceinline__ void fft_pfa(C (&x)[N]) {
+  constexpr int N1 = prime_power_factor(N);
+  constexpr int N2 = N / N1;
+  constexpr int t2 = modinv(N2 % N1, N1), t1 = modinv(N1 % N2, N2);
+  C sub[N1][N2];
+  static_for<0, N1>([&](auto A) {
+    constexpr int n1 = decltype(A)::value;
+    static_for<0, N2>([&](auto Bb) {
+      constexpr int n2 = decltype(Bb)::value;
+      sub[n1][n2] = x[(N2 * n1 + N1 * n2) % N];
+    });
+    fft<C, N2, INV>(sub[n1]);
+  });
+  static_for<0, N2>([&](auto Kk) {
+    constexpr int k2 = decltype(Kk)::value;
+    C tmp[N1];
+    static_for<0, N1>([&](auto A) {
+      constexpr int n1 = decltype(A)::value;
+      tmp[n1] = sub[n1][k2];
+    });
+    fft<C, N1, INV>(tmp);
+    static_for<0, N1>([&](auto A) {
+      constexpr int k1 = decltype(A)::value;
+      x[(N2 * t2 * k1 + N1 * t1 * k2) % N] = tmp[k1];
+    });
+  });
+}
+
+template <typename C, int N, bool INV>
+__device__ __forceinline__ void fft(C (&x)[N]) {
+  if constexpr (N == 1) {
+    return;
+  } else if constexpr (smallest_factor(N) == N) {
+    dft_prime<C, N, INV>(x);
+  } else if constexpr (prime_power_factor(N) == N) {
+    fft_ct<C, N, INV>(x);
+  } else {
+    fft_pfa<C, N, INV>(x);
   }
 }
 

@@ -227,6 +227,9 @@ if __name__ == "__main__":
                      code_max_iters=60, beta=0.3)
         case_trainer("train_odd", (9, 7), (3, 3), 3, 3, 3, rho_dict=10.0, inner_iters=3,
                      code_max_iters=80, beta=0.4)
+    if run_all or "trainer" in which or "train_14" in which:
+        case_trainer("train_14", (14, 14), (3, 3), 5, 3, 3, rho_dict=1.0, inner_iters=4,
+                     code_max_iters=120, beta=0.3)
     if run_all or "minibatch" in which:
         case_minibatch("minibatch", (10, 10), (3, 3), 5, 3, 2, rho_dict=1.0, inner_iters=4,
                        code_max_iters=50, beta=0.3)

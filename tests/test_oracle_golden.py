@@ -101,7 +101,7 @@ def _trainer_from(g):
                      code_max_iters=int(g["code_max_iters"]), code_rel_tol=float(g["code_rel_tol"]))
 
 
-@pytest.mark.parametrize("name", ["train_2d", "train_odd"])
+@pytest.mark.parametrize("name", ["train_2d", "train_odd", "train_14"])
 def test_trainer_steps(golden, name):
     g = golden(name)
     tr = _trainer_from(g)

@@ -351,7 +351,7 @@ def test_fused_minibatch_matches_composed_reference(golden):
 
 
 def test_fused_single_sample_steps_match_reference(golden):
-    g = golden("train_2d")
+    g = golden("train_14")
     shape = _shape(g)
     tr = ob.OnlineTrainer(shape, _cfg(g, fused=True))
     assert tr.use_fused(1)
@@ -364,7 +364,7 @@ def test_fused_single_sample_steps_match_reference(golden):
     assert rel(tr.working_freq, g["working_freq"]) < TOL64
 
 
-@pytest.mark.parametrize("dims,K,B", [((16, 16), 7, 5), ((24, 24), 12, 3), ((12, 9), 4, 4), ((20, 20), 33, 2)])
+@pytest.mark.parametrize("dims,K,B", [((14, 14), 7, 5), ((18, 18), 12, 3), ((10, 10), 4, 4), ((30, 30), 33, 2)])
 def test_fused_equals_cufft_path(dims, K, B):
     shape = ob.SignalShape(dims, (3, 3))
     X = O.synth_images(2 * B, dims, dims, 3, filter_dims=(3, 3), seed=9, density=0.05).reshape(2 * B, -1)
@@ -397,9 +397,9 @@ def test_fused_float32_matches_oracle_42x42():
 
 
 def test_fused_divergence_raises():
-    shape = ob.SignalShape((12, 12), (3, 3))
+    shape = ob.SignalShape((14, 14), (3, 3))
     tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=4, batch_size=2))
-    X = np.random.default_rng(0).normal(size=(2, 144))
+    X = np.random.default_rng(0).normal(size=(2, 196))
     X[1, 5] = np.nan
     assert tr.use_fused(2)
     with pytest.raises(ob.DivergenceError, match="iteration"):
