@@ -113,9 +113,10 @@ int ocsc_code_admm(int dtype, int H, int W, int K, int B, const void* xh, const 
  * stopping semantics as ocsc_code_admm.  ocsc_code_fused_cluster returns the cluster
  * size the launch would use, or 0 when (dtype, H, W, K) is not supported. */
 int ocsc_code_fused_cluster(int dtype, int H, int W, int K, int B);
-/* Launch plan of ocsc_code_fused (host array of 6 int32): cluster size, threads per CTA,
- * dynamic shared memory bytes, registers per thread, max threads per block, max active
- * clusters.  Returns the cluster size (0 = unsupported). */
+/* Launch plan of ocsc_code_fused (host array of 8 int32): main cluster size, threads per
+ * CTA, dynamic shared memory bytes, registers per thread, main-shape resident clusters,
+ * samples run with the main shape, tail cluster size (0 = none), tail resident clusters.
+ * Returns the main cluster size (0 = unsupported). */
 int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32_t* info);
 int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
                     const void* den, double beta, double rho, int max_iters, double rel_tol,
@@ -141,7 +142,8 @@ int ocsc_synthesize(int dtype, int K, int nfreq, int B, const void* Wh, const vo
 int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int nfreq, int B, const void* z,
                             int64_t z_sb, int64_t z_sk, int64_t z_sp, const void* x, int64_t x_sb,
                             int64_t x_sp, void* S, void* c, void* stream);
-/* inv_p = scale * (S_p + ridge I)^-1 via per-frequency Cholesky (packed in/out).
+/* inv_p = scale * (S_p + ridge I)^-1, per-frequency in-place Gauss-Jordan in shared memory
+ * (HPD, no pivoting; packed in/out, K <= 118 for complex128).
  * info (device int32): 0, or 1 + first frequency whose matrix was not positive definite. */
 int ocsc_history_invert(int dtype_hist, int K, int nfreq, const void* S, double ridge, double scale,
                         void* inv, int32_t* info, void* stream);

@@ -22,6 +22,9 @@
 // produces F(U) (needed by the history), the code U, and the objective.
 #include <cooperative_groups.h>
 
+#include <map>
+#include <tuple>
+
 #include "common.cuh"
 #include "fft_small.cuh"
 
@@ -32,6 +35,7 @@ namespace ocsc {
 template <typename T>
 struct FusedArgs {
   int K, B, max_iters;
+  int b0;  // first sample of this launch (a mini-batch may be split over two cluster shapes)
   double tol, beta;
   T kappa;
   const cx<T>* xh;  // (B, nf)
@@ -82,10 +86,12 @@ struct Smem {
   static __host__ __device__ size_t w_bytes(int nk) { return al(sizeof(T) * (size_t)nk * N * G::WP); }
   static __host__ __device__ size_t x_bytes(int nk) { return al(sizeof(cx<T>) * (size_t)nk * G::PS); }
   static __host__ __device__ size_t g_bytes() { return al(sizeof(cx<T>) * (size_t)N * G::RS); }
-  static __host__ __device__ size_t p_bytes() { return al(sizeof(cx<T>) * (size_t)G::NF); }
+  static __host__ __device__ size_t p_bytes(int cs) {
+    return al(sizeof(cx<T>) * (size_t)cs * ((G::NF + cs - 1) / cs));
+  }
   static __host__ __device__ size_t n_bytes(int cs) { return al(sizeof(double) * 8 * (size_t)cs); }
   static __host__ __device__ size_t total(int nk, int cs) {
-    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes() + n_bytes(cs) + 6 * 32 * sizeof(double);
+    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes(cs) + n_bytes(cs) + 6 * 32 * sizeof(double);
   }
   static __host__ __device__ int threads(int nk) {
     const int wc = (nk * G::Wh + 15) / 16, wr = (nk * N + 31) / 32;
@@ -99,17 +105,21 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
-  __syncthreads();
   if (lane == 0)
 #pragma unroll
     for (int i = 0; i < NV; ++i) scratch[i * 32 + warp] = v[i];
   __syncthreads();
+  if (warp == 0) {
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    double s = 0.0;
-    for (int q = 0; q < nw; ++q) s += scratch[i * 32 + q];
-    v[i] = s;
+    for (int i = 0; i < NV; ++i) {
+      double s = lane < nw ? scratch[i * 32 + lane] : 0.0;
+      s = warp_sum(s);
+      if (lane == 0) scratch[32 * NV + i] = s;
+    }
   }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = scratch[32 * NV + i];
   __syncthreads();
 }
 
@@ -168,7 +178,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   cg::cluster_group cl = cg::this_cluster();
   const int CS = (int)cl.num_blocks();
   const int r = (int)cl.block_rank();
-  const int b = blockIdx.x / CS;
+  const int b = a.b0 + (int)(blockIdx.x / CS);
   const int K = a.K;
   const int k0 = (int)((int64_t)r * K / CS), k1 = (int)((int64_t)(r + 1) * K / CS);
   const int nk = k1 - k0;
@@ -179,7 +189,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   T* wS = reinterpret_cast<T*>(smem + off);   off += S::w_bytes(nkmax);
   C* X = reinterpret_cast<C*>(smem + off);    off += S::x_bytes(nkmax);
   C* gS = reinterpret_cast<C*>(smem + off);   off += S::g_bytes();
-  C* part = reinterpret_cast<C*>(smem + off); off += S::p_bytes();
+  C* part = reinterpret_cast<C*>(smem + off); off += S::p_bytes(CS);
   double* norms = reinterpret_cast<double*>(smem + off);
   double* scratch = norms + 8 * CS;
 
@@ -207,44 +217,63 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   __syncthreads();
 
   // ---- column transform of item (cj, cv): Good-Thomas 2 x M across lanes l, l^16 ----------
+  // lane parity h shifts every input/output row index by +-M (mod N): the shift's sign is a
+  // compile-time function of the row, its magnitude a per-lane register, so no selects
+  const int dpx = hpar ? M * RS : 0;  // +M rows in the workspace
+  const int dpd = hpar ? M * Wh : 0;  // +M rows in D / F(U)
+  const T sgn = hpar ? (T)-1 : (T)1;
   auto col_phase = [&](auto mode_c, C* emit) {
     constexpr int mode = decltype(mode_c)::value;
     C z[M];
-    int u = hpar ? M : 0;  // input map n = (M h + 2 n2) mod N
-#pragma unroll
-    for (int n2 = 0; n2 < M; ++n2) {
+    sfft::static_for<0, M>([&](auto Nn) {
+      constexpr int n2 = decltype(Nn)::value;
+      constexpr int u0 = 2 * n2;                  // row for h = 0
+      constexpr int sh = (u0 < M) ? 1 : -1;       // row for h = 1 is u0 + sh*M
+      const int ox = u0 * RS + sh * dpx;
       if constexpr (mode == COL_I) {
-        const C g = gS[u * RS + cv];
-        z[n2] = cmul(dcol[u * Wh], mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
+        const C g = gS[ox + cv];
+        z[n2] = cmul(dcol[u0 * Wh + sh * dpd], mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
       } else {
-        z[n2] = colp[u * RS];
+        z[n2] = colp[ox];
       }
-      u = u + 2 >= N ? u + 2 - N : u + 2;
-    }
+    });
     sfft::fft<C, M, false>(z);
-    int k = hpar ? M : 0;  // output map k = (M h + (M+1) k2) mod N
-#pragma unroll
-    for (int k2 = 0; k2 < M; ++k2) {
+    sfft::static_for<0, M>([&](auto Kk) {
+      constexpr int k2 = decltype(Kk)::value;
+      constexpr int kA = ((M + 1) * k2) % N;      // output row for h = 0; h = 1 is kA + sh*M
+      constexpr int sh = (kA < M) ? 1 : -1;
       const C p = mkc<C>(__shfl_xor_sync(0xffffffffu, z[k2].x, 16), __shfl_xor_sync(0xffffffffu, z[k2].y, 16));
-      const C o = hpar ? csub(p, z[k2]) : cadd(z[k2], p);
+      const C o = mkc<C>(fma(sgn, z[k2].x, p.x), fma(sgn, z[k2].y, p.y));  // h=0: z+p, h=1: p-z
       if (cvalid) {
+        const int ox = kA * RS + sh * dpx;
         if constexpr (mode == COL_I) {
-          colp[k * RS] = mkc<C>(o.x, -o.y);
+          colp[ox] = mkc<C>(o.x, -o.y);
         } else {
-          if constexpr (mode == COL_FE) emit[(int64_t)cj * NF + k * Wh + cv] = o;
-          colp[k * RS] = cmul(dcol[k * Wh], o);
+          const int od = kA * Wh + sh * dpd;
+          if constexpr (mode == COL_FE) emit[(int64_t)cj * NF + od + cv] = o;
+          colp[ox] = cmul(dcol[od], o);
         }
       }
-      k = k + M + 1 >= N ? k + M + 1 - N : k + M + 1;
-    }
+    });
   };
-  auto reduce_part = [&]() {
+  // partial synthesis sum over own filters, pushed straight into the owner CTA's receive slot
+  // (owner of frequency f = the CTA whose slice [f0, f1) contains it); part is CS x slice
+  const int slice = (NF + CS - 1) / CS;
+  auto reduce_push = [&]() {
     for (int f = tid; f < NF; f += nt) {
       const int o = (f / Wh) * RS + f % Wh;
       C s = mkc<C>(0, 0);
       for (int j = 0; j < nk; ++j) s = cadd(s, X[j * PS + o]);
-      part[f] = s;
+      const int owner = f / slice;
+      cl.map_shared_rank(part, owner)[r * slice + (f - owner * slice)] = s;
     }
+  };
+  // y[f] for my slice from the CS received partials (local loads only)
+  auto gather_y = [&](int f) {
+    C y = mkc<C>(0, 0);
+    const int fl = f - r * slice;
+    for (int qq = 0; qq < CS; ++qq) y = cadd(y, part[qq * slice + fl]);
+    return y;
   };
 
   int it = 0, stat = 0;
@@ -252,7 +281,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     // ---- A: forward column transforms times D, partial synthesis ------------------------
     col_phase(std::integral_constant<int, COL_F>{}, nullptr);
     __syncthreads();
-    reduce_part();
+    reduce_push();
     cl.sync();  // #1: partials and the previous iteration's norms are visible
     bool stop = false;
     if (it > 0) {
@@ -274,16 +303,16 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     if (!stop && it == a.max_iters) stop = true;
     if (stop) break;
     ++it;
-    // ---- reduce-scatter y over the cluster; g = (X - y)/den on my slice; all-gather g ----
+    // ---- y on my slice from the pushed partials, g = (X - y)/den, all-gather g ------------
     {
-      const int f0 = (int)((int64_t)r * NF / CS), f1 = (int)((int64_t)(r + 1) * NF / CS);
-      for (int f = f0 + tid; f < f1; f += nt) {
-        C y = mkc<C>(0, 0);
-        for (int qq = 0; qq < CS; ++qq) y = cadd(y, cl.map_shared_rank(part, qq)[f]);
+      const int f0 = r * slice, f1 = min(NF, f0 + slice);
+      const int nsl = f1 - f0;
+      for (int e = tid; e < nsl * CS; e += nt) {  // (frequency, destination) pairs
+        const int f = f0 + e % nsl, qq = e / nsl;
+        const C y = gather_y(f);
         const T inv = (T)1 / a.den[f];
         const C g = cscale(csub(a.xh[(int64_t)b * NF + f], y), inv);
-        const int o = (f / Wh) * RS + f % Wh;
-        for (int qq = 0; qq < CS; ++qq) cl.map_shared_rank(gS, qq)[o] = g;
+        cl.map_shared_rank(gS, qq)[(f / Wh) * RS + f % Wh] = g;
       }
     }
     cl.sync();  // #2: g complete in every CTA
@@ -307,8 +336,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
           const T go = clampk(wo, kappa), uo = wo - go;
           const T wn = uo + c;
           const T gn = clampk(wn, kappa), un = wn - gn;
-          bad |= !(fabs(un) <= (T)3.0e38);
-          const A d0 = (A)(un - uo), d2 = (A)(gn - go);
+          const A d0 = (A)(un - uo), d2 = (A)(gn - go);  // a non-finite code poisons these sums
           s0 = fma(d0, d0, s0);
           s1 = fma((A)un, (A)un, s1);
           s2 = fma(d2, d2, s2);
@@ -321,6 +349,8 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       sfft::fft<C, M, false>(z);
       row_forward_post<C, N>(z, xrow);
     }
+    // a non-finite code value poisons this thread's partial sums
+    bad = !isfinite(s0) || !isfinite(s1) || !isfinite(s2) || !isfinite(s3);
     double nv[5] = {(double)s0, (double)s1, (double)s2, (double)s3, bad ? 1.0 : 0.0};
     block_allsum<5>(nv, scratch);  // (contains the barrier that ends the row phase)
     if (tid < CS) {
@@ -357,14 +387,13 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   __syncthreads();
   col_phase(std::integral_constant<int, COL_FE>{}, a.uh_out + ((int64_t)b * K + k0) * NF);
   __syncthreads();
-  reduce_part();
+  reduce_push();
   cl.sync();
   double e = 0.0;
   {
-    const int f0 = (int)((int64_t)r * NF / CS), f1 = (int)((int64_t)(r + 1) * NF / CS);
+    const int f0 = r * slice, f1 = min(NF, f0 + slice);
     for (int f = f0 + tid; f < f1; f += nt) {
-      C y = mkc<C>(0, 0);
-      for (int qq = 0; qq < CS; ++qq) y = cadd(y, cl.map_shared_rank(part, qq)[f]);
+      const C y = gather_y(f);
       const C res = csub(a.xh[(int64_t)b * NF + f], y);
       e += herm_weight(f % Wh, N) * ((double)res.x * res.x + (double)res.y * res.y);
     }
@@ -392,59 +421,115 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
 }
 
 // ---------------------------------------------------------------- dispatch --
-struct FusedPlan {
-  int cs = 0, threads = 0;
+struct FusedShape {
+  int cs = 0, threads = 0, nk = 0, active = 0;
   size_t smem = 0;
+};
+struct FusedPlan {
+  FusedShape main, tail;  // main shape for the first b_main samples, tail shape for the rest
+  int b_main = 0;
 };
 
 template <typename T, int N>
+static int max_active_clusters(const FusedShape& sh, int B) {
+  auto kern = k_code_fused<T, N>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+  if (sh.cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B * sh.cs, 1, 1);
+  cfg.blockDim = dim3(sh.threads, 1, 1);
+  cfg.dynamicSmemBytes = sh.smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = sh.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// Choose cluster shapes.  Per-cluster time ~ nk (filters per CTA); a wave runs `active`
+// clusters at once.  The main shape maximises samples per unit time; a remainder smaller
+// than the main shape's wave goes to the shape that finishes it soonest (usually a wider
+// cluster: BASELINE config 1 runs 45 samples as 3 waves of 15 eight-CTA clusters and the last
+// 5 as sixteen-CTA clusters instead of a mostly idle fourth wave).
+template <typename T, int N>
 static FusedPlan plan_for(int K, int B) {
-  FusedPlan best;
-  int dev = 0, max_smem = 0, sms = 148;
-  if (cudaGetDevice(&dev) != cudaSuccess) return best;
+  FusedPlan plan;
+  int dev = 0, max_smem = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return plan;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, k_code_fused<T, N>) != cudaSuccess) return best;
-  double best_cost = 1e300;
+  if (cudaFuncGetAttributes(&fa, k_code_fused<T, N>) != cudaSuccess) return plan;
+  FusedShape shapes[4];
+  int ns = 0;
   for (int cs : {2, 4, 8, 16}) {
     if (cs > K) break;
-    const int nk = (K + cs - 1) / cs;
-    const size_t smem = Smem<T, N>::total(nk, cs);
-    if (smem > (size_t)max_smem) continue;
-    const int threads = Smem<T, N>::threads(nk);
-    if (threads > fa.maxThreadsPerBlock) continue;  // registers x threads must fit the SM
-    int per_sm = (int)(228 * 1024 / (smem + 1024));
-    if (per_sm < 1) per_sm = 1;
-    const int resident = (sms * per_sm) / cs;
-    if (resident < 1) continue;
-    const int waves = (B + resident - 1) / resident;
-    const double cost = (double)waves * nk * (1.0 + 0.05 * cs);
-    if (cost < best_cost) {
-      best_cost = cost;
-      best.cs = cs;
-      best.threads = threads;
-      best.smem = smem;
+    FusedShape sh;
+    sh.cs = cs;
+    sh.nk = (K + cs - 1) / cs;
+    sh.smem = Smem<T, N>::total(sh.nk, cs);
+    sh.threads = Smem<T, N>::threads(sh.nk);
+    if (sh.smem > (size_t)max_smem || sh.threads > fa.maxThreadsPerBlock) continue;
+    sh.active = max_active_clusters<T, N>(sh, B);
+    if (sh.active > 0) shapes[ns++] = sh;
+  }
+  if (!ns) return plan;
+  // main shape: most samples per unit time (ties -> smaller cluster)
+  int best = 0;
+  for (int i = 1; i < ns; ++i)
+    if ((double)shapes[i].active / shapes[i].nk > (double)shapes[best].active / shapes[best].nk * 1.02) best = i;
+  plan.main = shapes[best];
+  const int full = (B / plan.main.active) * plan.main.active;
+  const int rem = B - full;
+  plan.b_main = B;
+  if (rem > 0 && full > 0) {
+    // finish the remainder with whichever shape completes it first
+    double best_t = (double)plan.main.nk;  // one more (partial) wave of the main shape
+    for (int i = 0; i < ns; ++i) {
+      const double t = (double)((rem + shapes[i].active - 1) / shapes[i].active) * shapes[i].nk;
+      if (t < best_t * 0.95) {
+        best_t = t;
+        plan.tail = shapes[i];
+        plan.b_main = full;
+      }
     }
   }
-  return best;
+  return plan;
 }
 
 template <typename T, int N>
-static int launch_fused(const FusedArgs<T>& a, cudaStream_t s) {
-  FusedPlan p = plan_for<T, N>(a.K, a.B);
-  if (!p.cs) return fail(OCSC_EARG, "fused code ADMM: no cluster shape fits shared memory");
+static const FusedPlan& cached_plan(int K, int B) {
+  static std::map<std::tuple<int, int, int>, FusedPlan> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto key = std::make_tuple(dev, K, B);
+  auto it = cache.find(key);
+  if (it == cache.end()) it = cache.emplace(key, plan_for<T, N>(K, B)).first;
+  return it->second;
+}
+
+template <typename T, int N>
+static int launch_shape(FusedArgs<T> a, const FusedShape& sh, int b0, int nb, cudaStream_t s) {
+  if (nb <= 0) return OCSC_OK;
   auto kern = k_code_fused<T, N>;
-  OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-  if (p.cs > 8) OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem));
+  if (sh.cs > 8) OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  a.b0 = b0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.B * p.cs, 1, 1);
-  cfg.blockDim = dim3(p.threads, 1, 1);
-  cfg.dynamicSmemBytes = p.smem;
+  cfg.gridDim = dim3(nb * sh.cs, 1, 1);
+  cfg.blockDim = dim3(sh.threads, 1, 1);
+  cfg.dynamicSmemBytes = sh.smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.cs;
+  attr[0].val.clusterDim.x = sh.cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -455,36 +540,30 @@ static int launch_fused(const FusedArgs<T>& a, cudaStream_t s) {
 }
 
 template <typename T, int N>
+static int launch_fused(const FusedArgs<T>& a, cudaStream_t s) {
+  const FusedPlan& p = cached_plan<T, N>(a.K, a.B);
+  if (!p.main.cs) return fail(OCSC_EARG, "fused code ADMM: no cluster shape fits this device");
+  int rc = launch_shape<T, N>(a, p.main, 0, p.b_main, s);
+  if (rc) return rc;
+  return launch_shape<T, N>(a, p.tail, p.b_main, a.B - p.b_main, s);
+}
+
+template <typename T, int N>
 static int query_fused(int K, int B, int* info) {
-  FusedPlan p = plan_for<T, N>(K, B);
+  const FusedPlan& p = cached_plan<T, N>(K, B);
   if (info) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, k_code_fused<T, N>);
-    info[0] = p.cs;
-    info[1] = p.threads;
-    info[2] = (int)p.smem;
+    info[0] = p.main.cs;
+    info[1] = p.main.threads;
+    info[2] = (int)p.main.smem;
     info[3] = fa.numRegs;
-    info[4] = fa.maxThreadsPerBlock;
-    int clusters = 0;
-    if (p.cs) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(B * p.cs, 1, 1);
-      cfg.blockDim = dim3(p.threads, 1, 1);
-      cfg.dynamicSmemBytes = p.smem;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = p.cs;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaFuncSetAttribute(k_code_fused<T, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-      if (p.cs > 8) cudaFuncSetAttribute(k_code_fused<T, N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaOccupancyMaxActiveClusters(&clusters, k_code_fused<T, N>, &cfg);
-    }
-    info[5] = clusters;
+    info[4] = p.main.active;
+    info[5] = p.b_main;
+    info[6] = p.tail.cs;
+    info[7] = p.tail.active;
   }
-  return p.cs;
+  return p.main.cs;
 }
 
 // the grids the fused kernel is instantiated for (BASELINE config 1 is 42 x 42)
@@ -505,7 +584,7 @@ static int fused_dispatch(int H, int W, bool query, const FusedArgs<T>* a, int K
 using namespace ocsc;
 
 extern "C" int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32_t* info) {
-  for (int i = 0; i < 6; ++i) info[i] = 0;
+  for (int i = 0; i < 8; ++i) info[i] = 0;
   if (K <= 0 || B <= 0) return 0;
   if (dtype == OCSC_F32) return fused_dispatch<float>(H, W, true, nullptr, K, B, nullptr, info);
   if (dtype == OCSC_F64) return fused_dispatch<double>(H, W, true, nullptr, K, B, nullptr, info);
@@ -528,12 +607,12 @@ extern "C" int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void
   if (B == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
   if (dtype == OCSC_F32) {
-    FusedArgs<float> a{K, B, max_iters, rel_tol, beta, (float)(beta / rho), (const float2*)xh, (const float2*)Wh,
+    FusedArgs<float> a{K, B, max_iters, 0, rel_tol, beta, (float)(beta / rho), (const float2*)xh, (const float2*)Wh,
                        (const float*)den, (float*)u, (float*)t, (float2*)uh, obj, resid, iters, status};
     return fused_dispatch<float>(H, W, false, &a, K, B, s);
   }
   if (dtype == OCSC_F64) {
-    FusedArgs<double> a{K, B, max_iters, rel_tol, beta, beta / rho, (const double2*)xh, (const double2*)Wh,
+    FusedArgs<double> a{K, B, max_iters, 0, rel_tol, beta, beta / rho, (const double2*)xh, (const double2*)Wh,
                         (const double*)den, (double*)u, (double*)t, (double2*)uh, obj, resid, iters, status};
     return fused_dispatch<double>(H, W, false, &a, K, B, s);
   }

@@ -4,9 +4,9 @@
 // inverse ((1/t) sum z z^H + rho P I)^-1, refreshed by an O(K^3) solve per
 // sample (dictionary.py:73-114).  Here the state is the un-normalised sums
 //     S_p = sum_b z_bp z_bp^H  (packed lower, K(K+1)/2),   c_p = sum_b conj(x_bp) z_bp
-// updated by a rank-B accumulation per mini-batch; the inverse is rebuilt once per
-// mini-batch by a per-frequency Cholesky (A = S + t rho P I = L L^H) and an explicit
-// packed inverse, which the J dictionary rounds then apply as a Hermitian GEMV.
+// updated by a rank-B accumulation per mini-batch; the inverse of A = S + t rho P I is
+// rebuilt once per mini-batch per frequency (in-place Gauss-Jordan in shared memory) and
+// stored packed; the J dictionary rounds then apply it as a Hermitian GEMV.
 // Algebra: ((1/t)S + rho P I)^-1 = t (S + t rho P I)^-1, so the row solve
 // d = (conj(c/t) + rho P (v - theta)) . inv_gram  becomes
 // conj(d) = (S + t rho P I)^-1 (c + t rho P conj(v - theta)).
@@ -88,70 +88,172 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
 }
 
 // -------------------------------------------------------------- inversion --
-// One CTA per frequency, two packed K x K buffers in shared memory:
-// Cholesky in place, triangular inverse into the second, then A^-1 = L^-H L^-1
-// back into the first.
+// One CTA per frequency: A = S + ridge I expanded to a full K x K Hermitian matrix in shared
+// memory, inverted in place by Gauss-Jordan elimination (A is Hermitian positive definite,
+// so no pivoting is needed: every pivot is a positive Schur-complement diagonal).  Each of
+// the K steps is one fully parallel rank-1 update (three block barriers per step).
 template <typename Th>
-__global__ void __launch_bounds__(256) k_hist_invert(int K, const cx<Th>* __restrict__ S, Th ridge, Th scale,
+__global__ void __launch_bounds__(512) k_hist_invert(int K, const cx<Th>* __restrict__ S, Th ridge, Th scale,
                                                      cx<Th>* inv, int32_t* info) {
   using C = cx<Th>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t npk = (int64_t)K * (K + 1) / 2;
+  const int LD = K + 1;  // padded row stride
   C* A = reinterpret_cast<C*>(smem_raw);
-  C* Li = A + npk;
-  __shared__ Th inv_d;
+  C* rowk = A + (int64_t)K * LD;
+  C* colk = rowk + K;
+  __shared__ Th pinv_s;
   const int p = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t npk = (int64_t)K * (K + 1) / 2;
   const C* Sp = S + (int64_t)p * npk;
-  for (int64_t e = threadIdx.x; e < npk; e += blockDim.x) A[e] = Sp[e];
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    const int i = e / K, j = e % K;
+    C v = i >= j ? Sp[packed_index(i, j)] : cconj(Sp[packed_index(j, i)]);
+    if (i == j) v = mkc<C>(v.x + ridge, (Th)0);
+    A[i * LD + j] = v;
+  }
   __syncthreads();
-  for (int i = threadIdx.x; i < K; i += blockDim.x) A[packed_index(i, i)].x += ridge;
-  __syncthreads();
-  for (int j = 0; j < K; ++j) {
+  for (int k = 0; k < K; ++k) {
     if (threadIdx.x == 0) {
-      Th d = A[packed_index(j, j)].x;
-      if (!(d > (Th)0)) {
-        atomicCAS(info, 0, p + 1);
-        d = (Th)NAN;
+      const Th pv = A[k * LD + k].x;
+      if (!(pv > (Th)0)) atomicCAS(info, 0, p + 1);
+      pinv_s = (Th)1 / pv;
+    }
+    __syncthreads();
+    const Th pinv = pinv_s;
+    for (int j = threadIdx.x; j < K; j += blockDim.x) {
+      rowk[j] = cscale(A[k * LD + j], pinv);
+      colk[j] = A[j * LD + k];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = threadIdx.x >> 5; i < K; i += nw) {
+      C* Ai = A + i * LD;
+      if (i == k) {
+        for (int j = lane; j < K; j += 32) Ai[j] = j == k ? mkc<C>(pinv, (Th)0) : rowk[j];
+      } else {
+        const C ci = colk[i];
+        for (int j = lane; j < K; j += 32) {
+          if (j == k) {
+            Ai[j] = cscale(ci, -pinv);
+          } else {
+            const C rj = rowk[j];
+            C a = Ai[j];
+            a.x -= ci.x * rj.x - ci.y * rj.y;
+            a.y -= ci.x * rj.y + ci.y * rj.x;
+            Ai[j] = a;
+          }
+        }
       }
-      d = sqrt(d);
-      A[packed_index(j, j)] = mkc<C>(d, 0);
-      inv_d = (Th)1 / d;
     }
     __syncthreads();
-    for (int i = j + 1 + threadIdx.x; i < K; i += blockDim.x) A[packed_index(i, j)] = cscale(A[packed_index(i, j)], inv_d);
+  }
+  cx<Th>* out = inv + (int64_t)p * npk;
+  for (int64_t e = threadIdx.x; e < npk; e += blockDim.x) {
+    // packed (i, j), j <= i
+    int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+    while ((int64_t)i * (i + 1) / 2 > e) --i;
+    while ((int64_t)(i + 1) * (i + 2) / 2 <= e) ++i;
+    const int j = (int)(e - (int64_t)i * (i + 1) / 2);
+    out[e] = cscale(A[i * LD + j], scale);
+  }
+}
+
+// Register-blocked Gauss-Jordan for moderate K (the BASELINE K = 100): thread t owns the
+// BI x BJ block of A at (bi*BI, bj*BJ) in registers for all K steps; per step only row k and
+// column k travel through shared memory, so shared traffic is O(K) instead of O(K^2).
+template <typename Th, int BI, int BJ>
+__global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>* __restrict__ S, Th ridge, Th scale,
+                                                            cx<Th>* inv, int32_t* info) {
+  using C = cx<Th>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* rowk = reinterpret_cast<C*>(smem_raw);
+  C* colk = rowk + K;
+  const int p = blockIdx.x;
+  const int64_t npk = (int64_t)K * (K + 1) / 2;
+  const C* Sp = S + (int64_t)p * npk;
+  const int tjn = (K + BJ - 1) / BJ, tin = (K + BI - 1) / BI;
+  const int t = threadIdx.x;
+  const bool active = t < tin * tjn;
+  const int i0 = active ? (t / tjn) * BI : K, j0 = active ? (t % tjn) * BJ : K;
+  C a[BI][BJ];
+#pragma unroll
+  for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < BJ; ++jj) {
+      const int i = i0 + ii, j = j0 + jj;
+      C v = mkc<C>(0, 0);
+      if (i < K && j < K) {
+        v = i >= j ? Sp[packed_index(i, j)] : cconj(Sp[packed_index(j, i)]);
+        if (i == j) v = mkc<C>(v.x + ridge, (Th)0);
+      }
+      a[ii][jj] = v;
+    }
+  for (int k = 0; k < K; ++k) {
+    const bool own_row = k >= i0 && k < i0 + BI, own_col = k >= j0 && k < j0 + BJ;
+    // publish row k and column k (only their owners)
+    if (own_row) {
+#pragma unroll
+      for (int ii = 0; ii < BI; ++ii)
+        if (i0 + ii == k)
+#pragma unroll
+          for (int jj = 0; jj < BJ; ++jj)
+            if (j0 + jj < K) rowk[j0 + jj] = a[ii][jj];
+    }
+    if (own_col) {
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj)
+        if (j0 + jj == k)
+#pragma unroll
+          for (int ii = 0; ii < BI; ++ii)
+            if (i0 + ii < K) colk[i0 + ii] = a[ii][jj];
+    }
     __syncthreads();
-    for (int i = j + 1 + warp; i < K; i += nwarps) {
-      const C lij = A[packed_index(i, j)];
-      C* rowi = A + packed_index(i, 0);
-      for (int k = j + 1 + lane; k <= i; k += 32) {
-        const C lkj = A[packed_index(k, j)];
-        // A[i][k] -= L[i][j] conj(L[k][j])
-        rowi[k] = csub(rowi[k], mkc<C>(lij.x * lkj.x + lij.y * lkj.y, lij.y * lkj.x - lij.x * lkj.y));
+    const Th pinv = (Th)1 / rowk[k].x;
+    if (t == 0 && !(rowk[k].x > (Th)0)) atomicCAS(info, 0, p + 1);
+    // generic rank-1 update with row/column k masked out (ci = 0 on row k, rs = 0 on column k)
+    C rs[BJ];
+#pragma unroll
+    for (int jj = 0; jj < BJ; ++jj) {
+      const int j = j0 + jj;
+      rs[jj] = (j < K && j != k) ? cscale(rowk[j], pinv) : mkc<C>(0, 0);
+    }
+#pragma unroll
+    for (int ii = 0; ii < BI; ++ii) {
+      const int i = i0 + ii;
+      const C ci = (i < K && i != k) ? colk[i] : mkc<C>(0, 0);
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj) {
+        C& v = a[ii][jj];
+        v.x = fma(-ci.x, rs[jj].x, fma(ci.y, rs[jj].y, v.x));
+        v.y = fma(-ci.x, rs[jj].y, fma(-ci.y, rs[jj].x, v.y));
       }
     }
+    // row k -> scaled row, column k -> -scaled column, pivot -> 1/pivot (owners only)
+    if (own_row) {
+#pragma unroll
+      for (int ii = 0; ii < BI; ++ii)
+        if (i0 + ii == k)
+#pragma unroll
+          for (int jj = 0; jj < BJ; ++jj) a[ii][jj] = (j0 + jj == k) ? mkc<C>(pinv, (Th)0) : rs[jj];
+    }
+    if (own_col) {
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj)
+        if (j0 + jj == k)
+#pragma unroll
+          for (int ii = 0; ii < BI; ++ii)
+            if (i0 + ii != k && i0 + ii < K) a[ii][jj] = cscale(colk[i0 + ii], -pinv);
+    }
     __syncthreads();
   }
-  // Li = L^-1 (lower), column c by thread c
-  for (int col = threadIdx.x; col < K; col += blockDim.x) {
-    Li[packed_index(col, col)] = mkc<C>((Th)1 / A[packed_index(col, col)].x, 0);
-    for (int i = col + 1; i < K; ++i) {
-      C acc = mkc<C>(0, 0);
-      const C* rowi = A + packed_index(i, 0);
-      for (int k = col; k < i; ++k) cfma(acc, rowi[k], Li[packed_index(k, col)]);
-      Li[packed_index(i, col)] = cscale(acc, -(Th)1 / rowi[i].x);
+  cx<Th>* out = inv + (int64_t)p * npk;
+#pragma unroll
+  for (int ii = 0; ii < BI; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < BJ; ++jj) {
+      const int i = i0 + ii, j = j0 + jj;
+      if (i < K && j <= i) out[packed_index(i, j)] = cscale(a[ii][jj], scale);
     }
-  }
-  __syncthreads();
-  // A^-1[i][j] = sum_{k >= i} conj(Li[k][i]) Li[k][j]   (i >= j)
-  C* out = inv + (int64_t)p * npk;
-  for (int i = warp; i < K; i += nwarps) {
-    for (int j = lane; j <= i; j += 32) {
-      C acc = mkc<C>(0, 0);
-      for (int k = i; k < K; ++k) cfmac(acc, Li[packed_index(k, i)], Li[packed_index(k, j)]);
-      out[packed_index(i, j)] = cscale(acc, scale);
-    }
-  }
 }
 
 template <typename T>
@@ -243,15 +345,27 @@ extern "C" int ocsc_history_invert(int dtype_hist, int K, int nfreq, const void*
   cudaStream_t s = as_stream(stream);
   OCSC_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (nfreq == 0) return OCSC_OK;
-  const size_t smem = 2 * csize(dtype_hist) * (size_t)K * (K + 1) / 2;
+  if (K > 32 && K <= 100 && (dtype_hist == OCSC_F64 || dtype_hist == OCSC_F32)) {
+    // register-blocked path: 4 x 5 blocks, ceil(K/4) * ceil(K/5) <= 500 threads
+    const int threads = ((((K + 3) / 4) * ((K + 4) / 5)) + 31) / 32 * 32;
+    const size_t sm = csize(dtype_hist) * 2 * (size_t)K;
+    if (dtype_hist == OCSC_F64)
+      k_hist_invert_reg<double, 4, 5><<<nfreq, threads, sm, s>>>(K, (const double2*)S, ridge, scale, (double2*)inv, info);
+    else
+      k_hist_invert_reg<float, 4, 5><<<nfreq, threads, sm, s>>>(K, (const float2*)S, (float)ridge, (float)scale, (float2*)inv, info);
+    OCSC_LAUNCHED("k_hist_invert_reg");
+    return OCSC_OK;
+  }
+  const size_t smem = csize(dtype_hist) * ((size_t)K * (K + 1) + 2 * (size_t)K);
   if (smem > 227 * 1024)
-    return fail(OCSC_EARG, "history_invert: K=" + std::to_string(K) + " exceeds the shared-memory Cholesky (K<=120 f64, K<=170 f32)");
+    return fail(OCSC_EARG, "history_invert: K=" + std::to_string(K) +
+                               " exceeds the shared-memory inverse (K<=118 complex128, K<=167 complex64)");
   if (dtype_hist == OCSC_F32) {
     OCSC_CUDA(cudaFuncSetAttribute(k_hist_invert<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_hist_invert<float><<<nfreq, 256, smem, s>>>(K, (const float2*)S, (float)ridge, (float)scale, (float2*)inv, info);
+    k_hist_invert<float><<<nfreq, 512, smem, s>>>(K, (const float2*)S, (float)ridge, (float)scale, (float2*)inv, info);
   } else if (dtype_hist == OCSC_F64) {
     OCSC_CUDA(cudaFuncSetAttribute(k_hist_invert<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_hist_invert<double><<<nfreq, 256, smem, s>>>(K, (const double2*)S, ridge, scale, (double2*)inv, info);
+    k_hist_invert<double><<<nfreq, 512, smem, s>>>(K, (const double2*)S, ridge, scale, (double2*)inv, info);
   } else {
     return fail(OCSC_EARG, "dtype must be 4 or 8");
   }
