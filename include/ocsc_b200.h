@@ -118,6 +118,11 @@ int ocsc_code_fused_cluster(int dtype, int H, int W, int K, int B);
  * samples run with the main shape, tail cluster size (0 = none), tail resident clusters.
  * Returns the main cluster size (0 = unsupported). */
 int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32_t* info);
+/* Development aid: device buffer of 64 int64 that receives clock64() phase stamps of CTA 0
+ * for iterations 8..15 of the next fused launches (NULL disables). */
+int ocsc_debug_fused_profile(void* buf);
+/* Development aid: device buffer of 2*B int64 receiving %globaltimer at each sample's start/end. */
+int ocsc_debug_fused_timeline(void* buf);
 int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
                     const void* den, double beta, double rho, int max_iters, double rel_tol,
                     void* u, void* t, void* uh, double* obj, double* resid, int32_t* iters,

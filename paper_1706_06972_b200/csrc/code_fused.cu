@@ -32,6 +32,19 @@ namespace cg = cooperative_groups;
 
 namespace ocsc {
 
+// optional phase timestamps (development aid): CTA 0, thread 0, iterations 8..15
+__device__ long long* g_fused_prof = nullptr;
+__device__ long long* g_fused_timeline = nullptr;  // [sample][2]: globaltimer at start / end (CTA rank 0)
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define OCSC_STAMP(slot)                                                                       \
+  do {                                                                                         \
+    if (prof && pit >= 8 && pit < 16) prof[(pit - 8) * 8 + (slot)] = clock64();               \
+  } while (0)
+
 template <typename T>
 struct FusedArgs {
   int K, B, max_iters;
@@ -63,7 +76,9 @@ template <int N>
 struct Geo {
   static constexpr int M = N / 2;
   static constexpr int Wh = M + 1;
-  static constexpr int WP = N + 1;  // odd float row stride of w
+  // float row stride of w: even (float2 accesses) and odd in 8-byte units, so a warp of row
+  // tasks (one row per lane) hits 16 distinct 8-byte bank pairs per half-warp
+  static constexpr int WP = (N % 4 == 2) ? N + 2 : ((N % 4 == 0) ? N + 2 : N + 1);
   static constexpr int NF = N * Wh;
   // complex row stride of the workspace: odd, >= Wh, and N*RS == Wh (mod 16) when possible,
   // so the row tasks (lane -> row) and the column half-warps (lane -> column, running across
@@ -89,9 +104,15 @@ struct Smem {
   static __host__ __device__ size_t p_bytes(int cs) {
     return al(sizeof(cx<T>) * (size_t)cs * ((G::NF + cs - 1) / cs));
   }
-  static __host__ __device__ size_t n_bytes(int cs) { return al(sizeof(double) * 8 * (size_t)cs); }
+  // per-warp norm partials from every CTA of the cluster: [CS][32 warps][8] (arithmetic type)
+  static __host__ __device__ size_t n_bytes(int cs) { return al(sizeof(T) * 8 * 32 * (size_t)cs); }
+  // this CTA's slice of the sample spectrum and of den
+  static __host__ __device__ size_t s_bytes(int cs) {
+    const size_t sl = (G::NF + cs - 1) / cs;
+    return al(sizeof(cx<T>) * sl) + al(sizeof(T) * sl);
+  }
   static __host__ __device__ size_t total(int nk, int cs) {
-    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes(cs) + n_bytes(cs) + 6 * 32 * sizeof(double);
+    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes(cs) + n_bytes(cs) + s_bytes(cs) + 6 * 32 * sizeof(double);
   }
   static __host__ __device__ int threads(int nk) {
     const int wc = (nk * G::Wh + 15) / 16, wr = (nk * N + 31) / 32;
@@ -172,7 +193,6 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   using C = cx<T>;
   using G = Geo<N>;
   using S = Smem<T, N>;
-  using A = T;  // norm accumulators follow the arithmetic precision
   constexpr int M = G::M, Wh = G::Wh, WP = G::WP, RS = G::RS, PS = G::PS, NF = G::NF;
 
   cg::cluster_group cl = cg::this_cluster();
@@ -190,8 +210,11 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   C* X = reinterpret_cast<C*>(smem + off);    off += S::x_bytes(nkmax);
   C* gS = reinterpret_cast<C*>(smem + off);   off += S::g_bytes();
   C* part = reinterpret_cast<C*>(smem + off); off += S::p_bytes(CS);
-  double* norms = reinterpret_cast<double*>(smem + off);
-  double* scratch = norms + 8 * CS;
+  T* nrm = reinterpret_cast<T*>(smem + off); off += S::n_bytes(CS);
+  const int slice_ = (NF + CS - 1) / CS;
+  C* xsl = reinterpret_cast<C*>(smem + off);  off += S::al(sizeof(C) * slice_);
+  T* dsl = reinterpret_cast<T*>(smem + off);  off += S::al(sizeof(T) * slice_);
+  double* scratch = reinterpret_cast<double*>(smem + off);
 
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -214,6 +237,12 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
 
   for (int i = tid; i < nk * N * WP; i += nt) wS[i] = (T)0;
   for (int i = tid; i < nk * PS; i += nt) X[i] = mkc<C>(0, 0);
+  for (int i = tid; i < slice_; i += nt) {
+    const int f = r * slice_ + i;
+    xsl[i] = f < NF ? a.xh[(int64_t)b * NF + f] : mkc<C>(0, 0);
+    dsl[i] = f < NF ? (T)1 / a.den[f] : (T)0;
+  }
+  const int nwarps = nt >> 5;
   __syncthreads();
 
   // ---- column transform of item (cj, cv): Good-Thomas 2 x M across lanes l, l^16 ----------
@@ -243,7 +272,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       constexpr int kA = ((M + 1) * k2) % N;      // output row for h = 0; h = 1 is kA + sh*M
       constexpr int sh = (kA < M) ? 1 : -1;
       const C p = mkc<C>(__shfl_xor_sync(0xffffffffu, z[k2].x, 16), __shfl_xor_sync(0xffffffffu, z[k2].y, 16));
-      const C o = mkc<C>(fma(sgn, z[k2].x, p.x), fma(sgn, z[k2].y, p.y));  // h=0: z+p, h=1: p-z
+      const C o = vfma(z[k2], vsplat<C>(sgn), p);  // h=0: z+p, h=1: p-z
       if (cvalid) {
         const int ox = kA * RS + sh * dpx;
         if constexpr (mode == COL_I) {
@@ -277,87 +306,117 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   };
 
   int it = 0, stat = 0;
+  long long* prof = (blockIdx.x == 0 && tid == 0) ? g_fused_prof : nullptr;
+  long long* tl = (r == 0 && tid == 0) ? g_fused_timeline : nullptr;
+  if (tl) tl[2 * b] = global_ns();
   for (;;) {
+    const int pit = it;
     // ---- A: forward column transforms times D, partial synthesis ------------------------
+    OCSC_STAMP(0);
     col_phase(std::integral_constant<int, COL_F>{}, nullptr);
     __syncthreads();
+    OCSC_STAMP(1);
     reduce_push();
     cl.sync();  // #1: partials and the previous iteration's norms are visible
+    OCSC_STAMP(2);
+    // ---- y on my slice from the pushed partials, g = (X - y)/den, pushed to every rank -----
+    // (issued before the stopping decision so its latency overlaps; a stopping iteration just
+    // discards it)
+    {
+      const int f0 = r * slice, f1 = min(NF, f0 + slice);
+      for (int f = f0 + tid; f < f1; f += nt) {
+        const C y = gather_y(f);
+        const int fl = f - f0;
+        const C g = cscale(csub(xsl[fl], y), dsl[fl]);
+        const int o = (f / Wh) * RS + f % Wh;
+        for (int qq = 0; qq < CS; ++qq) cl.map_shared_rank(gS, qq)[o] = g;
+      }
+    }
     bool stop = false;
     if (it > 0) {
-      double n4[5] = {0, 0, 0, 0, 0};
-      for (int qq = 0; qq < CS; ++qq)
+      // every warp reduces the CS x nwarps partials in the same fixed order (lane-strided,
+      // then a fixed butterfly): identical decision everywhere, no block barrier
+      T n4[5] = {0, 0, 0, 0, 0};
+      for (int qq = 0; qq < CS; ++qq) {
+        if (lane < nwarps) {
+          const T* src = nrm + (qq * 32 + lane) * 8;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) n4[i] += norms[8 * qq + i];
-      if (n4[4] > 0.0) {
-        stat = 2;
-        stop = true;
-      } else {
-        const double num = sqrt(n4[0]), den = sqrt(n4[1]), gap = sqrt(n4[2]), dual = sqrt(n4[3]);
-        if (num <= a.tol * fmax(den, 1e-12) && gap <= a.tol * fmax(fmax(den, dual), 1e-12)) {
-          stat = 1;
-          stop = true;
+          for (int i = 0; i < 5; ++i) n4[i] += src[i];
         }
+      }
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) n4[i] += __shfl_xor_sync(0xffffffffu, n4[i], o);
+      // coding.py:113-118 on squared norms: num <= tol max(den, 1e-12) and
+      // gap <= tol max(den, |dual|, 1e-12)
+      const T tol2 = (T)(a.tol * a.tol), fl2 = (T)1e-24;
+      int st_ = 0;
+      if (n4[4] > (T)0) st_ = 2;
+      else if (n4[0] <= tol2 * fmax(n4[1], fl2) && n4[2] <= tol2 * fmax(fmax(n4[1], n4[3]), fl2)) st_ = 1;
+      OCSC_STAMP(3);
+      if (st_) {
+        stat = st_;
+        stop = true;
       }
     }
     if (!stop && it == a.max_iters) stop = true;
     if (stop) break;
     ++it;
-    // ---- y on my slice from the pushed partials, g = (X - y)/den, all-gather g ------------
-    {
-      const int f0 = r * slice, f1 = min(NF, f0 + slice);
-      const int nsl = f1 - f0;
-      for (int e = tid; e < nsl * CS; e += nt) {  // (frequency, destination) pairs
-        const int f = f0 + e % nsl, qq = e / nsl;
-        const C y = gather_y(f);
-        const T inv = (T)1 / a.den[f];
-        const C g = cscale(csub(a.xh[(int64_t)b * NF + f], y), inv);
-        cl.map_shared_rank(gS, qq)[(f / Wh) * RS + f % Wh] = g;
-      }
-    }
+    OCSC_STAMP(4);
     cl.sync();  // #2: g complete in every CTA
+    OCSC_STAMP(5);
     // ---- B: inverse column transforms of conj(D) g ---------------------------------------
     col_phase(std::integral_constant<int, COL_I>{}, nullptr);
     __syncthreads();
     // ---- C: row IFFT -> c -> update w (registers) -> t -> row FFT --------------------------
-    A s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    // (even, odd) pixel pairs run as 2-wide FP32x2 arithmetic
+    C s0 = mkc<C>(0, 0), s1 = mkc<C>(0, 0), s2 = mkc<C>(0, 0), s3 = mkc<C>(0, 0);
     bool bad = false;
     if (rvalid) {
       C z[M];
       row_inverse_pre<C, N>(xrow, z);
       sfft::fft<C, M, false>(z);
+      const C cs2 = mkc<C>(cscl, -cscl);  // c = (Re, -Im) * 2/P of the conjugated result
+      C* w2 = reinterpret_cast<C*>(wrow);
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        T tv[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const T c = (e ? -z[m].y : z[m].x) * cscl;
-          const T wo = wrow[2 * m + e];
-          const T go = clampk(wo, kappa), uo = wo - go;
-          const T wn = uo + c;
-          const T gn = clampk(wn, kappa), un = wn - gn;
-          const A d0 = (A)(un - uo), d2 = (A)(gn - go);  // a non-finite code poisons these sums
-          s0 = fma(d0, d0, s0);
-          s1 = fma((A)un, (A)un, s1);
-          s2 = fma(d2, d2, s2);
-          s3 = fma((A)gn, (A)gn, s3);
-          wrow[2 * m + e] = wn;
-          tv[e] = un - gn;
-        }
-        z[m] = mkc<C>(tv[0], tv[1]);
+        const C c = vmul(z[m], cs2);
+        const C wo = w2[m];
+        const C go = mkc<C>(clampk(wo.x, kappa), clampk(wo.y, kappa));
+        const C uo = vsub(wo, go);
+        const C wn = vadd(uo, c);
+        const C gn = mkc<C>(clampk(wn.x, kappa), clampk(wn.y, kappa));
+        const C un = vsub(wn, gn);
+        const C d0 = vsub(un, uo), d2 = vsub(gn, go);  // a non-finite code poisons these sums
+        s0 = vfma(d0, d0, s0);
+        s1 = vfma(un, un, s1);
+        s2 = vfma(d2, d2, s2);
+        s3 = vfma(gn, gn, s3);
+        w2[m] = wn;
+        z[m] = vsub(un, gn);  // t for the next iteration
       }
       sfft::fft<C, M, false>(z);
       row_forward_post<C, N>(z, xrow);
     }
-    // a non-finite code value poisons this thread's partial sums
-    bad = !isfinite(s0) || !isfinite(s1) || !isfinite(s2) || !isfinite(s3);
-    double nv[5] = {(double)s0, (double)s1, (double)s2, (double)s3, bad ? 1.0 : 0.0};
-    block_allsum<5>(nv, scratch);  // (contains the barrier that ends the row phase)
-    if (tid < CS) {
-      double* dst = cl.map_shared_rank(norms, tid) + 8 * r;
+    // a non-finite code value poisons this thread's partial sums; warp-reduce in float and
+    // push each warp's five partials straight into every CTA of the cluster (no block barrier)
+    {
+      T q[5] = {s0.x + s0.y, s1.x + s1.y, s2.x + s2.y, s3.x + s3.y, (T)0};
+      q[4] = (isfinite(q[0]) && isfinite(q[1]) && isfinite(q[2]) && isfinite(q[3])) ? (T)0 : (T)1;
 #pragma unroll
-      for (int i = 0; i < 5; ++i) dst[i] = nv[i];
+      for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
+      if (lane < CS) {
+        T* dst = cl.map_shared_rank(nrm, lane) + (r * 32 + warp) * 8;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) dst[i] = q[i];
+      }
     }
+    OCSC_STAMP(6);
+    __syncthreads();  // row outputs complete before the next column phase
+    OCSC_STAMP(7);
   }
 
   // ---- outputs: U = S(w) (and t), F(U), objective -------------------------------------------
@@ -367,9 +426,10 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     T* uo = a.u_out + rowoff;
     T* to = a.t_out ? a.t_out + rowoff : nullptr;
     C z[M];
+    const C* w2 = reinterpret_cast<const C*>(wrow);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const T va = wrow[2 * m], vb = wrow[2 * m + 1];
+      const T va = w2[m].x, vb = w2[m].y;
       const T ga = clampk(va, kappa), gb = clampk(vb, kappa);
       const T ua = va - ga, ub = vb - gb;
       uo[2 * m] = ua;
@@ -394,29 +454,31 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     const int f0 = r * slice, f1 = min(NF, f0 + slice);
     for (int f = f0 + tid; f < f1; f += nt) {
       const C y = gather_y(f);
-      const C res = csub(a.xh[(int64_t)b * NF + f], y);
+      const C res = csub(xsl[f - f0], y);
       e += herm_weight(f % Wh, N) * ((double)res.x * res.x + (double)res.y * res.y);
     }
   }
   double ev[2] = {e, l1};
   block_allsum<2>(ev, scratch);
+  double* fin = scratch + 6 * 32 - 2 * 16;  // [16][2] slots at the end of the scratch area
   if (tid == 0) {
-    double* dst = cl.map_shared_rank(norms, 0) + 8 * r;
-    dst[5] = ev[0];
-    dst[6] = ev[1];
+    double* dst = cl.map_shared_rank(fin, 0) + 2 * r;
+    dst[0] = ev[0];
+    dst[1] = ev[1];
   }
   cl.sync();
   if (r == 0 && tid == 0) {
     double energy = 0.0, l1s = 0.0;
     for (int qq = 0; qq < CS; ++qq) {
-      energy += norms[8 * qq + 5];
-      l1s += norms[8 * qq + 6];
+      energy += fin[2 * qq];
+      l1s += fin[2 * qq + 1];
     }
     const double invPd = 1.0 / ((double)N * N);
     a.obj[b] = 0.5 * invPd * energy + a.beta * l1s;
     if (a.resid) a.resid[b] = invPd * energy;
     a.iters[b] = it;
     a.status[b] = stat;
+    if (tl) tl[2 * b + 1] = global_ns();
   }
 }
 
@@ -582,6 +644,18 @@ static int fused_dispatch(int H, int W, bool query, const FusedArgs<T>* a, int K
 }  // namespace ocsc
 
 using namespace ocsc;
+
+extern "C" int ocsc_debug_fused_profile(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  OCSC_CUDA(cudaMemcpyToSymbol(g_fused_prof, &p, sizeof(p)));
+  return OCSC_OK;
+}
+
+extern "C" int ocsc_debug_fused_timeline(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  OCSC_CUDA(cudaMemcpyToSymbol(g_fused_timeline, &p, sizeof(p)));
+  return OCSC_OK;
+}
 
 extern "C" int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32_t* info) {
   for (int i = 0; i < 8; ++i) info[i] = 0;

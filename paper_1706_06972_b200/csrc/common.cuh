@@ -67,6 +67,19 @@ template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) {
   acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
 }
 
+// ---- 2-wide arithmetic: Blackwell FP32x2 (FADD2/FMUL2/FFMA2) for float2, plain for double2 ----
+__device__ __forceinline__ float2 vadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 vmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 vfma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 vsub(float2 a, float2 b) { return __ffma2_rn(b, make_float2(-1.f, -1.f), a); }
+__device__ __forceinline__ double2 vadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 vmul(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ double2 vfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+__device__ __forceinline__ double2 vsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+template <typename C> __device__ __forceinline__ C vsplat(decltype(C::x) s) { return mkc<C>(s, s); }
+
 template <typename To, typename From> __device__ __forceinline__ cx<To> ccast(From a) {
   return mkc<cx<To>>((To)a.x, (To)a.y);
 }

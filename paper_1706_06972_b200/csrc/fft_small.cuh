@@ -93,7 +93,8 @@ __device__ __forceinline__ C twiddle(C v) {
   }
 }
 
-// direct DFT of prime length R (R = 2 butterfly; odd R with the j <-> R-j pairing)
+// direct DFT of prime length R (R = 2 butterfly; odd R with the j <-> R-j pairing).
+// Complex adds and real-by-complex products run as 2-wide FP32x2 instructions.
 template <typename C, int R, bool INV>
 __device__ __forceinline__ void dft_prime(C (&x)[R]) {
   using T = decltype(C::x);
@@ -101,8 +102,8 @@ __device__ __forceinline__ void dft_prime(C (&x)[R]) {
     return;
   } else if constexpr (R == 2) {
     const C a = x[0], b = x[1];
-    x[0] = mkc<C>(a.x + b.x, a.y + b.y);
-    x[1] = mkc<C>(a.x - b.x, a.y - b.y);
+    x[0] = vadd(a, b);
+    x[1] = vsub(a, b);
   } else {
     constexpr int Hh = (R - 1) / 2;
     C s[Hh], d[Hh];
@@ -110,31 +111,28 @@ __device__ __forceinline__ void dft_prime(C (&x)[R]) {
     C sum = x0;
     static_for<1, Hh + 1>([&](auto J) {
       constexpr int j = decltype(J)::value;
-      s[j - 1] = mkc<C>(x[j].x + x[R - j].x, x[j].y + x[R - j].y);
-      d[j - 1] = mkc<C>(x[j].x - x[R - j].x, x[j].y - x[R - j].y);
-      sum.x += s[j - 1].x;
-      sum.y += s[j - 1].y;
+      s[j - 1] = vadd(x[j], x[R - j]);
+      d[j - 1] = vsub(x[j], x[R - j]);
+      sum = vadd(sum, s[j - 1]);
     });
     static_for<1, Hh + 1>([&](auto Kk) {
       constexpr int k = decltype(Kk)::value;
-      C a = x0;
-      T bx = 0, by = 0;
+      C a = x0, bsum = mkc<C>(0, 0);
       static_for<1, Hh + 1>([&](auto J) {
         constexpr int j = decltype(J)::value;
         constexpr T c = (T)ce_cos(2.0 * kPi * ((j * k) % R) / R);
         constexpr T sn = (T)ce_sin(2.0 * kPi * ((j * k) % R) / R);
-        a.x = fma(s[j - 1].x, c, a.x);
-        a.y = fma(s[j - 1].y, c, a.y);
-        bx = fma(d[j - 1].x, sn, bx);
-        by = fma(d[j - 1].y, sn, by);
+        a = vfma(s[j - 1], vsplat<C>(c), a);
+        if constexpr (j == 1) bsum = vmul(d[0], vsplat<C>(sn));
+        else bsum = vfma(d[j - 1], vsplat<C>(sn), bsum);
       });
       // forward: X[k] = a - i*b, X[R-k] = a + i*b (b = sum d_j sin); inverse swaps
       if constexpr (!INV) {
-        x[k] = mkc<C>(a.x + by, a.y - bx);
-        x[R - k] = mkc<C>(a.x - by, a.y + bx);
+        x[k] = mkc<C>(a.x + bsum.y, a.y - bsum.x);
+        x[R - k] = mkc<C>(a.x - bsum.y, a.y + bsum.x);
       } else {
-        x[k] = mkc<C>(a.x - by, a.y + bx);
-        x[R - k] = mkc<C>(a.x + by, a.y - bx);
+        x[k] = mkc<C>(a.x - bsum.y, a.y + bsum.x);
+        x[R - k] = mkc<C>(a.x + bsum.y, a.y - bsum.x);
       }
     });
     x[0] = sum;
