@@ -291,8 +291,14 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   auto reduce_push = [&]() {
     for (int f = tid; f < NF; f += nt) {
       const int o = (f / Wh) * RS + f % Wh;
-      C s = mkc<C>(0, 0);
-      for (int j = 0; j < nk; ++j) s = cadd(s, X[j * PS + o]);
+      C s = mkc<C>(0, 0), s2 = mkc<C>(0, 0);  // two chains: the loads issue back to back
+      int j = 0;
+      for (; j + 1 < nk; j += 2) {
+        s = vadd(s, X[j * PS + o]);
+        s2 = vadd(s2, X[(j + 1) * PS + o]);
+      }
+      if (j < nk) s = vadd(s, X[j * PS + o]);
+      s = vadd(s, s2);
       const int owner = f / slice;
       cl.map_shared_rank(part, owner)[r * slice + (f - owner * slice)] = s;
     }
@@ -317,6 +323,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     __syncthreads();
     OCSC_STAMP(1);
     reduce_push();
+    OCSC_STAMP(3);
     cl.sync();  // #1: partials and the previous iteration's norms are visible
     OCSC_STAMP(2);
     // ---- y on my slice from the pushed partials, g = (X - y)/den, pushed to every rank -----
@@ -354,7 +361,6 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       int st_ = 0;
       if (n4[4] > (T)0) st_ = 2;
       else if (n4[0] <= tol2 * fmax(n4[1], fl2) && n4[2] <= tol2 * fmax(fmax(n4[1], n4[3]), fl2)) st_ = 1;
-      OCSC_STAMP(3);
       if (st_) {
         stat = st_;
         stop = true;
