@@ -147,11 +147,13 @@ int ocsc_synthesize(int dtype, int K, int nfreq, int B, const void* Wh, const vo
 int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int nfreq, int B, const void* z,
                             int64_t z_sb, int64_t z_sk, int64_t z_sp, const void* x, int64_t x_sb,
                             int64_t x_sp, void* S, void* c, void* stream);
-/* inv_p = scale * (S_p + ridge I)^-1, per-frequency in-place Gauss-Jordan in shared memory
- * (HPD, no pivoting; packed in/out, K <= 118 for complex128).
- * info (device int32): 0, or 1 + first frequency whose matrix was not positive definite. */
-int ocsc_history_invert(int dtype_hist, int K, int nfreq, const void* S, double ridge, double scale,
-                        void* inv, int32_t* info, void* stream);
+/* inv_p = scale * (S_p + ridge I)^-1, per-frequency in-place Gauss-Jordan (HPD, no pivoting)
+ * in registers/shared memory, computed in dtype_hist and stored packed as dtype_inv
+ * (complex64 storage for float32 training halves the bytes the J row solves re-read).
+ * K <= 118 (complex128) / 167 (complex64).
+ * info (device int32): 0, or 1 + a frequency whose matrix was not positive definite. */
+int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfreq, const void* S, double ridge,
+                        double scale, void* inv, int32_t* info, void* stream);
 /* packed (nfreq, K(K+1)/2) Hermitian -> full (nfreq, K, K), times scale */
 int ocsc_packed_to_full(int dtype, int K, int nfreq, const void* packed, double scale, void* full,
                         void* stream);
@@ -164,8 +166,8 @@ int ocsc_nonfinite(int dtype, int64_t n_reals, const void* a, int32_t* flag, voi
 /* Row solve, dictionary.py:134-142, in sum form:
  * conj(D_p) = inv_p (c_p + ridge conj(V_p - Theta_p)), inv from ocsc_history_invert
  * with scale 1, ridge = t rho P.  V/Theta/D element (k,p) at [k*sk + p*sp]. */
-int ocsc_dict_rowsolve(int dtype, int dtype_hist, int K, int nfreq, const void* inv, const void* c,
-                       double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
+int ocsc_dict_rowsolve(int dtype, int dtype_hist, int dtype_inv, int K, int nfreq, const void* inv,
+                       const void* c, double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
                        void* Dh, void* stream);
 /* One fused projection round on half spectra (K, H, Wh), dictionary.py:145-154 + :205-207:
  * alpha_k = crop(irfft2(D_k + Theta_k)) / max(||.||, 1); V_k = rfft2(pad(alpha_k));

@@ -51,10 +51,10 @@ SIGNATURES = {
     "ocsc_code_objective": [_I, _I, _I, _I, _I, _P, _P, _P, _D, _P, _P, _P, _P],
     "ocsc_synthesize": [_I, _I, _I, _I, _P, _P, _P, _P],
     "ocsc_history_accumulate": [_I, _I, _I, _I, _I, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P],
-    "ocsc_history_invert": [_I, _I, _I, _P, _D, _D, _P, _P, _P],
+    "ocsc_history_invert": [_I, _I, _I, _I, _P, _D, _D, _P, _P, _P],
     "ocsc_packed_to_full": [_I, _I, _I, _P, _D, _P, _P],
     "ocsc_nonfinite": [_I, _I64, _P, _P, _P],
-    "ocsc_dict_rowsolve": [_I, _I, _I, _I, _P, _P, _D, _P, _P, _I64, _I64, _P, _P],
+    "ocsc_dict_rowsolve": [_I, _I, _I, _I, _I, _P, _P, _D, _P, _P, _I64, _I64, _P, _P],
     "ocsc_dict_project": [_I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "ocsc_crop_irfft": [_I, _I, _I, _I, _I, _I, _P, _P, _P],
     "ocsc_crop_normalize_cols": [_I, _I, _I, _I, _I, _I, _P, _P, _P],

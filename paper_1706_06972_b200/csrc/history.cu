@@ -23,10 +23,14 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
                                                     int64_t z_sb, int64_t z_sk, int64_t z_sp,
                                                     const cx<Tin>* __restrict__ x, int64_t x_sb, int64_t x_sp,
                                                     cx<Th>* S, cx<Th>* c) {
+  // products of one chunk of <= BC samples are formed in the input precision (FP32 FMAs in
+  // float32 mode: the chunk sum of <= 32 terms keeps ~1e-7 relative accuracy); the running
+  // history sums themselves are kept in the history precision
+  using Ci = cx<Tin>;
   using C = cx<Th>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* Zs = reinterpret_cast<C*>(smem_raw);  // [BC][K]
-  C* xs = Zs + (int64_t)BC * K;            // [BC]
+  Ci* Zs = reinterpret_cast<Ci*>(smem_raw);  // [BC][K]
+  Ci* xs = Zs + (int64_t)BC * K;             // [BC]
   const int p = blockIdx.x;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
   C* Sp = S + (int64_t)p * npk;
@@ -36,34 +40,33 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
     const int bc = min(BC, B - b0);
     for (int e = threadIdx.x; e < bc * K; e += blockDim.x) {
       const int bb = e / K, k = e % K;
-      Zs[bb * K + k] = ccast<Th>(z[(int64_t)(b0 + bb) * z_sb + (int64_t)k * z_sk + (int64_t)p * z_sp]);
+      Zs[bb * K + k] = z[(int64_t)(b0 + bb) * z_sb + (int64_t)k * z_sk + (int64_t)p * z_sp];
     }
-    for (int bb = threadIdx.x; bb < bc; bb += blockDim.x)
-      xs[bb] = ccast<Th>(x[(int64_t)(b0 + bb) * x_sb + (int64_t)p * x_sp]);
+    for (int bb = threadIdx.x; bb < bc; bb += blockDim.x) xs[bb] = x[(int64_t)(b0 + bb) * x_sb + (int64_t)p * x_sp];
     __syncthreads();
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
-      C acc = mkc<C>(0, 0);
+      Ci acc = mkc<Ci>(0, 0);
       for (int bb = 0; bb < bc; ++bb) cfmac(acc, xs[bb], Zs[bb * K + k]);
       C& dst = c[(int64_t)p * K + k];
-      dst = cadd(dst, acc);
+      dst = cadd(dst, ccast<Th>(acc));
     }
     for (int tile = threadIdx.x; tile < ntiles; tile += blockDim.x) {
       int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
       while (I * (I + 1) / 2 > tile) --I;
       while ((I + 1) * (I + 2) / 2 <= tile) ++I;
       const int J = tile - I * (I + 1) / 2;
-      C acc[4][4];
+      Ci acc[4][4];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[r][q] = mkc<C>(0, 0);
+        for (int q = 0; q < 4; ++q) acc[r][q] = mkc<Ci>(0, 0);
       for (int bb = 0; bb < bc; ++bb) {
-        C zi[4], zj[4];
+        Ci zi[4], zj[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int i = 4 * I + r, j = 4 * J + r;
-          zi[r] = i < K ? Zs[bb * K + i] : mkc<C>(0, 0);
-          zj[r] = j < K ? Zs[bb * K + j] : mkc<C>(0, 0);
+          zi[r] = i < K ? Zs[bb * K + i] : mkc<Ci>(0, 0);
+          zj[r] = j < K ? Zs[bb * K + j] : mkc<Ci>(0, 0);
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r)
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
           const int j = 4 * J + q;
           if (j > i) continue;
           C& dst = Sp[packed_index(i, j)];
-          dst = cadd(dst, acc[r][q]);
+          dst = cadd(dst, ccast<Th>(acc[r][q]));
         }
       }
     }
@@ -92,9 +95,9 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
 // memory, inverted in place by Gauss-Jordan elimination (A is Hermitian positive definite,
 // so no pivoting is needed: every pivot is a positive Schur-complement diagonal).  Each of
 // the K steps is one fully parallel rank-1 update (three block barriers per step).
-template <typename Th>
+template <typename Th, typename Ti>
 __global__ void __launch_bounds__(512) k_hist_invert(int K, const cx<Th>* __restrict__ S, Th ridge, Th scale,
-                                                     cx<Th>* inv, int32_t* info) {
+                                                     cx<Ti>* inv, int32_t* info) {
   using C = cx<Th>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int LD = K + 1;  // padded row stride
@@ -147,23 +150,23 @@ __global__ void __launch_bounds__(512) k_hist_invert(int K, const cx<Th>* __rest
     }
     __syncthreads();
   }
-  cx<Th>* out = inv + (int64_t)p * npk;
+  cx<Ti>* out = inv + (int64_t)p * npk;
   for (int64_t e = threadIdx.x; e < npk; e += blockDim.x) {
     // packed (i, j), j <= i
     int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
     while ((int64_t)i * (i + 1) / 2 > e) --i;
     while ((int64_t)(i + 1) * (i + 2) / 2 <= e) ++i;
     const int j = (int)(e - (int64_t)i * (i + 1) / 2);
-    out[e] = cscale(A[i * LD + j], scale);
+    out[e] = ccast<Ti>(cscale(A[i * LD + j], scale));
   }
 }
 
 // Register-blocked Gauss-Jordan for moderate K (the BASELINE K = 100): thread t owns the
 // BI x BJ block of A at (bi*BI, bj*BJ) in registers for all K steps; per step only row k and
 // column k travel through shared memory, so shared traffic is O(K) instead of O(K^2).
-template <typename Th, int BI, int BJ>
+template <typename Th, typename Ti, int BI, int BJ>
 __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>* __restrict__ S, Th ridge, Th scale,
-                                                            cx<Th>* inv, int32_t* info) {
+                                                            cx<Ti>* inv, int32_t* info) {
   using C = cx<Th>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* rowk = reinterpret_cast<C*>(smem_raw);
@@ -246,13 +249,13 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
     }
     __syncthreads();
   }
-  cx<Th>* out = inv + (int64_t)p * npk;
+  cx<Ti>* out = inv + (int64_t)p * npk;
 #pragma unroll
   for (int ii = 0; ii < BI; ++ii)
 #pragma unroll
     for (int jj = 0; jj < BJ; ++jj) {
       const int i = i0 + ii, j = j0 + jj;
-      if (i < K && j <= i) out[packed_index(i, j)] = cscale(a[ii][jj], scale);
+      if (i < K && j <= i) out[packed_index(i, j)] = ccast<Ti>(cscale(a[ii][jj], scale));
     }
 }
 
@@ -280,8 +283,8 @@ __global__ void k_nonfinite(int64_t n, const T* a, int32_t* flag) {
 
 // ------------------------------------------------------------- row solve --
 // One CTA per frequency; thread j forms row j of the packed Hermitian GEMV.
-template <typename Tc, typename Th>
-__global__ void __launch_bounds__(128) k_rowsolve(int K, int nf, const cx<Th>* __restrict__ inv,
+template <typename Tc, typename Th, typename Ti>
+__global__ void __launch_bounds__(128) k_rowsolve(int K, int nf, const cx<Ti>* __restrict__ inv,
                                                   const cx<Th>* __restrict__ c, Th ridge,
                                                   const cx<Tc>* __restrict__ Vh, const cx<Tc>* __restrict__ Th_,
                                                   int64_t sk, int64_t sp, cx<Tc>* Dh) {
@@ -297,12 +300,12 @@ __global__ void __launch_bounds__(128) k_rowsolve(int K, int nf, const cx<Th>* _
     rhs[k] = mkc<C>(ck.x + ridge * v.x, ck.y - ridge * v.y);
   }
   __syncthreads();
-  const C* Ap = inv + (int64_t)p * npk;
+  const cx<Ti>* Ap = inv + (int64_t)p * npk;
   for (int j = threadIdx.x; j < K; j += blockDim.x) {
     C acc = mkc<C>(0, 0);
-    const C* row = Ap + packed_index(j, 0);
-    for (int k = 0; k <= j; ++k) cfma(acc, row[k], rhs[k]);
-    for (int k = j + 1; k < K; ++k) cfmac(acc, Ap[packed_index(k, j)], rhs[k]);
+    const cx<Ti>* row = Ap + packed_index(j, 0);
+    for (int k = 0; k <= j; ++k) cfma(acc, ccast<Th>(row[k]), rhs[k]);
+    for (int k = j + 1; k < K; ++k) cfmac(acc, ccast<Th>(Ap[packed_index(k, j)]), rhs[k]);
     Dh[(int64_t)j * sk + (int64_t)p * sp] = mkc<cx<Tc>>((Tc)acc.x, (Tc)-acc.y);
   }
 }
@@ -319,7 +322,7 @@ extern "C" int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int 
   if (K <= 0 || nfreq < 0 || B < 0) return fail(OCSC_ESHAPE, "history_accumulate: bad extents");
   if (nfreq == 0 || B == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
-  const size_t cs = csize(dtype_hist);
+  const size_t cs = csize(dtype_in);
   int BC = (int)((160 * 1024) / (cs * (K + 1)));
   if (BC > 32) BC = 32;
   if (BC < 1) return fail(OCSC_EARG, "history_accumulate: K too large for one CTA");
@@ -339,38 +342,38 @@ extern "C" int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int 
   return OCSC_OK;
 }
 
-extern "C" int ocsc_history_invert(int dtype_hist, int K, int nfreq, const void* S, double ridge, double scale,
-                                   void* inv, int32_t* info, void* stream) {
+template <typename Th, typename Ti>
+static int launch_invert(int K, int nfreq, const void* S, double ridge, double scale, void* inv, int32_t* info,
+                         cudaStream_t s) {
+  if (K > 32 && K <= 100) {
+    // register-blocked path: 4 x 5 blocks, ceil(K/4) * ceil(K/5) <= 500 threads
+    const int threads = ((((K + 3) / 4) * ((K + 4) / 5)) + 31) / 32 * 32;
+    const size_t sm = sizeof(cx<Th>) * 2 * (size_t)K;
+    k_hist_invert_reg<Th, Ti, 4, 5><<<nfreq, threads, sm, s>>>(K, (const cx<Th>*)S, (Th)ridge, (Th)scale,
+                                                              (cx<Ti>*)inv, info);
+    OCSC_LAUNCHED("k_hist_invert_reg");
+    return OCSC_OK;
+  }
+  const size_t smem = sizeof(cx<Th>) * ((size_t)K * (K + 1) + 2 * (size_t)K);
+  if (smem > 227 * 1024)
+    return fail(OCSC_EARG, "history_invert: K=" + std::to_string(K) +
+                               " exceeds the shared-memory inverse (K<=118 complex128, K<=167 complex64)");
+  OCSC_CUDA(cudaFuncSetAttribute(k_hist_invert<Th, Ti>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_hist_invert<Th, Ti><<<nfreq, 512, smem, s>>>(K, (const cx<Th>*)S, (Th)ridge, (Th)scale, (cx<Ti>*)inv, info);
+  OCSC_LAUNCHED("k_hist_invert");
+  return OCSC_OK;
+}
+
+extern "C" int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfreq, const void* S, double ridge,
+                                   double scale, void* inv, int32_t* info, void* stream) {
   if (K <= 0 || nfreq < 0) return fail(OCSC_ESHAPE, "history_invert: bad extents");
   cudaStream_t s = as_stream(stream);
   OCSC_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (nfreq == 0) return OCSC_OK;
-  if (K > 32 && K <= 100 && (dtype_hist == OCSC_F64 || dtype_hist == OCSC_F32)) {
-    // register-blocked path: 4 x 5 blocks, ceil(K/4) * ceil(K/5) <= 500 threads
-    const int threads = ((((K + 3) / 4) * ((K + 4) / 5)) + 31) / 32 * 32;
-    const size_t sm = csize(dtype_hist) * 2 * (size_t)K;
-    if (dtype_hist == OCSC_F64)
-      k_hist_invert_reg<double, 4, 5><<<nfreq, threads, sm, s>>>(K, (const double2*)S, ridge, scale, (double2*)inv, info);
-    else
-      k_hist_invert_reg<float, 4, 5><<<nfreq, threads, sm, s>>>(K, (const float2*)S, (float)ridge, (float)scale, (float2*)inv, info);
-    OCSC_LAUNCHED("k_hist_invert_reg");
-    return OCSC_OK;
-  }
-  const size_t smem = csize(dtype_hist) * ((size_t)K * (K + 1) + 2 * (size_t)K);
-  if (smem > 227 * 1024)
-    return fail(OCSC_EARG, "history_invert: K=" + std::to_string(K) +
-                               " exceeds the shared-memory inverse (K<=118 complex128, K<=167 complex64)");
-  if (dtype_hist == OCSC_F32) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_hist_invert<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_hist_invert<float><<<nfreq, 512, smem, s>>>(K, (const float2*)S, (float)ridge, (float)scale, (float2*)inv, info);
-  } else if (dtype_hist == OCSC_F64) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_hist_invert<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_hist_invert<double><<<nfreq, 512, smem, s>>>(K, (const double2*)S, ridge, scale, (double2*)inv, info);
-  } else {
-    return fail(OCSC_EARG, "dtype must be 4 or 8");
-  }
-  OCSC_LAUNCHED("k_hist_invert");
-  return OCSC_OK;
+  if (dtype_hist == OCSC_F64 && dtype_inv == OCSC_F64) return launch_invert<double, double>(K, nfreq, S, ridge, scale, inv, info, s);
+  if (dtype_hist == OCSC_F64 && dtype_inv == OCSC_F32) return launch_invert<double, float>(K, nfreq, S, ridge, scale, inv, info, s);
+  if (dtype_hist == OCSC_F32 && dtype_inv == OCSC_F32) return launch_invert<float, float>(K, nfreq, S, ridge, scale, inv, info, s);
+  return fail(OCSC_EARG, "history_invert: unsupported dtype pair");
 }
 
 extern "C" int ocsc_packed_to_full(int dtype, int K, int nfreq, const void* packed, double scale, void* full,
@@ -401,20 +404,21 @@ extern "C" int ocsc_nonfinite(int dtype, int64_t n_reals, const void* a, int32_t
   return OCSC_OK;
 }
 
-extern "C" int ocsc_dict_rowsolve(int dtype, int dtype_hist, int K, int nfreq, const void* inv, const void* c,
-                                  double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp, void* Dh,
-                                  void* stream) {
+extern "C" int ocsc_dict_rowsolve(int dtype, int dtype_hist, int dtype_inv, int K, int nfreq, const void* inv,
+                                  const void* c, double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
+                                  void* Dh, void* stream) {
   if (K <= 0 || nfreq < 0) return fail(OCSC_ESHAPE, "dict_rowsolve: bad extents");
   if (nfreq == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
   const size_t smem = csize(dtype_hist) * K;
-#define RS(TC, TH)                                                                                       \
-  k_rowsolve<TC, TH><<<nfreq, 128, smem, s>>>(K, nfreq, (const cx<TH>*)inv, (const cx<TH>*)c, (TH)ridge, \
-                                              (const cx<TC>*)Vh, (const cx<TC>*)Th, sk, sp, (cx<TC>*)Dh)
-  if (dtype == OCSC_F32 && dtype_hist == OCSC_F32) RS(float, float);
-  else if (dtype == OCSC_F32 && dtype_hist == OCSC_F64) RS(float, double);
-  else if (dtype == OCSC_F64 && dtype_hist == OCSC_F64) RS(double, double);
-  else return fail(OCSC_EARG, "dict_rowsolve: unsupported dtype pair");
+#define RS(TC, TH, TI)                                                                                   \
+  k_rowsolve<TC, TH, TI><<<nfreq, 128, smem, s>>>(K, nfreq, (const cx<TI>*)inv, (const cx<TH>*)c, (TH)ridge, \
+                                                  (const cx<TC>*)Vh, (const cx<TC>*)Th, sk, sp, (cx<TC>*)Dh)
+  if (dtype == OCSC_F32 && dtype_hist == OCSC_F32 && dtype_inv == OCSC_F32) RS(float, float, float);
+  else if (dtype == OCSC_F32 && dtype_hist == OCSC_F64 && dtype_inv == OCSC_F64) RS(float, double, double);
+  else if (dtype == OCSC_F32 && dtype_hist == OCSC_F64 && dtype_inv == OCSC_F32) RS(float, double, float);
+  else if (dtype == OCSC_F64 && dtype_hist == OCSC_F64 && dtype_inv == OCSC_F64) RS(double, double, double);
+  else return fail(OCSC_EARG, "dict_rowsolve: unsupported dtype combination");
 #undef RS
   OCSC_LAUNCHED("k_rowsolve");
   return OCSC_OK;

@@ -9,7 +9,8 @@ un-normalised sums
     c_p = sum conj(x_p) z_p
 
 which a rank-B kernel updates per mini-batch, and rebuilds the regularised
-inverse by a per-frequency Cholesky only when a dictionary update needs it.
+inverse (per-frequency in-place Gauss-Jordan on the HPD matrix, in registers /
+shared memory) only when a dictionary update needs it.
 The reference's `cross` and `inv_gram` are derived views (c/t and
 t (S + t rho P I)^-1), bit-for-bit the same quantities up to rounding.
 
@@ -45,7 +46,7 @@ class HistoryState:
     """Running frequency-domain summary of all samples seen (dictionary.py:30-54)."""
 
     def __init__(self, shape: SignalShape, n_filters: int, rho: float, nfreq: int | None = None,
-                 dtype: torch.dtype = torch.complex128):
+                 dtype: torch.dtype = torch.complex128, inv_dtype: torch.dtype | None = None):
         self.shape = shape
         self.rho = float(rho)
         self.count = 0
@@ -54,6 +55,7 @@ class HistoryState:
         dev = _lib.device()
         self.S = torch.zeros((self.nfreq, _npk(self.K)), dtype=dtype, device=dev)
         self.c = torch.zeros((self.nfreq, self.K), dtype=dtype, device=dev)
+        self.inv_dtype = dtype if inv_dtype is None else inv_dtype
         self._inv = None          # packed (S + t rho P I)^-1, valid for count == _inv_count
         self._inv_count = -1
         self._info = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -84,8 +86,9 @@ class HistoryState:
         """(P, K, K) exact inverse of (averaged Gram + rho P I)."""
         if self.count == 0:
             return np.zeros((self.nfreq, self.K, self.K), dtype=np.complex128)
-        full = torch.empty((self.nfreq, self.K, self.K), dtype=self.S.dtype, device=self.S.device)
-        _lib.call("ocsc_packed_to_full", _lib.code(self.S.dtype), self.K, self.nfreq, _lib.ptr(self.inverse()),
+        inv = self.inverse()
+        full = torch.empty((self.nfreq, self.K, self.K), dtype=inv.dtype, device=inv.device)
+        _lib.call("ocsc_packed_to_full", _lib.code(inv.dtype), self.K, self.nfreq, _lib.ptr(inv),
                   float(self.count), _lib.ptr(full), _lib.stream())
         return _np(full).astype(np.complex128)
 
@@ -109,10 +112,11 @@ class HistoryState:
     def inverse(self, check: bool = True) -> torch.Tensor:
         """Packed (S + t rho P I)^-1 for the current count (cached)."""
         if self._inv is None:
-            self._inv = torch.empty_like(self.S)
+            self._inv = torch.empty(self.S.shape, dtype=self.inv_dtype, device=self.S.device)
         if self._inv_count != self.count:
-            _lib.call("ocsc_history_invert", _lib.code(self.S.dtype), self.K, self.nfreq, _lib.ptr(self.S),
-                      self.count * self.ridge, 1.0, _lib.ptr(self._inv), _lib.ptr(self._info), _lib.stream())
+            _lib.call("ocsc_history_invert", _lib.code(self.S.dtype), _lib.code(self.inv_dtype), self.K, self.nfreq,
+                      _lib.ptr(self.S), self.count * self.ridge, 1.0, _lib.ptr(self._inv), _lib.ptr(self._info),
+                      _lib.stream())
             self._inv_count = self.count
             if check and int(self._info.cpu()[0]) != 0:
                 raise DivergenceError("history Gram matrix lost positive definiteness")
@@ -162,7 +166,8 @@ def batch_history(z_freqs, x_freqs, shape: SignalShape, rho: float = 10.0) -> Hi
 def _rowsolve_dev(h: HistoryState, vh: torch.Tensor, th: torch.Tensor, sk: int, sp: int) -> torch.Tensor:
     inv = h.inverse()
     out = torch.empty_like(vh)
-    _lib.call("ocsc_dict_rowsolve", _lib.code(vh.dtype), _lib.code(h.S.dtype), h.K, h.nfreq, _lib.ptr(inv),
+    _lib.call("ocsc_dict_rowsolve", _lib.code(vh.dtype), _lib.code(h.S.dtype), _lib.code(inv.dtype), h.K, h.nfreq,
+              _lib.ptr(inv),
               _lib.ptr(h.c), h.count * h.ridge, _lib.ptr(vh), _lib.ptr(th), sk, sp, _lib.ptr(out), _lib.stream())
     return out
 

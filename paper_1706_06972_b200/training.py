@@ -141,8 +141,9 @@ class _HalfHistory(HistoryState):
     def inv_gram(self) -> np.ndarray:
         if self.count == 0:
             return np.zeros((self.shape.size, self.K, self.K), dtype=np.complex128)
-        full = torch.empty((self.nfreq, self.K, self.K), dtype=self.S.dtype, device=self.S.device)
-        _lib.call("ocsc_packed_to_full", _lib.code(self.S.dtype), self.K, self.nfreq, _lib.ptr(self.inverse()),
+        inv = self.inverse()
+        full = torch.empty((self.nfreq, self.K, self.K), dtype=inv.dtype, device=inv.device)
+        _lib.call("ocsc_packed_to_full", _lib.code(inv.dtype), self.K, self.nfreq, _lib.ptr(inv),
                   float(self.count), _lib.ptr(full), _lib.stream())
         return _np(self._extend(full)).astype(np.complex128)
 
@@ -175,7 +176,9 @@ class OnlineTrainer:
         self.Dh = self.Wh.clone()
         self.Th = torch.zeros_like(self.Wh)
         self.den = code_den(self.Wh, self.coding_config.rho)
-        self.history = _HalfHistory(shape, K, config.rho_dict, nfreq=self.nf, dtype=hist_cdtype)
+        # the inverse the J row solves re-read is stored at the arithmetic precision
+        self.history = _HalfHistory(shape, K, config.rho_dict, nfreq=self.nf, dtype=hist_cdtype,
+                                    inv_dtype=self.cdtype)
         self.rng = np.random.default_rng(config.seed)
         self._prev_code = None
         self._prev_alpha = self.alpha.clone()
@@ -233,11 +236,11 @@ class OnlineTrainer:
         h = self.history
         inv = h.inverse(check=False)
         ridge = h.count * h.ridge
-        dt, ht = _lib.code(self.dtype), _lib.code(h.S.dtype)
+        dt, ht, it_ = _lib.code(self.dtype), _lib.code(h.S.dtype), _lib.code(inv.dtype)
         s = _lib.stream()
         self.Th.zero_()
         for _ in range(J):
-            _lib.call("ocsc_dict_rowsolve", dt, ht, self.K, self.nf, _lib.ptr(inv), _lib.ptr(h.c), ridge,
+            _lib.call("ocsc_dict_rowsolve", dt, ht, it_, self.K, self.nf, _lib.ptr(inv), _lib.ptr(h.c), ridge,
                       _lib.ptr(self.Wh), _lib.ptr(self.Th), self.nf, 1, _lib.ptr(self.Dh), s)
             _lib.call("ocsc_dict_project", dt, self.H, self.W, self.M0, self.M1, self.K, _lib.ptr(self.Dh),
                       _lib.ptr(self.Th), _lib.ptr(self.Wh), _lib.ptr(self.alpha), s)
