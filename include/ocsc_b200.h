@@ -154,6 +154,13 @@ int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int nfreq, int 
  * info (device int32): 0, or 1 + a frequency whose matrix was not positive definite. */
 int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfreq, const void* S, double ridge,
                         double scale, void* inv, int32_t* info, void* stream);
+/* Large K (multiple of 32; BASELINE configs 3-4): blocked right-looking Cholesky of
+ * S_p + ridge I per frequency (one CTA per frequency, 32x32 tiles, panel staged in shared
+ * memory, one warp per trailing tile).  L is written full (nfreq, K, K), lower triangle;
+ * ocsc_history_factor_bytes gives its size.  info as ocsc_history_invert. */
+size_t ocsc_history_factor_bytes(int dtype_hist, int K, int nfreq);
+int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void* S, double ridge, void* L,
+                        int32_t* info, void* stream);
 /* packed (nfreq, K(K+1)/2) Hermitian -> full (nfreq, K, K), times scale */
 int ocsc_packed_to_full(int dtype, int K, int nfreq, const void* packed, double scale, void* full,
                         void* stream);
@@ -169,6 +176,11 @@ int ocsc_nonfinite(int dtype, int64_t n_reals, const void* a, int32_t* flag, voi
 int ocsc_dict_rowsolve(int dtype, int dtype_hist, int dtype_inv, int K, int nfreq, const void* inv,
                        const void* c, double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
                        void* Dh, void* stream);
+/* Row solve with the Cholesky factor of ocsc_history_factor (two triangular solves per
+ * frequency): conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)). */
+int ocsc_dict_rowsolve_chol(int dtype, int dtype_hist, int K, int nfreq, const void* L, const void* c,
+                            double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
+                            void* Dh, void* stream);
 /* One fused projection round on half spectra (K, H, Wh), dictionary.py:145-154 + :205-207:
  * alpha_k = crop(irfft2(D_k + Theta_k)) / max(||.||, 1); V_k = rfft2(pad(alpha_k));
  * Theta_k += D_k - V_k.  Pruned separable DFTs: only the M0 x M1 support is touched.

@@ -53,6 +53,9 @@ SIGNATURES = {
     "ocsc_history_accumulate": [_I, _I, _I, _I, _I, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P],
     "ocsc_history_invert": [_I, _I, _I, _I, _P, _D, _D, _P, _P, _P],
     "ocsc_packed_to_full": [_I, _I, _I, _P, _D, _P, _P],
+    "ocsc_history_factor_bytes": [_I, _I, _I],
+    "ocsc_history_factor": [_I, _I, _I, _P, _D, _P, _P, _P],
+    "ocsc_dict_rowsolve_chol": [_I, _I, _I, _I, _P, _P, _D, _P, _P, _I64, _I64, _P, _P],
     "ocsc_nonfinite": [_I, _I64, _P, _P, _P],
     "ocsc_dict_rowsolve": [_I, _I, _I, _I, _I, _P, _P, _D, _P, _P, _I64, _I64, _P, _P],
     "ocsc_dict_project": [_I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
@@ -61,7 +64,7 @@ SIGNATURES = {
     "ocsc_support_rfft": [_I, _I, _I, _I, _I, _I, _P, _P, _P],
     "ocsc_norms2": [_I, _I64, _P, _P, _P, _P],
 }
-_RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ,
+_RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ, "ocsc_history_factor_bytes": _SZ,
              "ocsc_kernel_launches": ctypes.c_int64}
 
 _lib = None

@@ -45,8 +45,12 @@ def _npk(K: int) -> int:
 class HistoryState:
     """Running frequency-domain summary of all samples seen (dictionary.py:30-54)."""
 
+    # largest K the in-register / shared-memory Gauss-Jordan inverse handles, per history dtype
+    GJ_MAX_K = {torch.complex128: 118, torch.complex64: 167}
+
     def __init__(self, shape: SignalShape, n_filters: int, rho: float, nfreq: int | None = None,
-                 dtype: torch.dtype = torch.complex128, inv_dtype: torch.dtype | None = None):
+                 dtype: torch.dtype = torch.complex128, inv_dtype: torch.dtype | None = None,
+                 solver: str = "auto"):
         self.shape = shape
         self.rho = float(rho)
         self.count = 0
@@ -56,6 +60,11 @@ class HistoryState:
         self.S = torch.zeros((self.nfreq, _npk(self.K)), dtype=dtype, device=dev)
         self.c = torch.zeros((self.nfreq, self.K), dtype=dtype, device=dev)
         self.inv_dtype = dtype if inv_dtype is None else inv_dtype
+        if solver == "auto":
+            solver = "gj" if self.K <= self.GJ_MAX_K[dtype] else "chol"
+        if solver == "chol" and self.K % 32:
+            raise ValueError(f"the blocked Cholesky path needs K % 32 == 0 (K={self.K})")
+        self.solver = solver      # "gj": explicit packed inverse; "chol": blocked Cholesky factor
         self._inv = None          # packed (S + t rho P I)^-1, valid for count == _inv_count
         self._inv_count = -1
         self._info = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -109,8 +118,40 @@ class HistoryState:
                   _lib.stream())
         self.count += B
 
+    def factor(self, check: bool = True) -> torch.Tensor:
+        """Full-layout Cholesky factor L of S + t rho P I (large-K path, cached)."""
+        if self._inv is None:
+            nbytes = _lib.load().ocsc_history_factor_bytes(_lib.code(self.S.dtype), self.K, self.nfreq)
+            self._inv = torch.empty((self.nfreq, self.K, self.K), dtype=self.S.dtype, device=self.S.device)
+            assert self._inv.numel() * self._inv.element_size() == nbytes
+        if self._inv_count != self.count:
+            _lib.call("ocsc_history_factor", _lib.code(self.S.dtype), self.K, self.nfreq, _lib.ptr(self.S),
+                      self.count * self.ridge, _lib.ptr(self._inv), _lib.ptr(self._info), _lib.stream())
+            self._inv_count = self.count
+            if check and int(self._info.cpu()[0]) != 0:
+                raise DivergenceError("history Gram matrix lost positive definiteness")
+        return self._inv
+
+    def rowsolve(self, vh: torch.Tensor, th: torch.Tensor, sk: int, sp: int, out: torch.Tensor,
+                 check: bool = True) -> torch.Tensor:
+        """conj(D_p) = (S + t rho P I)^-1 (c_p + t rho P conj(V_p - Theta_p)) into `out` (row solve)."""
+        ridge = self.count * self.ridge
+        if self.solver == "chol":
+            L = self.factor(check)
+            _lib.call("ocsc_dict_rowsolve_chol", _lib.code(vh.dtype), _lib.code(self.S.dtype), self.K, self.nfreq,
+                      _lib.ptr(L), _lib.ptr(self.c), ridge, _lib.ptr(vh), _lib.ptr(th), sk, sp, _lib.ptr(out),
+                      _lib.stream())
+        else:
+            inv = self.inverse(check)
+            _lib.call("ocsc_dict_rowsolve", _lib.code(vh.dtype), _lib.code(self.S.dtype), _lib.code(inv.dtype),
+                      self.K, self.nfreq, _lib.ptr(inv), _lib.ptr(self.c), ridge, _lib.ptr(vh), _lib.ptr(th), sk, sp,
+                      _lib.ptr(out), _lib.stream())
+        return out
+
     def inverse(self, check: bool = True) -> torch.Tensor:
         """Packed (S + t rho P I)^-1 for the current count (cached)."""
+        if self.solver != "gj":
+            raise ValueError(f"explicit inverse not available on the blocked Cholesky path (K={self.K})")
         if self._inv is None:
             self._inv = torch.empty(self.S.shape, dtype=self.inv_dtype, device=self.S.device)
         if self._inv_count != self.count:
@@ -164,12 +205,7 @@ def batch_history(z_freqs, x_freqs, shape: SignalShape, rho: float = 10.0) -> Hi
 
 
 def _rowsolve_dev(h: HistoryState, vh: torch.Tensor, th: torch.Tensor, sk: int, sp: int) -> torch.Tensor:
-    inv = h.inverse()
-    out = torch.empty_like(vh)
-    _lib.call("ocsc_dict_rowsolve", _lib.code(vh.dtype), _lib.code(h.S.dtype), _lib.code(inv.dtype), h.K, h.nfreq,
-              _lib.ptr(inv),
-              _lib.ptr(h.c), h.count * h.ridge, _lib.ptr(vh), _lib.ptr(th), sk, sp, _lib.ptr(out), _lib.stream())
-    return out
+    return h.rowsolve(vh, th, sk, sp, torch.empty_like(vh))
 
 
 def solve_dict_rows(h: HistoryState, v_freq, dual_freq) -> np.ndarray:

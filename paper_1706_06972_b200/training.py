@@ -58,6 +58,7 @@ class TrainConfig:
     history_dtype: str = "float64" # history sums and Cholesky
     poll: int = 16                 # code-ADMM convergence poll interval (iterations)
     fused: bool = True             # on-chip cluster kernel when the grid has one (else cuFFT path)
+    history_solver: str = "auto"   # "gj" explicit inverse (K <= 118/167) | "chol" blocked Cholesky | "auto"
 
     def coding(self) -> CodingConfig:
         return CodingConfig(beta=self.beta, rho=self.rho_code, max_iters=self.code_max_iters,
@@ -178,7 +179,7 @@ class OnlineTrainer:
         self.den = code_den(self.Wh, self.coding_config.rho)
         # the inverse the J row solves re-read is stored at the arithmetic precision
         self.history = _HalfHistory(shape, K, config.rho_dict, nfreq=self.nf, dtype=hist_cdtype,
-                                    inv_dtype=self.cdtype)
+                                    inv_dtype=self.cdtype, solver=config.history_solver)
         self.rng = np.random.default_rng(config.seed)
         self._prev_code = None
         self._prev_alpha = self.alpha.clone()
@@ -234,14 +235,11 @@ class OnlineTrainer:
         if J == 0:
             return
         h = self.history
-        inv = h.inverse(check=False)
-        ridge = h.count * h.ridge
-        dt, ht, it_ = _lib.code(self.dtype), _lib.code(h.S.dtype), _lib.code(inv.dtype)
+        dt = _lib.code(self.dtype)
         s = _lib.stream()
         self.Th.zero_()
         for _ in range(J):
-            _lib.call("ocsc_dict_rowsolve", dt, ht, it_, self.K, self.nf, _lib.ptr(inv), _lib.ptr(h.c), ridge,
-                      _lib.ptr(self.Wh), _lib.ptr(self.Th), self.nf, 1, _lib.ptr(self.Dh), s)
+            h.rowsolve(self.Wh, self.Th, self.nf, 1, self.Dh, check=False)
             _lib.call("ocsc_dict_project", dt, self.H, self.W, self.M0, self.M1, self.K, _lib.ptr(self.Dh),
                       _lib.ptr(self.Th), _lib.ptr(self.Wh), _lib.ptr(self.alpha), s)
         _lib.call("ocsc_code_den", dt, self.K, self.nf, _lib.ptr(self.Wh), self.coding_config.rho,

@@ -405,3 +405,56 @@ def test_fused_divergence_raises():
     with pytest.raises(ob.DivergenceError, match="iteration"):
         tr.partial_fit(X)
     assert tr.history.count == 0
+
+
+# ------------------------------------------------- large-K history solver --
+
+def _random_history(K, nfreq, B, seed, dtype=torch.complex128, solver="auto"):
+    rng = np.random.default_rng(seed)
+    shape = ob.SignalShape((nfreq,), (1,))
+    h = ob.HistoryState(shape, K, 1.0, dtype=dtype, solver=solver)
+    z = (rng.normal(size=(B, nfreq, K)) + 1j * rng.normal(size=(B, nfreq, K))) / np.sqrt(2)
+    x = (rng.normal(size=(B, nfreq)) + 1j * rng.normal(size=(B, nfreq))) / np.sqrt(2)
+    zd = torch.as_tensor(z, dtype=dtype, device="cuda")
+    xd = torch.as_tensor(x, dtype=dtype, device="cuda")
+    h.accumulate(zd, (nfreq * K, 1, K), xd, (nfreq, 1), B)
+    return h, z, x
+
+
+def _dense_rowsolve(z, x, v, th, t_rho_p):
+    """Reference-form row solve: conj(d) = (sum z z^H + t rho P I)^-1 (c + t rho P conj(v - th))."""
+    B, P, K = z.shape
+    out = np.empty((P, K), complex)
+    for p in range(P):
+        S = np.einsum("bi,bj->ij", z[:, p], z[:, p].conj())
+        c = np.einsum("b,bk->k", x[:, p].conj(), z[:, p])
+        rhs = c + t_rho_p * np.conj(v[p] - th[p])
+        out[p] = np.conj(np.linalg.solve(S + t_rho_p * np.eye(K), rhs))
+    return out
+
+
+@pytest.mark.parametrize("K,solver", [(64, "chol"), (64, "gj"), (256, "chol"), (96, "chol")])
+def test_history_solvers_match_dense(K, solver):
+    nfreq, B = 5, 12
+    h, z, x = _random_history(K, nfreq, B, seed=K, solver=solver)
+    rng = np.random.default_rng(1)
+    v = rng.normal(size=(nfreq, K)) + 1j * rng.normal(size=(nfreq, K))
+    th = rng.normal(size=(nfreq, K)) + 1j * rng.normal(size=(nfreq, K))
+    vd = torch.as_tensor(v, device="cuda")
+    td = torch.as_tensor(th, device="cuda")
+    got = h.rowsolve(vd, td, 1, K, torch.empty_like(vd)).cpu().numpy()
+    want = _dense_rowsolve(z, x, v, th, B * 1.0 * nfreq)
+    assert rel(got, want) < 1e-11
+
+
+def test_trainer_cholesky_path_equals_inverse_path():
+    shape = ob.SignalShape((14, 14), (3, 3))
+    X = O.synth_images(8, (14, 14), (14, 14), 3, filter_dims=(3, 3), seed=5, density=0.05).reshape(8, -1)
+    kw = dict(n_filters=64, beta=0.3, rho_code=1.0, rho_dict=1.0, inner_iters=3, seed=2, code_max_iters=40,
+              batch_size=4, stop_tol=0.0)
+    a = ob.OnlineTrainer(shape, ob.TrainConfig(history_solver="gj", **kw))
+    b = ob.OnlineTrainer(shape, ob.TrainConfig(history_solver="chol", **kw))
+    for m in range(2):
+        ra, rb = a.partial_fit(X[4 * m:4 * m + 4]), b.partial_fit(X[4 * m:4 * m + 4])
+        assert np.allclose(ra.objectives, rb.objectives, rtol=1e-11, atol=0)
+    assert rel(a.final_filters(), b.final_filters()) < 1e-11
