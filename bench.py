@@ -319,6 +319,89 @@ def run_b200(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def run_history_microbench(args, rank, world, local_rank):
+    """BASELINE config 4: per-frequency rank-64 history accumulation + (A + rho I) Cholesky solve.
+
+    P = 128 x 128 independent frequencies (full grid: random codes are not Hermitian),
+    complex64, z ~ CN(0,1) and x ~ CN(0,1) seeded, rho = 1 (plain ridge on the summed A),
+    one right-hand side per frequency (the accumulated cross term).  Bytes/flops per
+    SURVEY.md 8(d): G6 and G7 formulas.
+    """
+    import torch
+
+    import paper_1706_06972_b200 as ob
+    from paper_1706_06972_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    _lib.load()
+    P, B, s = 128 * 128, 64, 4
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    fp32 = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 2 * 1965e6 / 1e12
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    shape = ob.SignalShape((P,), (1,))
+    for K in args.ks:
+        z = torch.complex(torch.randn(B, P, K, device=dev, generator=gen),
+                          torch.randn(B, P, K, device=dev, generator=gen)) / np.sqrt(2)
+        x = torch.complex(torch.randn(B, P, device=dev, generator=gen),
+                          torch.randn(B, P, device=dev, generator=gen)) / np.sqrt(2)
+        zero = torch.zeros(P, K, dtype=torch.complex64, device=dev)
+        out = torch.empty_like(zero)
+        times = {"accumulate": [], "factor": [], "solve": []}
+        for rep in range(args.warmup + args.steps):
+            h = ob.HistoryState(shape, K, 1.0 / P, dtype=torch.complex64, solver="chol")  # ridge rho*P = 1
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            torch.cuda.synchronize()
+            ev[0].record()
+            h.accumulate(z, (P * K, 1, K), x, (P, 1), B)
+            ev[1].record()
+            h.count = 1  # plain ridge rho = 1 on the summed A (t * rho * P with t = 1)
+            h.factor(check=False)
+            ev[2].record()
+            h.rowsolve(zero, zero, 1, K, out, check=False)
+            ev[3].record()
+            torch.cuda.synchronize()
+            if rep >= args.warmup:
+                times["accumulate"].append(ev[0].elapsed_time(ev[1]))
+                times["factor"].append(ev[1].elapsed_time(ev[2]))
+                times["solve"].append(ev[2].elapsed_time(ev[3]))
+            del h
+        # parity on a few frequencies against a dense complex128 solve
+        zz = z[:, :4].cpu().numpy().astype(np.complex128)
+        xx = x[:, :4].cpu().numpy().astype(np.complex128)
+        ref = []
+        for p in range(4):
+            A = np.einsum("bi,bj->ij", zz[:, p], zz[:, p].conj()) + np.eye(K)
+            ref.append(np.conj(np.linalg.solve(A, np.einsum("b,bk->k", xx[:, p].conj(), zz[:, p]))))
+        ref = np.array(ref)
+        err = float(np.linalg.norm(out[:4].cpu().numpy() - ref) / np.linalg.norm(ref))
+        npk = K * (K + 1) / 2
+        g6_bytes = 2 * P * npk * 2 * s + B * P * (K + 1) * 2 * s
+        g6_flops = 4 * K * (K + 1) * B * P
+        g7_bytes = 2 * P * npk * 2 * s + 2 * P * K * 2 * s
+        g7_flops = (4 / 3) * K ** 3 * P + 8 * K * K * P
+        ta, tf, ts = (min(times[k]) for k in ("accumulate", "factor", "solve"))
+        line = {"metric": "history accumulation + Cholesky solve (BASELINE config 4)", "K": K, "P": P, "B": B,
+                "dtype": "c64", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms": {"accumulate": ta, "factor": tf, "solve": ts, "total": ta + tf + ts},
+                "accumulate": {"GB/s": g6_bytes / ta / 1e6, "GFLOP/s": g6_flops / ta / 1e6,
+                               "frac_hbm": g6_bytes / ta / 1e6 / hbm, "frac_fp32": g6_flops / ta / 1e9 / fp32},
+                "cholesky_solve": {"GB/s": g7_bytes / (tf + ts) / 1e6, "GFLOP/s": g7_flops / (tf + ts) / 1e6,
+                                   "frac_hbm": g7_bytes / (tf + ts) / 1e6 / hbm,
+                                   "frac_fp32": g7_flops / (tf + ts) / 1e9 / fp32},
+                "peaks": {"hbm_GB/s": hbm, "fp32_TFLOP/s_nominal": fp32},
+                "parity_rel_err_vs_dense_c128": err, "data": "synthetic CN(0,1), seeded"}
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        del z, x
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,6 +410,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=CFG["B"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 4],
+                    help="1: BASELINE config 1 training step (default); 4: history + Cholesky microbenchmark")
+    ap.add_argument("--ks", type=int, nargs="+", default=[64, 128, 256, 512], help="K values for --config 4")
     args = ap.parse_args()
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
@@ -340,6 +426,9 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
+        if args.config == 4:
+            run_history_microbench(args, rank, world, local_rank)
+            return
         run_b200(args, rank, world, local_rank)
     finally:
         if world > 1:
