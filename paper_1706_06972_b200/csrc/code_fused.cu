@@ -76,9 +76,9 @@ template <int N>
 struct Geo {
   static constexpr int M = N / 2;
   static constexpr int Wh = M + 1;
-  // float row stride of w: even (float2 accesses) and odd in 8-byte units, so a warp of row
-  // tasks (one row per lane) hits 16 distinct 8-byte bank pairs per half-warp
-  static constexpr int WP = (N % 4 == 2) ? N + 2 : ((N % 4 == 0) ? N + 2 : N + 1);
+  // float row stride of w: even (float2 accesses) and odd in 8-byte units (N = 2 * odd), so a
+  // warp of row tasks (one row per lane) hits distinct 8-byte bank pairs
+  static constexpr int WP = N;
   static constexpr int NF = N * Wh;
   // complex row stride of the workspace: odd, >= Wh, and N*RS == Wh (mod 16) when possible,
   // so the row tasks (lane -> row) and the column half-warps (lane -> column, running across
@@ -289,8 +289,10 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   // (owner of frequency f = the CTA whose slice [f0, f1) contains it); part is CS x slice
   const int slice = (NF + CS - 1) / CS;
   auto reduce_push = [&]() {
-    for (int f = tid; f < NF; f += nt) {
-      const int o = (f / Wh) * RS + f % Wh;
+    // iterate the workspace index o = u*RS + v (v < Wh) so a warp reads contiguous words
+    for (int o = tid; o < N * RS; o += nt) {
+      const int u = o / RS, v = o - u * RS;
+      if (v >= Wh) continue;
       C s = mkc<C>(0, 0), s2 = mkc<C>(0, 0);  // two chains: the loads issue back to back
       int j = 0;
       for (; j + 1 < nk; j += 2) {
@@ -299,6 +301,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       }
       if (j < nk) s = vadd(s, X[j * PS + o]);
       s = vadd(s, s2);
+      const int f = u * Wh + v;
       const int owner = f / slice;
       cl.map_shared_rank(part, owner)[r * slice + (f - owner * slice)] = s;
     }
@@ -346,9 +349,9 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       T n4[5] = {0, 0, 0, 0, 0};
       for (int qq = 0; qq < CS; ++qq) {
         if (lane < nwarps) {
-          const T* src = nrm + (qq * 32 + lane) * 8;
+          const T* src = nrm + qq * 8 * 32 + lane;  // [qq][i][warp]: lanes read consecutive words
 #pragma unroll
-          for (int i = 0; i < 5; ++i) n4[i] += src[i];
+          for (int i = 0; i < 5; ++i) n4[i] += src[i * 32];
         }
       }
 #pragma unroll
@@ -415,9 +418,9 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
       if (lane < CS) {
-        T* dst = cl.map_shared_rank(nrm, lane) + (r * 32 + warp) * 8;
+        T* dst = cl.map_shared_rank(nrm, lane) + r * 8 * 32 + warp;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) dst[i] = q[i];
+        for (int i = 0; i < 5; ++i) dst[i * 32] = q[i];
       }
     }
     OCSC_STAMP(6);
