@@ -235,5 +235,10 @@ if __name__ == "__main__":
                        code_max_iters=50, beta=0.3)
     if run_all or "train_online" in which:
         case_train_online()
+    if run_all or "files" in which:
+        rng = np.random.default_rng(1007)
+        ocsc.save_dictionary(rng.normal(size=(6, 3)), (2, 3), os.path.join(HERE, "dict_2x3_k3.dic"))
+        ocsc.save_sample(rng.normal(size=20), (4, 5), os.path.join(HERE, "sample_4x5.smp"))
+        print("wrote dict_2x3_k3.dic, sample_4x5.smp")
     if "cfg0" in which:
         case_cfg0()

@@ -458,3 +458,32 @@ def test_trainer_cholesky_path_equals_inverse_path():
         ra, rb = a.partial_fit(X[4 * m:4 * m + 4]), b.partial_fit(X[4 * m:4 * m + 4])
         assert np.allclose(ra.objectives, rb.objectives, rtol=1e-11, atol=0)
     assert rel(a.final_filters(), b.final_filters()) < 1e-11
+
+
+# --------------------------------------------------------------- checkpoints --
+
+def test_checkpoint_resume_is_bit_identical(tmp_path):
+    shape = ob.SignalShape((14, 14), (3, 3))
+    X = O.synth_images(16, (14, 14), (14, 14), 3, filter_dims=(3, 3), seed=8, density=0.05).reshape(16, -1)
+    cfg = ob.TrainConfig(n_filters=6, beta=0.3, rho_dict=1.0, inner_iters=3, code_max_iters=60, batch_size=4,
+                         stop_tol=1e-9, dtype="float32")
+    a = ob.OnlineTrainer(shape, cfg)
+    objs_a = [a.partial_fit(X[4 * m:4 * m + 4]).objectives for m in range(4)]
+    b = ob.OnlineTrainer(shape, cfg)
+    objs_b = [b.partial_fit(X[4 * m:4 * m + 4]).objectives for m in range(2)]
+    ob.save_checkpoint(b, tmp_path / "t.npz")
+    c = ob.load_checkpoint(tmp_path / "t.npz")
+    objs_b += [c.partial_fit(X[4 * m:4 * m + 4]).objectives for m in range(2, 4)]
+    assert all(np.array_equal(p, q) for p, q in zip(objs_a, objs_b))
+    assert np.array_equal(a.final_filters(), c.final_filters())
+    assert a.history.count == c.history.count and a.dict_change == c.dict_change
+    assert a.rng.bit_generator.state == c.rng.bit_generator.state
+
+
+def test_dictionary_file_round_trip_from_trainer(tmp_path):
+    shape = ob.SignalShape((10, 10), (3, 3))
+    tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=4))
+    f = tr.final_filters()
+    ob.save_dictionary(f, shape.filter_dims, tmp_path / "d.dic")
+    g, dims = ob.load_dictionary(tmp_path / "d.dic")
+    assert dims == (3, 3) and np.array_equal(f, g)
