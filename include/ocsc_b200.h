@@ -197,6 +197,10 @@ int ocsc_crop_normalize_cols(int dtype, int H, int W, int M0, int M1, int K, con
 /* Support (K, M0*M1) -> spectra (K, H, Wh) via the pruned forward DFT (dict_state_from_filters). */
 int ocsc_support_rfft(int dtype, int H, int W, int M0, int M1, int K, const void* alpha, void* Vh,
                       void* stream);
+/* Tolerance test of the batch dictionary update (dictionary.py:210-214): per filter k,
+ * out[2k] = ||D_k - V_k||^2, out[2k+1] = ||D_k||^2 over the full spectrum, from half spectra
+ * (K, H, Wh) with Hermitian weights. */
+int ocsc_dict_gaps(int dtype, int H, int W, int K, const void* Dh, const void* Vh, double* out, void* stream);
 /* out[0] += sum (a-b)^2, out[1] += sum a^2 over n reals (b may be NULL: treated as 0) */
 int ocsc_norms2(int dtype, int64_t n, const void* a, const void* b, double* out, void* stream);
 

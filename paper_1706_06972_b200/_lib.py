@@ -63,6 +63,7 @@ SIGNATURES = {
     "ocsc_crop_normalize_cols": [_I, _I, _I, _I, _I, _I, _P, _P, _P],
     "ocsc_support_rfft": [_I, _I, _I, _I, _I, _I, _P, _P, _P],
     "ocsc_norms2": [_I, _I64, _P, _P, _P, _P],
+    "ocsc_dict_gaps": [_I, _I, _I, _I, _P, _P, _P, _P],
 }
 _RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ, "ocsc_history_factor_bytes": _SZ,
              "ocsc_kernel_launches": ctypes.c_int64}

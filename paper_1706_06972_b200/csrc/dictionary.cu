@@ -233,3 +233,41 @@ extern "C" int ocsc_norms2(int dtype, int64_t n, const void* a, const void* b, d
   OCSC_LAUNCHED("k_norms2");
   return OCSC_OK;
 }
+
+namespace ocsc {
+// per filter: out[2k] += sum_p w_p |D_k[p] - V_k[p]|^2, out[2k+1] += sum_p w_p |D_k[p]|^2 over the
+// half spectrum with Hermitian weights (= full-spectrum squared norms, dictionary.py:210-214)
+template <typename T>
+__global__ void k_dict_gaps(int H, int W, const cx<T>* __restrict__ Dh, const cx<T>* __restrict__ Vh, double* out) {
+  __shared__ double scratch[64];
+  const int k = blockIdx.x;
+  const int Wh = W / 2 + 1, nf = H * Wh;
+  double s[2] = {0.0, 0.0};
+  for (int p = threadIdx.x; p < nf; p += blockDim.x) {
+    const cx<T> d = Dh[(int64_t)k * nf + p], v = Vh[(int64_t)k * nf + p];
+    const double w = herm_weight(p % Wh, W);
+    const double ex = (double)d.x - v.x, ey = (double)d.y - v.y;
+    s[0] += w * (ex * ex + ey * ey);
+    s[1] += w * ((double)d.x * d.x + (double)d.y * d.y);
+  }
+  block_sum<2>(s, scratch);
+  if (threadIdx.x == 0) {
+    out[2 * k] = s[0];
+    out[2 * k + 1] = s[1];
+  }
+}
+}  // namespace ocsc
+
+extern "C" int ocsc_dict_gaps(int dtype, int H, int W, int K, const void* Dh, const void* Vh, double* out,
+                              void* stream) {
+  if (K <= 0) return OCSC_OK;
+  cudaStream_t s = as_stream(stream);
+  if (dtype == OCSC_F32)
+    k_dict_gaps<float><<<K, 256, 0, s>>>(H, W, (const float2*)Dh, (const float2*)Vh, out);
+  else if (dtype == OCSC_F64)
+    k_dict_gaps<double><<<K, 256, 0, s>>>(H, W, (const double2*)Dh, (const double2*)Vh, out);
+  else
+    return fail(OCSC_EARG, "dtype must be 4 or 8");
+  OCSC_LAUNCHED("k_dict_gaps");
+  return OCSC_OK;
+}

@@ -411,10 +411,111 @@ def fit(samples, shape: SignalShape, config: TrainConfig, test_samples=None, ret
     return train_online(samples, shape, config, test_samples, return_codes=return_codes)
 
 
+def _dictionary_to_tolerance(tr: OnlineTrainer, iters: int, tol: float | None) -> None:
+    """update_dictionary(d_prev, h, iters, tol) (dictionary.py:176-215) on trainer device state."""
+    h = tr.history
+    dt = _lib.code(tr.dtype)
+    s = _lib.stream()
+    gaps = torch.empty(2 * tr.K, dtype=torch.float64, device=tr.dev)
+    tr.Th.zero_()
+    for _ in range(iters):
+        h.rowsolve(tr.Wh, tr.Th, tr.nf, 1, tr.Dh, check=False)
+        _lib.call("ocsc_dict_project", dt, tr.H, tr.W, tr.M0, tr.M1, tr.K, _lib.ptr(tr.Dh), _lib.ptr(tr.Th),
+                  _lib.ptr(tr.Wh), _lib.ptr(tr.alpha), s)
+        if tol is not None:
+            _lib.call("ocsc_dict_gaps", dt, tr.H, tr.W, tr.K, _lib.ptr(tr.Dh), _lib.ptr(tr.Wh), _lib.ptr(gaps), s)
+            g = gaps.cpu().numpy().reshape(tr.K, 2)
+            if (np.sqrt(g[:, 0]) / np.maximum(np.sqrt(g[:, 1]), 1e-12)).max() < tol:
+                break
+    _lib.call("ocsc_code_den", dt, tr.K, tr.nf, _lib.ptr(tr.Wh), tr.coding_config.rho, _lib.ptr(tr.den), s)
+
+
+def train_batch(samples, shape: SignalShape, config: TrainConfig, test_samples=None) -> TrainReport:
+    """Batch alternation (training.py:234-305), device-resident.
+
+    Every outer iteration codes the whole corpus at once (warm-started from the previous
+    codes, cuFFT code-ADMM path), rebuilds the history from all codes (rank-N accumulation,
+    uniform weights: batch_history, dictionary.py:117-131), and runs the dictionary ADMM to
+    `batch_dict_tol` (at most `batch_dict_iters` rounds).
+    """
+    samples = np.atleast_2d(np.asarray(samples, dtype=np.float64))
+    filters0 = init_dictionary(shape, config.n_filters, config.seed)
+    report = TrainReport(config=config, shape=shape)
+    if samples.size == 0:
+        report.filters = filters0
+        return report
+    if samples.shape[1] != shape.size:
+        raise ShapeMismatchError(f"samples must be (N, {shape.size}), got {samples.shape}")
+    n = samples.shape[0]
+    tr = OnlineTrainer(shape, replace(config, batch_size=n, fused=False))
+    coding = config.coding()
+    buf = tr._buffers(n, False)
+    x = tr._x[:n]
+    x.copy_(torch.from_numpy(samples.reshape(n, tr.H, tr.W)))
+    xh = rfft2_dev(x, shape)
+    uh = tr._uh[:n]
+    prev_u = None
+    prev_filters = tr.alpha.clone()
+    hist_cdtype = tr.history.S.dtype
+    norms = torch.zeros(2, dtype=torch.float64, device=tr.dev)
+    train_seconds = 0.0
+    final = tr.final_filters()
+    for outer in range(1, config.max_passes + 1):
+        tic = time.perf_counter()
+        infer_codes(xh, tr.Wh, tr.den, shape, coding, buf, n, warm=outer > 1, poll=config.poll)
+        status = buf.status[:n].cpu()
+        if bool((status == 2).any()):
+            it = int(buf.iters[:n][status.to(buf.iters.device) == 2].min().cpu())
+            raise DivergenceError(f"code solver diverged at iteration {it}")
+        code_change = 0.0
+        if prev_u is not None:
+            changes = []
+            for b in range(n):
+                norms.zero_()
+                _lib.call("ocsc_norms2", _lib.code(tr.dtype), buf.u[b].numel(), _lib.ptr(buf.u[b]),
+                          _lib.ptr(prev_u[b]), _lib.ptr(norms), _lib.stream())
+                a2, b2 = norms.cpu().tolist()
+                changes.append(np.sqrt(a2) / max(np.sqrt(b2), 1e-12))
+            code_change = float(np.mean(changes))
+            prev_u.copy_(buf.u[:n])
+        else:
+            prev_u = buf.u[:n].clone()
+        _lib.call("ocsc_rfft2", _lib.code(tr.dtype), tr.H, tr.W, n * tr.K, _lib.ptr(buf.u), _lib.ptr(uh),
+                  _lib.stream())
+        tr.history = _HalfHistory(shape, tr.K, config.rho_dict, nfreq=tr.nf, dtype=hist_cdtype,
+                                  inv_dtype=tr.cdtype, solver=config.history_solver)
+        tr.history.accumulate(uh, (tr.K * tr.nf, tr.nf, 1), xh, (tr.nf, 1), n)
+        _dictionary_to_tolerance(tr, config.batch_dict_iters, config.batch_dict_tol)
+        train_seconds += time.perf_counter() - tic
+        norms.zero_()
+        _lib.call("ocsc_norms2", _lib.code(tr.dtype), tr.alpha.numel(), _lib.ptr(tr.alpha), _lib.ptr(prev_filters),
+                  _lib.ptr(norms), _lib.stream())
+        a2, b2 = norms.cpu().tolist()
+        dict_change = np.sqrt(a2) / max(np.sqrt(b2), 1e-12)
+        prev_filters.copy_(tr.alpha)
+        # objectives of the current codes against the refreshed dictionary (training.py:280-283)
+        obj, _ = code_objectives(xh, tr.Wh, buf.u, shape, config.beta, n, torch.empty_like(uh))
+        result = _evaluate_pass(tr.coding_filters(), test_samples, shape, coding, config)
+        final = tr.final_filters()
+        report.records.append(PassRecord(
+            index=outer, time_s=train_seconds, train_obj=float(obj.cpu().mean()),
+            test_obj=None if result is None else result.test_objective,
+            psnr=None if result is None else result.psnr,
+            history_bytes=tr.history.nbytes, snapshot_id=_snapshot_id(final)))
+        if outer > 1 and code_change < config.stop_tol and dict_change < config.stop_tol:
+            report.stopped_early = True
+            break
+    report.filters = final
+    return report
+
+
 def train(mode: str, samples, shape, config, test_samples=None) -> TrainReport:
-    """Mode dispatch (training.py:374-383).  Only the online path is built for B200."""
+    """Mode dispatch (training.py:374-383): online (the hot path) and batch (row f2)."""
     if mode == "online":
         return train_online(samples, shape, replace(config, mode=mode), test_samples)
-    if mode in ("batch", "fista-dict"):
-        raise NotImplementedError(f"training mode {mode!r} is outside the B200 hot path (SURVEY.md 2.1 rows 4, 7)")
+    if mode == "batch":
+        return train_batch(samples, shape, replace(config, mode=mode), test_samples)
+    if mode == "fista-dict":
+        raise NotImplementedError("training mode 'fista-dict' is a baseline outside the B200 hot path "
+                                  "(SURVEY.md 2.1 row 7)")
     raise ValueError(f"unknown training mode: {mode!r}")

@@ -235,6 +235,18 @@ if __name__ == "__main__":
                        code_max_iters=50, beta=0.3)
     if run_all or "train_online" in which:
         case_train_online()
+    if run_all or "train_batch" in which:
+        X = synth_images(5, (1, 24), (1, 24), 2, filter_dims=(1, 4), seed=21, density=0.1).reshape(5, 24)
+        shape = ocsc.SignalShape((24,), (4,))
+        cfg = ocsc.TrainConfig(n_filters=3, beta=0.4, seed=2, max_passes=3, stop_tol=1e-12,
+                               code_max_iters=150, batch_dict_iters=60, batch_dict_tol=1e-6)
+        rep = ocsc.train_batch(X, shape, cfg)
+        X2 = synth_images(4, (8, 10), (8, 10), 2, filter_dims=(3, 3), seed=22, density=0.1).reshape(4, 80)
+        shape2 = ocsc.SignalShape((8, 10), (3, 3))
+        rep2 = ocsc.train_batch(X2, shape2, ocsc.TrainConfig(n_filters=4, beta=0.3, seed=1, max_passes=2,
+                                                             code_max_iters=120, batch_dict_iters=40))
+        save("train_batch", X=X, train_obj=np.array([r.train_obj for r in rep.records]), filters=rep.filters,
+             X2=X2, train_obj2=np.array([r.train_obj for r in rep2.records]), filters2=rep2.filters)
     if run_all or "files" in which:
         rng = np.random.default_rng(1007)
         ocsc.save_dictionary(rng.normal(size=(6, 3)), (2, 3), os.path.join(HERE, "dict_2x3_k3.dic"))

@@ -92,7 +92,7 @@ def test_train_dispatch_errors():
     with pytest.raises(ValueError, match="unknown training mode"):
         train("nope", np.zeros((1, 8)), SignalShape((8,), (2,)), TrainConfig())
     with pytest.raises(NotImplementedError):
-        train("batch", np.zeros((1, 8)), SignalShape((8,), (2,)), TrainConfig())
+        train("fista-dict", np.zeros((1, 8)), SignalShape((8,), (2,)), TrainConfig())
 
 
 def test_shard_rows_partitions_in_rank_order():

@@ -487,3 +487,20 @@ def test_dictionary_file_round_trip_from_trainer(tmp_path):
     ob.save_dictionary(f, shape.filter_dims, tmp_path / "d.dic")
     g, dims = ob.load_dictionary(tmp_path / "d.dic")
     assert dims == (3, 3) and np.array_equal(f, g)
+
+
+# ------------------------------------------------------------ batch mode (f2) --
+
+def test_train_batch_matches_reference(golden):
+    g = golden("train_batch")
+    shape = ob.SignalShape((24,), (4,))
+    cfg = ob.TrainConfig(n_filters=3, beta=0.4, seed=2, max_passes=3, stop_tol=1e-12, code_max_iters=150,
+                         batch_dict_iters=60, batch_dict_tol=1e-6)
+    rep = ob.train("batch", g["X"], shape, cfg)
+    assert np.allclose([r.train_obj for r in rep.records], g["train_obj"], rtol=1e-9, atol=0)
+    assert rel(rep.filters, g["filters"]) < 1e-9
+    shape2 = ob.SignalShape((8, 10), (3, 3))
+    rep2 = ob.train_batch(g["X2"], shape2, ob.TrainConfig(n_filters=4, beta=0.3, seed=1, max_passes=2,
+                                                            code_max_iters=120, batch_dict_iters=40))
+    assert np.allclose([r.train_obj for r in rep2.records], g["train_obj2"], rtol=1e-9, atol=0)
+    assert rel(rep2.filters, g["filters2"]) < 1e-9
