@@ -402,6 +402,93 @@ def run_history_microbench(args, rank, world, local_rank):
         del z, x
 
 
+def run_preprocess_microbench(args, rank, world, local_rank):
+    """grayscale + LCN + edge taper (preprocessing.py:92-100), one fused launch.
+
+    N = 1024 seeded RGB uint8 256 x 256 images (Flower/CIFAR-style stream, synthetic), float32 out
+    (what the float32 trainer consumes).  Input 201 MB + output 268 MB > L2, so no flush is needed.
+    Algorithmic bytes per image = H*W*3 (u8 in) + H*W*4 (f32 out).
+    """
+    import torch
+
+    import paper_1706_06972_b200 as ob
+    from paper_1706_06972_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    _lib.load()
+    N, H, W = 1024, 256, 256
+    rng = np.random.default_rng(2024 + rank)
+    host = torch.from_numpy(rng.integers(0, 256, size=(N, H, W, 3), dtype=np.uint8)).pin_memory()
+    imgs = host.to(dev)
+    spec = ob.PreprocessSpec(seed=rank * N)
+    out = ob.preprocess_batch(imgs, spec, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    l0 = _lib.load().ocsc_kernel_launches()
+    times = []
+    for rep in range(args.warmup + args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        out = ob.preprocess_batch(imgs, spec, out_dtype=torch.float32)
+        b.record()
+        torch.cuda.synchronize()
+        if rep >= args.warmup:
+            times.append(a.elapsed_time(b))
+    launches = (_lib.load().ocsc_kernel_launches() - l0) * args.steps // (args.warmup + args.steps)
+    e2e_t = []
+    res = torch.empty((N, H, W), dtype=torch.float32).pin_memory()
+    for rep in range(args.warmup + args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        o = ob.preprocess_batch(host.to(dev, non_blocking=True), spec, out_dtype=torch.float32)
+        res.copy_(o, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        if rep >= args.warmup:
+            e2e_t.append(a.elapsed_time(b))
+    from oracle import ocsc_oracle as O
+
+    ref = O.preprocess(host[0].numpy().astype(np.float64), seed=spec.seed)
+    err = float(np.abs(res[0].double().numpy() - ref).max() / np.abs(ref).max())
+    t0 = time.perf_counter()
+    for i in range(4):
+        O.preprocess(host[i].numpy().astype(np.float64), seed=spec.seed + i)
+    cpu_ips = 4 / (time.perf_counter() - t0)
+    ms = float(np.median(times))
+    algo = N * H * W * (3 + 4)
+    flops = N * H * W * (8 * spec.lcn_window + 4 * spec.taper_size + 10)
+    fp64 = 148 * 64 * 2 * 1965e6 / 1e12
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get("preprocess_dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    line = {"metric": "preprocessed images/s (grayscale + LCN + edge taper, SURVEY 8(f) f4)",
+            "value": N * world / (ms / 1e3), "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "dtype": "f64 arithmetic, u8 in, f32 out", "data": "synthetic RGB uint8, seeded",
+            "config": {"workload": f"{N} RGB {H}x{W} images per GPU per step", "l2": "working set > L2"},
+            "roofline": {"bound": "fp64", "kernel": "k_preprocess<uint8_t, float, 9, 11>",
+                         "achieved": flops / ms / 1e9, "peak": fp64, "unit": "TFLOP/s", "frac": flops / ms / 1e9 / fp64,
+                         "traffic": traffic, "algorithmic_flops_per_launch": flops,
+                         "flops_note": "per pixel 8*window (LCN: 2 passes x {x, x^2}) + 4*taper (2 passes) + 10 "
+                                       "(normalise, blend); float64 is the reference's arithmetic",
+                         "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (nominal; not in MEASURED_PEAKS)",
+                         "hbm": {"algorithmic_bytes": algo, "achieved_GB/s": algo / ms / 1e6, "peak": hbm,
+                                 "frac": algo / ms / 1e6 / hbm}},
+            "cpu_baseline": {"value": cpu_ips, "unit": "images/s", "cores": 1, "kind": "port",
+                             "sample": "4 images through oracle/ocsc_oracle.py preprocess (numpy, float64)"},
+            "e2e": {"value": N / (float(np.median(e2e_t)) / 1e3), "unit": "images/s",
+                    "h2d_bytes_per_step": N * H * W * 3, "d2h_bytes_per_step": N * H * W * 4},
+            "gpu_launches": int(launches), "parity_max_rel_err_vs_oracle_f32_out": err}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -410,8 +497,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=CFG["B"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[1, 4],
-                    help="1: BASELINE config 1 training step (default); 4: history + Cholesky microbenchmark")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 4, 5],
+                    help="1: BASELINE config 1 training step (default); 4: history + Cholesky microbenchmark; "
+                         "5: image preprocessing (row f4)")
     ap.add_argument("--ks", type=int, nargs="+", default=[64, 128, 256, 512], help="K values for --config 4")
     args = ap.parse_args()
     world = _env_int("WORLD_SIZE", 1)
@@ -428,6 +516,9 @@ def main():
     try:
         if args.config == 4:
             run_history_microbench(args, rank, world, local_rank)
+            return
+        if args.config == 5:
+            run_preprocess_microbench(args, rank, world, local_rank)
             return
         run_b200(args, rank, world, local_rank)
     finally:

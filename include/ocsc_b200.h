@@ -39,6 +39,7 @@ extern "C" {
 
 #define OCSC_F32 4
 #define OCSC_F64 8
+#define OCSC_U8 1            /* image input only (ocsc_preprocess)          */
 
 #define OCSC_OK 0
 #define OCSC_ESHAPE (-1)    /* errors.py:4-5  ShapeMismatchError            */
@@ -203,6 +204,22 @@ int ocsc_support_rfft(int dtype, int H, int W, int M0, int M1, int K, const void
 int ocsc_dict_gaps(int dtype, int H, int W, int K, const void* Dh, const void* Vh, double* out, void* stream);
 /* out[0] += sum (a-b)^2, out[1] += sum a^2 over n reals (b may be NULL: treated as 0) */
 int ocsc_norms2(int dtype, int64_t n, const void* a, const void* b, double* out, void* stream);
+
+/* Image preparation (preprocessing.py:36-100), ONE kernel over N images of H x W (channels 1,
+ * or 3 interleaved RGB mixed with the luminance weights :13).  flags bit 0: local contrast
+ * normalisation, Gaussian window `lcn_window` / `lcn_sigma`, std floor `lcn_epsilon` (:58-71);
+ * bit 1: edge taper with kernel size = ramp width `taper_size` (:74-89) and per-image width
+ * taper_sigmas[i] (device pointer), or, when taper_sigmas is NULL, numpy's
+ * default_rng(taper_seed0 + i).uniform(lo, hi) drawn on the device (:98-99, cli.py:116).
+ * scipy "reflect" borders; float64 arithmetic.  dtype_in: OCSC_U8 / OCSC_F32 / OCSC_F64;
+ * dtype_out: OCSC_F32 / OCSC_F64.  Replaces preprocess() per image (preprocessing.py:92). */
+int ocsc_preprocess(int dtype_in, int dtype_out, int N, int H, int W, int channels, const void* in, int flags,
+                    int lcn_window, double lcn_sigma, double lcn_epsilon, int taper_size,
+                    const double* taper_sigmas, int64_t taper_seed0, double taper_sigma_lo,
+                    double taper_sigma_hi, void* out, void* stream);
+/* Host-side: out[i] = numpy default_rng(seed0 + i).uniform(lo, hi) (SeedSequence + PCG64),
+ * bit-identical to numpy 2.x; the taper widths ocsc_preprocess draws (preprocessing.py:98-99). */
+int ocsc_taper_sigmas(int64_t seed0, int n, double lo, double hi, double* out);
 
 #ifdef __cplusplus
 }

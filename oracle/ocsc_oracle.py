@@ -375,6 +375,66 @@ def synth_images(n: int, dims0, grid, K0: int, filter_dims=(11, 11), seed: int =
 
 
 # BASELINE.json configs; rho_code = rho_dict = 1 (BASELINE "rho=1").
+# ---------------------------------------------------------- preprocessing --
+# preprocessing.py:13-100 (row f4): grayscale, Gaussian LCN, seeded edge taper.  scipy's
+# correlate1d(mode="reflect") is restated as np.pad(mode="symmetric") + a sliding dot product
+# with the kernel centre at size // 2.
+
+LUMA = (0.299, 0.587, 0.114)
+
+
+def gray(image):
+    a = np.asarray(image, dtype=np.float64)
+    return a if a.ndim == 2 else a[..., 0] * LUMA[0] + a[..., 1] * LUMA[1] + a[..., 2] * LUMA[2]
+
+
+def gauss(size: int, sigma: float):
+    xs = np.arange(size) - (size - 1) / 2.0
+    k = np.exp(-0.5 * (xs / sigma) ** 2)
+    return k / k.sum()
+
+
+def correlate_reflect(a, k, axis: int):
+    """scipy.ndimage.correlate1d(a, k, axis, mode='reflect') (preprocessing.py:53-55)."""
+    s = len(k)
+    c = s // 2
+    pad = [(0, 0)] * a.ndim
+    pad[axis] = (c, s - 1 - c)
+    p = np.pad(a, pad, mode="symmetric")
+    n = a.shape[axis]
+    out = np.zeros_like(a)
+    for t in range(s):
+        out += k[t] * np.take(p, np.arange(t, t + n), axis=axis)
+    return out
+
+
+def separable(a, k):
+    return correlate_reflect(correlate_reflect(a, k, 0), k, 1)
+
+
+def lcn(a, window=9, sigma=3.0, eps=1e-4):
+    k = gauss(window, sigma)
+    m = separable(a, k)
+    v = separable(a * a, k) - m * m
+    return (a - m) / np.maximum(np.sqrt(np.maximum(v, 0.0)), eps)
+
+
+def taper(a, size=11, sigma=2.0):
+    b = separable(a, gauss(size, sigma))
+
+    def ramp(n):
+        i = np.arange(n) + 0.5
+        return np.minimum(np.minimum(i, n - i) / size, 1.0)
+
+    w = np.outer(ramp(a.shape[0]), ramp(a.shape[1]))
+    return w * a + (1.0 - w) * b
+
+
+def preprocess(image, window=9, sigma=3.0, eps=1e-4, size=11, sigma_range=(1.0, 3.0), seed=0):
+    s = float(np.random.default_rng(seed).uniform(*sigma_range))
+    return taper(lcn(gray(image), window, sigma, eps), size, s)
+
+
 CONFIGS = {
     0: dict(n=10, dims0=(100, 100), grid=(100, 100), K0=20, K=100, beta=1.0, B=1, passes=1, dtype="float64"),
     1: dict(n=50_000, dims0=(32, 32), grid=(42, 42), K0=20, K=100, beta=1.0, B=50, passes=1, dtype="float32"),

@@ -21,7 +21,7 @@ from .errors import (
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libocsc_b200.so")
 
-F32, F64 = 4, 8
+F32, F64, U8 = 4, 8, 1
 
 _I, _I64, _D, _P, _SZ = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t
 
@@ -64,6 +64,8 @@ SIGNATURES = {
     "ocsc_support_rfft": [_I, _I, _I, _I, _I, _I, _P, _P, _P],
     "ocsc_norms2": [_I, _I64, _P, _P, _P, _P],
     "ocsc_dict_gaps": [_I, _I, _I, _I, _P, _P, _P, _P],
+    "ocsc_preprocess": [_I, _I, _I, _I, _I, _I, _P, _I, _I, _D, _D, _I, _P, _I64, _D, _D, _P, _P],
+    "ocsc_taper_sigmas": [_I64, _I, _D, _D, _P],
 }
 _RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ, "ocsc_history_factor_bytes": _SZ,
              "ocsc_kernel_launches": ctypes.c_int64}

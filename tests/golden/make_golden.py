@@ -247,6 +247,25 @@ if __name__ == "__main__":
                                                              code_max_iters=120, batch_dict_iters=40))
         save("train_batch", X=X, train_obj=np.array([r.train_obj for r in rep.records]), filters=rep.filters,
              X2=X2, train_obj2=np.array([r.train_obj for r in rep2.records]), filters2=rep2.filters)
+    if run_all or "preprocess" in which:
+        from ocsc import preprocessing as P
+
+        rng = np.random.default_rng(31)
+        rgb = rng.integers(0, 256, size=(37, 53, 3)).astype(np.float64)
+        gray = 128.0 + 40.0 * rng.normal(size=(20, 16))
+        tiny = rng.uniform(0, 255, size=(3, 4))
+        small = rng.normal(size=(5, 6))
+        stack = rng.integers(0, 256, size=(4, 32, 32, 3)).astype(np.float64)
+        save("preprocess", rgb=rgb, gray=gray, tiny=tiny, small=small, stack=stack,
+             gray_rgb=P.grayscale(rgb),
+             pre_rgb=P.preprocess(rgb, P.PreprocessSpec(seed=3)),
+             pre_gray=P.preprocess(gray),
+             pre_tiny=P.preprocess(tiny, P.PreprocessSpec(seed=1)),
+             lcn_even=P.local_contrast_normalize(gray, window=8, sigma=2.0),
+             lcn_tiny=P.local_contrast_normalize(tiny, window=9, sigma=3.0, epsilon=1e-2),
+             taper_small=P.edge_taper(small, size=7, sigma=1.5),
+             taper_even=P.edge_taper(gray, size=6, sigma=1.0),
+             pre_stack=np.stack([P.preprocess(im, P.PreprocessSpec(seed=5 + i)) for i, im in enumerate(stack)]))
     if run_all or "files" in which:
         rng = np.random.default_rng(1007)
         ocsc.save_dictionary(rng.normal(size=(6, 3)), (2, 3), os.path.join(HERE, "dict_2x3_k3.dic"))

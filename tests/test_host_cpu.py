@@ -147,3 +147,16 @@ def test_gloo_world2_exchange_is_rank_ordered():
         p.join(timeout=60)
     assert [r[1] for r in res] == [True, True]
     assert [r[2] for r in res] == [1.0, 1.0]
+
+
+def test_taper_sigmas_match_numpy_default_rng():
+    """The library's host SeedSequence + PCG64 (what the preprocessing kernel draws per image)
+    is bit-identical to numpy's default_rng(seed).uniform (preprocessing.py:98-99)."""
+    from paper_1706_06972_b200.preprocessing import PreprocessSpec, taper_sigma, taper_sigmas
+
+    got = taper_sigmas(0, 3000, (1.0, 3.0))
+    want = np.array([np.random.default_rng(s).uniform(1.0, 3.0) for s in range(3000)])
+    assert np.array_equal(got, want)
+    for s in (2**32 - 1, 2**32, 2**40 + 5, 2**63 - 1):
+        assert taper_sigma(PreprocessSpec(seed=s)) == float(np.random.default_rng(s).uniform(1.0, 3.0))
+    assert taper_sigmas(7, 1, (0.5, 4.0))[0] == np.random.default_rng(7).uniform(0.5, 4.0)

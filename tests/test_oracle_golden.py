@@ -161,3 +161,21 @@ def test_oracle_config0_full_size(golden):
     code[g["code_idx"]] = g["code_val"]
     assert rel(planes_to_cols(st["code"]).ravel(), code) < 1e-11
     assert rel(tr.final_filters(), g["final_filters"]) < 1e-11
+
+
+def test_oracle_preprocessing_matches_reference(golden):
+    g = golden("preprocess")
+
+    def close(a, b):
+        return np.abs(a - b).max() <= 1e-12 * max(np.abs(b).max(), 1.0)
+
+    assert close(O.gray(g["rgb"]), g["gray_rgb"])
+    assert close(O.preprocess(g["rgb"], seed=3), g["pre_rgb"])
+    assert close(O.preprocess(g["gray"]), g["pre_gray"])
+    assert close(O.preprocess(g["tiny"], seed=1), g["pre_tiny"])  # window > image: repeated reflection
+    assert close(O.lcn(g["gray"], 8, 2.0), g["lcn_even"])  # even window, off-centre kernel
+    assert close(O.lcn(g["tiny"], 9, 3.0, 1e-2), g["lcn_tiny"])
+    assert close(O.taper(g["small"], 7, 1.5), g["taper_small"])
+    assert close(O.taper(g["gray"], 6, 1.0), g["taper_even"])
+    for i, im in enumerate(g["stack"]):
+        assert close(O.preprocess(im, seed=5 + i), g["pre_stack"][i])

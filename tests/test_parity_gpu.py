@@ -504,3 +504,51 @@ def test_train_batch_matches_reference(golden):
                                                             code_max_iters=120, batch_dict_iters=40))
     assert np.allclose([r.train_obj for r in rep2.records], g["train_obj2"], rtol=1e-9, atol=0)
     assert rel(rep2.filters, g["filters2"]) < 1e-9
+
+
+# ----------------------------------------------------------- preprocessing (f4) --
+
+def test_preprocessing_matches_reference(golden):
+    g = golden("preprocess")
+
+    def close(a, b, tol=1e-12):
+        return np.abs(a - b).max() <= tol * max(np.abs(b).max(), 1.0)
+
+    assert close(ob.grayscale(g["rgb"]), g["gray_rgb"])
+    assert np.array_equal(ob.grayscale(g["gray"]), g["gray"])
+    assert close(ob.preprocess(g["rgb"], ob.PreprocessSpec(seed=3)), g["pre_rgb"])
+    assert close(ob.preprocess(g["gray"]), g["pre_gray"])
+    assert close(ob.preprocess(g["tiny"], ob.PreprocessSpec(seed=1)), g["pre_tiny"])
+    assert close(ob.local_contrast_normalize(g["gray"], window=8, sigma=2.0), g["lcn_even"])
+    assert close(ob.local_contrast_normalize(g["tiny"], window=9, sigma=3.0, epsilon=1e-2), g["lcn_tiny"])
+    assert close(ob.edge_taper(g["small"], size=7, sigma=1.5), g["taper_small"])
+    assert close(ob.edge_taper(g["gray"], size=6, sigma=1.0), g["taper_even"])
+    # the corpus form: one launch, u8 input, per-image seeds spec.seed + i (cli.py:116)
+    out = ob.preprocess_batch(g["stack"].astype(np.uint8), ob.PreprocessSpec(seed=5))
+    assert out.is_cuda and out.dtype == torch.float64
+    assert close(out.cpu().numpy(), g["pre_stack"])
+    out32 = ob.preprocess_batch(torch.from_numpy(g["stack"]).cuda(), ob.PreprocessSpec(seed=5),
+                                out_dtype=torch.float32)
+    assert close(out32.double().cpu().numpy(), g["pre_stack"], 1e-6)
+
+
+def test_preprocessing_reference_properties():
+    from oracle import ocsc_oracle as O
+
+    assert np.abs(ob.local_contrast_normalize(np.full((20, 20), 77.0))).max() < 1e-9
+    img = 128.0 + 40.0 * np.random.default_rng(94).normal(size=(64, 64))
+    out = ob.edge_taper(img, size=11, sigma=2.0)
+    assert np.abs(out[20:-20, 20:-20] - img[20:-20, 20:-20]).max() < 1e-12
+    assert np.abs(ob.edge_taper(np.full((30, 30), 4.25), size=7, sigma=1.5) - 4.25).max() < 1e-12
+    a = ob.preprocess(img, ob.PreprocessSpec(seed=1))
+    b = ob.preprocess(img, ob.PreprocessSpec(seed=2))
+    assert not np.array_equal(a, b) and np.abs(a[20:-20, 20:-20] - b[20:-20, 20:-20]).max() < 1e-12
+    with pytest.raises(ob.ShapeMismatchError):
+        ob.grayscale(np.zeros((3, 4, 4)))
+    # full-size stream: 64 RGB 266x266 images (config 3 grid) in one launch, spot-checked
+    rng = np.random.default_rng(7)
+    stack = rng.integers(0, 256, size=(64, 266, 266, 3), dtype=np.uint8)
+    out = ob.preprocess_batch(stack, ob.PreprocessSpec(seed=11)).cpu().numpy()
+    for i in (0, 37, 63):
+        ref = O.preprocess(stack[i].astype(np.float64), seed=11 + i)
+        assert np.abs(out[i] - ref).max() <= 1e-12 * np.abs(ref).max()
