@@ -44,6 +44,19 @@ WORKLOAD = ("BASELINE config 1: seeded synthetic 32x32 images zero-padded to 42x
             "beta=1, rho=1, J=10, <=300 code iterations, float32 (history float64), mini-batch 50 per GPU")
 
 
+# secondary training configs; printed as their own lines, not the headline
+TRAIN_CFGS = {
+    2: (dict(dims0=(100, 100), grid=(100, 100), fdims=(11, 11), K0=20, K=100, beta=1.0, rho_code=1.0,
+             rho_dict=1.0, J=10, max_iters=300, rel_tol=1e-3, B=10),
+        "BASELINE config 2: seeded synthetic 100x100 images (no padding), K=100 filters 11x11, beta=1, rho=1, "
+        "J=10, <=300 code iterations, float32 (history float64), mini-batch 10 per GPU"),
+    3: (dict(dims0=(256, 256), grid=(266, 266), fdims=(11, 11), K0=64, K=256, beta=0.5, rho_code=1.0,
+             rho_dict=1.0, J=10, max_iters=300, rel_tol=1e-3, B=32),
+        "BASELINE config 3: seeded synthetic 256x256 images zero-padded to 266x266, K=256 filters 11x11, "
+        "beta=0.5, rho=1, J=10, <=300 code iterations, float32 (history float64), mini-batch 32 per GPU"),
+}
+
+
 def _env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -262,6 +275,8 @@ def run_b200(args, rank, world, local_rank):
         pass
 
     # ---- e2e: public API, pinned host input, objectives back to host -----------------
+    del trainer, buf
+    torch.cuda.empty_cache()
     trainer2 = Trainer()
     Xh = torch.as_tensor(X).pin_memory()
     for s in range(args.warmup):
@@ -495,13 +510,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--batch", type=int, default=CFG["B"])
+    ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[1, 4, 5],
-                    help="1: BASELINE config 1 training step (default); 4: history + Cholesky microbenchmark; "
-                         "5: image preprocessing (row f4)")
+    ap.add_argument("--config", type=int, default=1, choices=[1, 2, 3, 4, 5],
+                    help="1: BASELINE config 1 training step (default); 2, 3: BASELINE configs 2 and 3; "
+                         "4: history + Cholesky microbenchmark; 5: image preprocessing (row f4)")
     ap.add_argument("--ks", type=int, nargs="+", default=[64, 128, 256, 512], help="K values for --config 4")
     args = ap.parse_args()
+    global CFG, WORKLOAD
+    if args.config in TRAIN_CFGS:
+        CFG, WORKLOAD = TRAIN_CFGS[args.config]
+        args.no_cpu_baseline = True
+    if args.batch is None:
+        args.batch = CFG["B"]
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local_rank = _env_int("LOCAL_RANK", 0)

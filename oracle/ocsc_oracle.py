@@ -374,7 +374,6 @@ def synth_images(n: int, dims0, grid, K0: int, filter_dims=(11, 11), seed: int =
     return out
 
 
-# BASELINE.json configs (SURVEY.md 8(d)); rho_code = rho_dict = 1 (BASELINE "rho=1").
 # ---------------------------------------------------------- preprocessing --
 # preprocessing.py:13-100 (row f4): grayscale, Gaussian LCN, seeded edge taper.  scipy's
 # correlate1d(mode="reflect") is restated as np.pad(mode="symmetric") + a sliding dot product
@@ -435,6 +434,7 @@ def preprocess(image, window=9, sigma=3.0, eps=1e-4, size=11, sigma_range=(1.0, 
     return taper(lcn(gray(image), window, sigma, eps), size, s)
 
 
+# BASELINE.json configs (SURVEY.md 8(d)); rho_code = rho_dict = 1 (BASELINE "rho=1").
 CONFIGS = {
     0: dict(n=10, dims0=(100, 100), grid=(100, 100), K0=20, K=100, beta=1.0, B=1, passes=1, dtype="float64"),
     1: dict(n=50_000, dims0=(32, 32), grid=(42, 42), K0=20, K=100, beta=1.0, B=50, passes=1, dtype="float32"),
