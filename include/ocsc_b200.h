@@ -128,6 +128,16 @@ int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void* xh, const
                     const void* den, double beta, double rho, int max_iters, double rel_tol,
                     void* u, void* t, void* uh, double* obj, double* resid, int32_t* iters,
                     int32_t* status, void* stream);
+/* Streaming code ADMM (coding.py:67-119, cold start) for grids whose state does not fit on
+ * chip: the same single-state iteration as ocsc_code_fused with w in `u` (HBM) and
+ * hand-written Good-Thomas row/column FFT passes (100 x 100 and 266 x 266: BASELINE configs
+ * 0, 2, 3).  On return u holds the codes U = S(w); iters/status as ocsc_code_admm.  `work`
+ * holds ocsc_code_stream_workspace_bytes() bytes. */
+int ocsc_code_stream_supported(int dtype, int H, int W);
+size_t ocsc_code_stream_workspace_bytes(int dtype, int H, int W, int K, int B);
+int ocsc_code_stream(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh, const void* den,
+                     double beta, double rho, int max_iters, double rel_tol, void* u, void* work,
+                     int32_t* iters, int32_t* status, int poll, void* stream);
 /* coding.py:122-134 for B codes: uh = rfft2(u) (B, K, nfreq) and
  * obj[b] = 0.5 ||x_b - sum_k w_k (*) u_bk||^2 + beta ||u_b||_1 (double, device);
  * resid[b] (optional) = ||x_b - reconstruction||^2 (evaluate.py:55-62 PSNR input). */

@@ -48,6 +48,9 @@ SIGNATURES = {
     "ocsc_debug_fused_profile": [_P],
     "ocsc_debug_fused_timeline": [_P],
     "ocsc_code_fused": [_I, _I, _I, _I, _I, _P, _P, _P, _D, _D, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P],
+    "ocsc_code_stream_supported": [_I, _I, _I],
+    "ocsc_code_stream_workspace_bytes": [_I, _I, _I, _I, _I],
+    "ocsc_code_stream": [_I, _I, _I, _I, _I, _P, _P, _P, _D, _D, _I, _D, _P, _P, _P, _P, _I, _P],
     "ocsc_code_objective": [_I, _I, _I, _I, _I, _P, _P, _P, _D, _P, _P, _P, _P],
     "ocsc_synthesize": [_I, _I, _I, _I, _P, _P, _P, _P],
     "ocsc_history_accumulate": [_I, _I, _I, _I, _I, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P],
@@ -67,7 +70,8 @@ SIGNATURES = {
     "ocsc_preprocess": [_I, _I, _I, _I, _I, _I, _P, _I, _I, _D, _D, _I, _P, _I64, _D, _D, _P, _P],
     "ocsc_taper_sigmas": [_I64, _I, _D, _D, _P],
 }
-_RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ, "ocsc_history_factor_bytes": _SZ,
+_RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ,
+             "ocsc_code_stream_workspace_bytes": _SZ, "ocsc_history_factor_bytes": _SZ,
              "ocsc_kernel_launches": ctypes.c_int64}
 
 _lib = None

@@ -86,7 +86,10 @@ class CodeBuffers:
         self.u = torch.zeros((B, K, H, W), dtype=dtype, device=dev)
         self.t = torch.zeros((B, K, H, W), dtype=dtype, device=dev)
         self.zh = torch.empty((B, K, H, W // 2 + 1), dtype=cdt, device=dev) if want_z else None
-        nbytes = _lib.load().ocsc_code_workspace_bytes(_lib.code(dtype), H, W, K, B, int(want_z))
+        lib = _lib.load()
+        nbytes = lib.ocsc_code_workspace_bytes(_lib.code(dtype), H, W, K, B, int(want_z))
+        if lib.ocsc_code_stream_supported(_lib.code(dtype), H, W):
+            nbytes = max(nbytes, lib.ocsc_code_stream_workspace_bytes(_lib.code(dtype), H, W, K, B))
         self.work = torch.empty(int(nbytes), dtype=torch.uint8, device=dev)
         self.iters = torch.zeros(B, dtype=torch.int32, device=dev)
         self.status = torch.zeros(B, dtype=torch.int32, device=dev)
@@ -100,6 +103,22 @@ def code_den(Wh: torch.Tensor, rho: float) -> torch.Tensor:
     den = torch.empty(nf, dtype=rdt, device=Wh.device)
     _lib.call("ocsc_code_den", _lib.code(rdt), K, nf, _lib.ptr(Wh), float(rho), _lib.ptr(den), _lib.stream())
     return den
+
+
+def stream_supported(shape: SignalShape, dtype: torch.dtype) -> bool:
+    """True when the streaming FFT kernels (csrc/code_stream.cu) cover this grid and dtype."""
+    H, W = shape.grid
+    return bool(_lib.load().ocsc_code_stream_supported(_lib.code(dtype), H, W))
+
+
+def infer_codes_stream(xh: torch.Tensor, Wh: torch.Tensor, den: torch.Tensor, shape: SignalShape,
+                       config: CodingConfig, buf: CodeBuffers, B: int, poll: int = 16) -> None:
+    """Cold-start batched ADMM through the streaming row/column FFT kernels; codes in buf.u."""
+    H, W = shape.grid
+    _lib.call("ocsc_code_stream", _lib.code(buf.dtype), H, W, buf.K, B, _lib.ptr(xh), _lib.ptr(Wh), _lib.ptr(den),
+              float(config.beta), float(config.rho), int(config.max_iters), float(config.rel_tol),
+              _lib.ptr(buf.u), _lib.ptr(buf.work), _lib.ptr(buf.iters), _lib.ptr(buf.status), int(poll),
+              _lib.stream())
 
 
 def infer_codes(xh: torch.Tensor, Wh: torch.Tensor, den: torch.Tensor, shape: SignalShape,

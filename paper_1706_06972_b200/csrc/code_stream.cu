@@ -1,0 +1,623 @@
+// Streaming code ADMM for grids too large to keep a sample on chip (
+// reference coding.py:67-119) -- BASELINE configs 2 (100 x 100) and 3 (266 x 266).
+//
+// Same iteration as the fused kernel (code_fused.cu), in the single-state form
+//     U = S_kappa(w), Gamma = clip_kappa(w), t = U - Gamma,
+//     g = (X - sum_k D_k F(t_k)) / den,  c_k = F^-1(conj(D_k) g),  w' = S_kappa(w) + c,
+// but with the state w (B, K, H, W) streamed from HBM and the 2-D real FFTs written here
+// as two line passes (rows along W, columns along H), each line a Good-Thomas prime-factor
+// transform of two register FFTs (fft_small.cuh) through shared memory:
+//
+//   k_rows   (per R rows of one sample): inverse row FFT of the column-inverse output ->
+//            c; w' = S(w) + c / P; the four stopping norms; t' = S(w') - clip(w'); forward
+//            row FFT of t' -> back into the same spectrum rows.   HBM: spectrum r+w, w r+w.
+//   k_cols_f (per L columns x K-group of one sample): forward column FFT of every plane,
+//            times D_k, summed over the group in registers -> one partial per group.
+//   k_g      g = (X - sum of partials) / den per frequency.
+//   k_cols_i (per L columns x K-group): conj(D_k) g -> inverse column FFT -> spectrum.
+//   k_decide the per-sample stopping test (code.cu), which freezes converged samples.
+//
+// Per iteration and sample that is 6 passes over K*P reals (spectrum written and read twice,
+// w read and written once) where the cuFFT path needs 10+ (and 5 kernels per 266-point
+// 2-D transform); the row passes of consecutive iterations are fused.  The FFT arithmetic is
+// FP32x2 straight-line code with compile-time twiddles.
+#include <cufft.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "fft_small.cuh"
+#include "transforms.cuh"
+
+namespace ocsc {
+
+__global__ void k_decide(int B, double tol, double* acc, int32_t* flags, int32_t* iters, int32_t* status);
+
+namespace {
+
+using sfft::fft;
+using sfft::modinv;
+
+// ------------------------------------------------------------------ geometry --
+// NR = W/2 = RA * RB and H = CA * CB, coprime pairs (Good-Thomas).  R rows per row-CTA,
+// L columns per column-CTA; thread counts cover the stage-2 tasks of one pass.
+template <typename T, int H_, int W_> struct SGeo;
+
+template <typename T> struct SGeo<T, 100, 100> {
+  static constexpr int H = 100, W = 100, RA = 2, RB = 25, CA = 4, CB = 25;
+  static constexpr int R = 64, NTR = 128;
+  static constexpr int L = 17, NTC = 96;
+};
+template <typename T> struct SGeo<T, 266, 266> {
+  static constexpr int H = 266, W = 266, RA = 7, RB = 19, CA = 14, CB = 19;
+  static constexpr int R = 16, NTR = 128;
+  static constexpr int L = 8, NTC = 128;
+};
+
+template <class G> struct Derived {
+  static constexpr int NR = G::W / 2, WH = G::W / 2 + 1, NF = G::H * WH;
+  static constexpr int PR = NR + 1;  // smem row pitch (complex)
+  static_assert(G::RA * G::RB == NR && G::CA * G::CB == G::H, "factorisation");
+  static_assert(G::L * G::CA <= G::NTC, "column stage-2 tasks must fit one pass");
+  static_assert(G::R * G::RA <= G::NTR, "row stage-2 tasks must fit one pass (in-place stage 2)");
+};
+
+template <typename T>
+__device__ __forceinline__ T shrink(T a, T kappa) {
+  return a > kappa ? a - kappa : (a < -kappa ? a + kappa : (a == a ? (T)0 : a));
+}
+template <typename T>
+__device__ __forceinline__ T clip(T a, T kappa) {
+  return a > kappa ? kappa : (a < -kappa ? -kappa : a);
+}
+
+struct Flags {
+  const int32_t* done;
+  const int32_t* all_done;
+};
+
+// ---------------------------------------------------------------- line FFTs --
+// Good-Thomas line transform of length N = A * B on a shared-memory line (stride 1):
+// stage 1 (tasks n2 < B): A-point DFTs on positions (B n1 + A n2) mod N, in place;
+// stage 2 (tasks k1 < A): B-point DFTs on (B k1 + A n2) mod N; output k = CRT(k1, k2).
+template <int A, int B_>
+struct Pfa {
+  static constexpr int N = A * B_;
+  static constexpr int tB = modinv(B_ % A, A), tA = modinv(A % B_, B_);
+  __device__ static constexpr int in_pos(int n1, int n2) { return (B_ * n1 + A * n2) % N; }
+  __device__ static constexpr int out_pos(int k1, int k2) { return (B_ * tB * k1 + A * tA * k2) % N; }
+};
+
+template <typename C, int A, int B_, bool INV>
+__device__ __forceinline__ void stage1(C* line, int stride, int n2) {
+  using P = Pfa<A, B_>;
+  C v[A];
+#pragma unroll
+  for (int n1 = 0; n1 < A; ++n1) v[n1] = line[P::in_pos(n1, n2) * stride];
+  fft<C, A, INV>(v);
+#pragma unroll
+  for (int n1 = 0; n1 < A; ++n1) line[P::in_pos(n1, n2) * stride] = v[n1];
+}
+
+template <typename C, int A, int B_, bool INV>
+__device__ __forceinline__ void stage2_load(const C* line, int stride, int k1, C (&v)[B_]) {
+  using P = Pfa<A, B_>;
+#pragma unroll
+  for (int n2 = 0; n2 < B_; ++n2) v[n2] = line[P::in_pos(k1, n2) * stride];
+  fft<C, B_, INV>(v);
+}
+
+// stage 2 of the row transform in place: every task loads its B-line into registers, the CTA
+// syncs, then the outputs land in natural order (tasks <= threads, one round); ends synced.
+template <typename C, class G, bool INV>
+__device__ __forceinline__ void row_stage2(C* SA, int nr, int tid) {
+  constexpr int PR = Derived<G>::PR;
+  const bool act = tid < nr * G::RA;
+  const int i = tid / G::RA, k1 = tid - (tid / G::RA) * G::RA;
+  C v[G::RB];
+  if (act) stage2_load<C, G::RA, G::RB, INV>(SA + i * PR, 1, k1, v);
+  __syncthreads();
+  if (act) {
+#pragma unroll
+    for (int k2 = 0; k2 < G::RB; ++k2) SA[i * PR + Pfa<G::RA, G::RB>::out_pos(k1, k2)] = v[k2];
+  }
+  __syncthreads();
+}
+
+// ----------------------------------------------------------------- row pass --
+template <typename T, class G>
+struct RowArgs {
+  int K, B;
+  T kappa, invP;
+  T* w;                 // (B, K, H, W) state
+  cx<T>* spec;          // (B, K, H, WH): in = column-inverse output, out = forward row FFT of t'
+  const cx<T>* tw;      // (WH,) e^{-2 pi i k / W}
+  double* acc;          // (B, 4) stopping norms
+  int32_t* bad;         // (B,) non-finite iterate seen (coding.py:105-106)
+  Flags fl;
+  int first;            // 1: w = 0 before this pass (cold start): c only, no previous state
+};
+
+template <typename T, class G>
+__global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
+  using C = cx<T>;
+  using D = Derived<G>;
+  constexpr int R = G::R, NR = D::NR, WH = D::WH, PR = D::PR, W = G::W, H = G::H;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* SA = reinterpret_cast<C*>(smraw);
+  __shared__ double scratch[4 * 32];
+  const int b = blockIdx.y;
+  if (*a.fl.all_done || a.fl.done[b]) return;
+  const int64_t rows = (int64_t)a.K * H;
+  const int64_t r0 = (int64_t)blockIdx.x * R;
+  const int nr = (int)(rows - r0 < R ? rows - r0 : R);
+  const int tid = threadIdx.x;
+  C* spec = a.spec + ((int64_t)b * rows + r0) * WH;
+  T* w = a.w + ((int64_t)b * rows + r0) * W;
+
+  // 0. prefetch this block's state rows (contiguous) into WB; consumed by the update
+  C* WB = SA + R * PR;
+  if (!a.first) {
+    const C* wsrc = reinterpret_cast<const C*>(w);
+    for (int e = tid; e < nr * NR; e += G::NTR) cp_async<sizeof(C)>(WB + e, wsrc + e);
+    cp_async_commit();
+  }
+  // 1. spectrum rows -> SA
+  for (int e = tid; e < nr * WH; e += G::NTR) {
+    const int i = e / WH, k = e - i * WH;
+    SA[i * PR + k] = spec[(int64_t)i * WH + k];
+  }
+  __syncthreads();
+  // 2. Hermitian pre-processing (pairs k, NR-k): Z = (X_k + X*_{NR-k}) + i e^{+i 2pi k/W}(X_k - X*_{NR-k})
+  for (int e = tid; e < nr * (NR / 2 + 1); e += G::NTR) {
+    const int i = e / (NR / 2 + 1), k = e - i * (NR / 2 + 1);
+    const int k2 = NR - k;
+    C* row = SA + i * PR;
+    const C x1 = row[k], x2 = row[k2];
+    const C t1 = a.tw[k], t2 = a.tw[k2];  // forward twiddles; inverse uses the conjugate
+    // Z[k]
+    const C s1 = mkc<C>(x1.x + x2.x, x1.y - x2.y), d1 = mkc<C>(x1.x - x2.x, x1.y + x2.y);
+    const C r1 = mkc<C>(d1.x * t1.x + d1.y * t1.y, d1.y * t1.x - d1.x * t1.y);  // d1 * conj(t1)
+    const C z1 = mkc<C>(s1.x - r1.y, s1.y + r1.x);
+    // Z[NR-k] (k2 in (0, NR]; for k = 0 it would be Z[NR] which does not exist)
+    const C s2 = mkc<C>(x2.x + x1.x, x2.y - x1.y), d2 = mkc<C>(x2.x - x1.x, x2.y + x1.y);
+    const C r2 = mkc<C>(d2.x * t2.x + d2.y * t2.y, d2.y * t2.x - d2.x * t2.y);
+    const C z2 = mkc<C>(s2.x - r2.y, s2.y + r2.x);
+    row[k] = z1;
+    if (k != 0 && k2 != k) row[k2] = z2;
+  }
+  __syncthreads();
+  // 3. inverse FFT_NR in place: stage 1, then stage 2 through registers (one round of tasks)
+  for (int e = tid; e < nr * G::RB; e += G::NTR) {
+    const int i = e / G::RB, n2 = e - i * G::RB;
+    stage1<C, G::RA, G::RB, true>(SA + i * PR, 1, n2);
+  }
+  __syncthreads();
+  row_stage2<C, G, true>(SA, nr, tid);
+  // 4. update: c = (Re z[n], Im z[n]) = (c[2n], c[2n+1]); w' = S(w) + c/P; norms; t' packed into SA
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  bool nonfinite = false;
+  if (!a.first) {
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  for (int e = tid; e < nr * NR; e += G::NTR) {
+    const int i = e / NR, n = e - i * NR;
+    const C z = SA[i * PR + n];
+    C* wp = reinterpret_cast<C*>(w + (int64_t)i * W) + n;
+    const C wo = a.first ? mkc<C>(0, 0) : WB[e];
+    T uo[2] = {shrink(wo.x, a.kappa), shrink(wo.y, a.kappa)};
+    T go[2] = {wo.x - uo[0], wo.y - uo[1]};
+    T wn[2] = {uo[0] + z.x * a.invP, uo[1] + z.y * a.invP};
+    T tn[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const T un = shrink(wn[j], a.kappa), gn = wn[j] - un;
+      const double d0 = (double)un - uo[j], d2 = (double)gn - go[j];
+      s[0] += d0 * d0;
+      s[1] += (double)un * un;
+      s[2] += d2 * d2;
+      s[3] += (double)gn * gn;
+      tn[j] = un - gn;
+    }
+    nonfinite |= !isfinite(wn[0]) || !isfinite(wn[1]);
+    *wp = mkc<C>(wn[0], wn[1]);
+    SA[i * PR + n] = mkc<C>(tn[0], tn[1]);
+  }
+  if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(a.bad + b, 1);
+  block_sum<4>(s, scratch);  // (contains __syncthreads)
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) atomicAdd(a.acc + 4 * b + j, s[j]);
+  }
+  // 5. forward FFT_NR of t' in place
+  for (int e = tid; e < nr * G::RB; e += G::NTR) {
+    const int i = e / G::RB, n2 = e - i * G::RB;
+    stage1<C, G::RA, G::RB, false>(SA + i * PR, 1, n2);
+  }
+  __syncthreads();
+  row_stage2<C, G, false>(SA, nr, tid);
+  // 6. post-processing X_k = (Z_k + Z*_{NR-k})/2 + e^{-i 2pi k/W} (Z_k - Z*_{NR-k})/(2i), k = 0..NR
+  for (int e = tid; e < nr * WH; e += G::NTR) {
+    const int i = e / WH, k = e - i * WH;
+    const C* row = SA + i * PR;
+    const C z1 = row[k == NR ? 0 : k], z2 = row[k == 0 ? 0 : NR - k];
+    const C s1 = mkc<C>((z1.x + z2.x) * (T)0.5, (z1.y - z2.y) * (T)0.5);
+    const C d1 = mkc<C>((z1.x - z2.x) * (T)0.5, (z1.y + z2.y) * (T)0.5);  // (Z - Z*)/2
+    const C q = mkc<C>(d1.y, -d1.x);                                          // / i
+    const C t = a.tw[k];
+    spec[(int64_t)i * WH + k] = mkc<C>(s1.x + q.x * t.x - q.y * t.y, s1.y + q.x * t.y + q.y * t.x);
+  }
+}
+
+// -------------------------------------------------------------- column passes --
+template <typename T, class G>
+struct ColArgs {
+  int K, B, groups, kper;
+  const cx<T>* Wh;      // (K, H, WH)
+  const cx<T>* xh;      // (B, H, WH)
+  const T* den;         // (H, WH)
+  cx<T>* spec;          // (B, K, H, WH)
+  cx<T>* part;          // (B, groups, H, WH)
+  cx<T>* g;             // (B, H, WH)
+  Flags fl;
+};
+
+// async copy of one plane's L-column block (H rows, row stride WH) into a [H][L] tile
+template <typename C, int H, int L, int NT>
+__device__ __forceinline__ void fetch_block(C* dst, const C* src, int WH, int nc, int tid) {
+  for (int e = tid; e < H * L; e += NT) {
+    const int h = e / L, c = e - h * L;
+    if (c < nc) cp_async<sizeof(C)>(dst + h * L + c, src + (int64_t)h * WH + c);
+  }
+  cp_async_commit();
+}
+
+// forward column FFT of every plane of the group, times D_k, summed in registers.  The
+// spectrum and D_k tiles of plane k+1 stream into the second buffer pair (cp.async)
+// while plane k is transformed.
+template <typename T, class G>
+__global__ void __launch_bounds__(G::NTC) k_cols_f(ColArgs<T, G> a) {
+  using C = cx<T>;
+  using D = Derived<G>;
+  constexpr int L = G::L, H = G::H, WH = D::WH, TILE = H * L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* buf = reinterpret_cast<C*>(smraw);  // [2][Y, Dk][H][L]
+  const int b = blockIdx.z, grp = blockIdx.y, c0 = blockIdx.x * L;
+  if (*a.fl.all_done || a.fl.done[b]) return;
+  const int nc = min(L, WH - c0);
+  const int tid = threadIdx.x;
+  const int k0 = grp * a.kper, k1e = min(a.K, k0 + a.kper);
+  const int c2 = tid % L, q1 = tid / L;  // stage-2 task: column c2, k1 = q1
+  const bool own = q1 < G::CA && c2 < nc;
+  C acc[G::CB];
+#pragma unroll
+  for (int j = 0; j < G::CB; ++j) acc[j] = mkc<C>(0, 0);
+  auto spec_of = [&](int k) { return a.spec + (((int64_t)b * a.K + k) * H) * WH + c0; };
+  auto dict_of = [&](int k) { return a.Wh + (int64_t)k * H * WH + c0; };
+  if (k0 < k1e) {
+    fetch_block<C, H, L, G::NTC>(buf, spec_of(k0), WH, nc, tid);
+    fetch_block<C, H, L, G::NTC>(buf + TILE, dict_of(k0), WH, nc, tid);
+  }
+  for (int k = k0; k < k1e; ++k) {
+    C* Y = buf + ((k - k0) & 1) * 2 * TILE;
+    const C* Dk = Y + TILE;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (k + 1 < k1e) {
+      C* nxt = buf + ((k + 1 - k0) & 1) * 2 * TILE;
+      fetch_block<C, H, L, G::NTC>(nxt, spec_of(k + 1), WH, nc, tid);
+      fetch_block<C, H, L, G::NTC>(nxt + TILE, dict_of(k + 1), WH, nc, tid);
+    }
+    for (int e = tid; e < G::CB * L; e += G::NTC) {
+      const int n2 = e / L, c = e - n2 * L;
+      if (c < nc) stage1<C, G::CA, G::CB, false>(Y + c, L, n2);
+    }
+    __syncthreads();
+    if (own) {
+      C v[G::CB];
+      stage2_load<C, G::CA, G::CB, false>(Y + c2, L, q1, v);
+#pragma unroll
+      for (int k2 = 0; k2 < G::CB; ++k2) {
+        const int row = Pfa<G::CA, G::CB>::out_pos(q1, k2);
+        cfma(acc[k2], Dk[row * L + c2], v[k2]);
+      }
+    }
+  }
+  if (own) {
+    C* dst = (a.groups == 1 ? a.g + (int64_t)b * H * WH : a.part + ((int64_t)b * a.groups + grp) * H * WH) + c0 + c2;
+    if (a.groups == 1) {
+      // g = (X - sum) / den directly
+      const C* x = a.xh + (int64_t)b * H * WH + c0 + c2;
+      const T* dn = a.den + c0 + c2;
+#pragma unroll
+      for (int k2 = 0; k2 < G::CB; ++k2) {
+        const int row = Pfa<G::CA, G::CB>::out_pos(q1, k2);
+        const T inv = (T)1 / dn[row * WH];
+        const C xv = x[(int64_t)row * WH];
+        dst[(int64_t)row * WH] = mkc<C>((xv.x - acc[k2].x) * inv, (xv.y - acc[k2].y) * inv);
+      }
+    } else {
+#pragma unroll
+      for (int k2 = 0; k2 < G::CB; ++k2) {
+        const int row = Pfa<G::CA, G::CB>::out_pos(q1, k2);
+        dst[(int64_t)row * WH] = acc[k2];
+      }
+    }
+  }
+}
+
+// g = (X - sum_groups part) / den  (first iteration: no partials, T = 0)
+template <typename T>
+__global__ void k_gsum(int B, int nf, int groups, const cx<T>* __restrict__ xh, const T* __restrict__ den,
+                       const cx<T>* __restrict__ part, cx<T>* __restrict__ g, Flags fl) {
+  const int b = blockIdx.y;
+  if (*fl.all_done || fl.done[b]) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nf) return;
+  cx<T> s = mkc<cx<T>>(0, 0);
+  if (part)
+    for (int j = 0; j < groups; ++j) s = cadd(s, part[((int64_t)b * groups + j) * nf + p]);
+  const T inv = (T)1 / den[p];
+  const cx<T> x = xh[(int64_t)b * nf + p];
+  g[(int64_t)b * nf + p] = mkc<cx<T>>((x.x - s.x) * inv, (x.y - s.y) * inv);
+}
+
+// conj(D_k) g -> inverse column FFT -> spectrum rows (for the row pass); the D_k tile of
+// plane k+1 streams in (cp.async) while plane k is transformed in the other buffer.
+template <typename T, class G>
+__global__ void __launch_bounds__(G::NTC) k_cols_i(ColArgs<T, G> a) {
+  using C = cx<T>;
+  using D = Derived<G>;
+  constexpr int L = G::L, H = G::H, WH = D::WH, TILE = H * L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* Gs = reinterpret_cast<C*>(smraw);  // [H][L] g tile
+  C* buf = Gs + TILE;                   // [2][H][L] D_k tiles, transformed in place
+  const int b = blockIdx.z, grp = blockIdx.y, c0 = blockIdx.x * L;
+  if (*a.fl.all_done || a.fl.done[b]) return;
+  const int nc = min(L, WH - c0);
+  const int tid = threadIdx.x;
+  const int k0 = grp * a.kper, k1e = min(a.K, k0 + a.kper);
+  auto dict_of = [&](int k) { return a.Wh + (int64_t)k * H * WH + c0; };
+  fetch_block<C, H, L, G::NTC>(Gs, a.g + (int64_t)b * H * WH + c0, WH, nc, tid);
+  if (k0 < k1e) fetch_block<C, H, L, G::NTC>(buf, dict_of(k0), WH, nc, tid);
+  const int c2 = tid % L, q1 = tid / L;
+  const bool own = q1 < G::CA && c2 < nc;
+  for (int k = k0; k < k1e; ++k) {
+    C* Y = buf + ((k - k0) & 1) * TILE;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (k + 1 < k1e) fetch_block<C, H, L, G::NTC>(buf + ((k + 1 - k0) & 1) * TILE, dict_of(k + 1), WH, nc, tid);
+    for (int e = tid; e < G::CB * L; e += G::NTC) {
+      const int n2 = e / L, c = e - n2 * L;
+      if (c < nc) {
+        // stage 1 with the input conj(D_k) g formed on the fly (positions of this task only)
+        using P = Pfa<G::CA, G::CB>;
+        C v[G::CA];
+#pragma unroll
+        for (int n1 = 0; n1 < G::CA; ++n1) {
+          const int idx = P::in_pos(n1, n2) * L + c;
+          v[n1] = cmulc(Y[idx], Gs[idx]);
+        }
+        fft<C, G::CA, true>(v);
+#pragma unroll
+        for (int n1 = 0; n1 < G::CA; ++n1) Y[P::in_pos(n1, n2) * L + c] = v[n1];
+      }
+    }
+    __syncthreads();
+    if (own) {
+      C v[G::CB];
+      stage2_load<C, G::CA, G::CB, true>(Y + c2, L, q1, v);
+      C* dst = a.spec + (((int64_t)b * a.K + k) * H) * WH + c0 + c2;
+#pragma unroll
+      for (int k2 = 0; k2 < G::CB; ++k2) dst[(int64_t)Pfa<G::CA, G::CB>::out_pos(q1, k2) * WH] = v[k2];
+    }
+  }
+}
+
+// final pass: u = S(w) in place
+template <typename T>
+__global__ void k_shrink_inplace(int64_t n, T kappa, T* __restrict__ u) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    u[i] = shrink(u[i], kappa);
+}
+
+// ------------------------------------------------------------------ host side --
+struct StreamWork {
+  void* part;
+  void* g;
+  double* acc;
+  int32_t* flags;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int k_groups(int K, int B, int ncb) {
+  // enough CTAs for ~4 waves of 148 SMs, at least 8 planes per CTA
+  int g = ceil_div(4 * 148, (int64_t)B * ncb);
+  g = std::max(1, std::min(g, K / 4));
+  return g;
+}
+
+size_t stream_layout(int dtype, int H, int W, int K, int B, int groups, StreamWork* w, char* base) {
+  const size_t s = dtype == OCSC_F64 ? 16 : 8;
+  const size_t nf = (size_t)H * (W / 2 + 1);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += align256(bytes); return p; };
+  char* part = take((size_t)B * groups * nf * s);
+  char* g = take((size_t)B * nf * s);
+  char* acc = take((size_t)B * 4 * sizeof(double));
+  char* flags = take((size_t)(2 * B + 2) * sizeof(int32_t));
+  if (w) {
+    w->part = part; w->g = g; w->acc = (double*)acc; w->flags = (int32_t*)flags;
+  }
+  return off;
+}
+
+template <typename T>
+const cx<T>* twiddles(int W) {
+  static std::mutex mu;
+  static std::map<int, void*> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(W);
+  if (it != cache.end()) return (const cx<T>*)it->second;
+  const int n = W / 2 + 1;
+  std::vector<cx<T>> h(n);
+  for (int k = 0; k < n; ++k) {
+    const double a = -2.0 * sfft::kPi * k / W;
+    h[k] = mkc<cx<T>>((T)cos(a), (T)sin(a));
+  }
+  void* d = nullptr;
+  if (cudaMalloc(&d, n * sizeof(cx<T>)) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), n * sizeof(cx<T>), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+  cache[W] = d;
+  return (const cx<T>*)d;
+}
+
+int32_t* pinned_flag() {
+  static int32_t* p = nullptr;
+  if (!p && cudaHostAlloc((void**)&p, 8 * sizeof(int32_t), cudaHostAllocPortable) != cudaSuccess) p = nullptr;
+  return p;
+}
+
+template <typename T, class G>
+int run(int K, int B, const void* xh, const void* Wh, const void* den, double beta, double rho, int max_iters,
+        double rel_tol, void* u, void* work, int32_t* iters, int32_t* status, int poll, cudaStream_t s) {
+  using D = Derived<G>;
+  constexpr int H = G::H, W = G::W, WH = D::WH, NF = D::NF;
+  const int dtype = sizeof(T) == 4 ? OCSC_F32 : OCSC_F64;
+  const int ncb = ceil_div(WH, G::L);
+  const int groups = k_groups(K, B, ncb);
+  const int kper = ceil_div(K, groups);
+  StreamWork sw;
+  stream_layout(dtype, H, W, K, B, groups, &sw, (char*)work);
+  // the spectrum lives in the caller's t buffer region: (B, K, H, WH) complex needs
+  // B*K*H*(W+2) reals; the workspace passed in holds it after the small buffers
+  cx<T>* spec = (cx<T>*)((char*)work + stream_layout(dtype, H, W, K, B, groups, nullptr, nullptr));
+  const cx<T>* tw = twiddles<T>(W);
+  if (!tw) return fail(OCSC_ECUDA, "code_stream: twiddle table allocation failed");
+  OCSC_CUDA(cudaMemsetAsync(sw.acc, 0, sizeof(double) * 4 * B, s));
+  OCSC_CUDA(cudaMemsetAsync(sw.flags, 0, sizeof(int32_t) * (2 * B + 2), s));
+  OCSC_CUDA(cudaMemsetAsync(iters, 0, sizeof(int32_t) * B, s));
+  OCSC_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * B, s));
+  if (B == 0 || max_iters <= 0) {
+    OCSC_CUDA(cudaMemsetAsync(u, 0, sizeof(T) * (size_t)B * K * H * W, s));
+    return OCSC_OK;
+  }
+  Flags fl{sw.flags, sw.flags + 2 * B};
+
+  RowArgs<T, G> ra{K, B, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, spec, tw, sw.acc, sw.flags + B, fl, 1};
+  ColArgs<T, G> ca{K, B, groups, kper, (const cx<T>*)Wh, (const cx<T>*)xh, (const T*)den, spec,
+                   (cx<T>*)sw.part, (cx<T>*)sw.g, fl};
+  const size_t row_smem = (size_t)G::R * (D::PR + D::NR) * sizeof(cx<T>);
+  const size_t colf_smem = 4 * (size_t)H * G::L * sizeof(cx<T>);
+  const size_t coli_smem = 3 * (size_t)H * G::L * sizeof(cx<T>);
+  OCSC_CUDA(cudaFuncSetAttribute(k_rows<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem));
+  OCSC_CUDA(cudaFuncSetAttribute(k_cols_f<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colf_smem));
+  OCSC_CUDA(cudaFuncSetAttribute(k_cols_i<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coli_smem));
+  const dim3 rgrid(ceil_div((int64_t)K * H, G::R), B);
+  const dim3 cgrid(ncb, groups, B);
+  const dim3 ggrid(ceil_div(NF, 256), B);
+
+  int32_t* host = poll > 0 ? pinned_flag() : nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  if (host) {
+    OCSC_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    OCSC_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  }
+  int rc = OCSC_OK, chunk = 0;
+  bool stop = false;
+  for (int it = 1; it <= max_iters && !stop; ++it) {
+    if (it > 1) {
+      k_cols_f<T, G><<<cgrid, G::NTC, colf_smem, s>>>(ca);  // groups == 1: writes g itself
+      count_launches(1);
+      if (groups > 1) {
+        k_gsum<T><<<ggrid, 256, 0, s>>>(B, NF, groups, (const cx<T>*)xh, (const T*)den, (const cx<T>*)sw.part,
+                                        (cx<T>*)sw.g, fl);
+        count_launches(1);
+      }
+    } else {
+      k_gsum<T><<<ggrid, 256, 0, s>>>(B, NF, groups, (const cx<T>*)xh, (const T*)den, nullptr, (cx<T>*)sw.g, fl);
+      count_launches(1);
+    }
+    k_cols_i<T, G><<<cgrid, G::NTC, coli_smem, s>>>(ca);
+    ra.first = it == 1;
+    k_rows<T, G><<<rgrid, G::NTR, row_smem, s>>>(ra);
+    k_decide<<<1, 256, 0, s>>>(B, rel_tol, sw.acc, sw.flags, iters, status);
+    count_launches(3);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { rc = cuda_fail(e, "code_stream launch"); break; }
+    if (host && it % poll == 0 && it < max_iters) {
+      const int slot = chunk & 1;
+      cudaMemcpyAsync(host + slot, sw.flags + 2 * B, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+      cudaEventRecord(ev[slot], s);
+      if (chunk > 0) {
+        cudaEventSynchronize(ev[slot ^ 1]);
+        if (host[slot ^ 1]) stop = true;
+      }
+      ++chunk;
+    }
+  }
+  if (host) {
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+  }
+  if (rc) return rc;
+  const int64_t n = (int64_t)B * K * H * W;
+  k_shrink_inplace<T><<<grid_for(n, 256), 256, 0, s>>>(n, (T)(beta / rho), (T*)u);
+  OCSC_LAUNCHED("k_shrink_inplace");
+  return OCSC_OK;
+}
+
+template <typename T>
+int dispatch(int H, int W, bool query, int K, int B, const void* xh, const void* Wh, const void* den, double beta,
+             double rho, int max_iters, double rel_tol, void* u, void* work, int32_t* iters, int32_t* status,
+             int poll, cudaStream_t s) {
+#define OCSC_STREAM_CASE(HH, WW)                                                                      \
+  if (H == HH && W == WW) {                                                                           \
+    if (query) return 1;                                                                              \
+    return run<T, SGeo<T, HH, WW>>(K, B, xh, Wh, den, beta, rho, max_iters, rel_tol, u, work, iters, \
+                                   status, poll, s);                                                  \
+  }
+  OCSC_STREAM_CASE(100, 100)
+  OCSC_STREAM_CASE(266, 266)
+#undef OCSC_STREAM_CASE
+  return query ? 0 : fail(OCSC_ESHAPE, "code_stream: no streaming instantiation for this grid");
+}
+
+}  // namespace
+}  // namespace ocsc
+
+using namespace ocsc;
+
+extern "C" int ocsc_code_stream_supported(int dtype, int H, int W) {
+  if (dtype == OCSC_F32) return dispatch<float>(H, W, true, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
+  if (dtype == OCSC_F64) return dispatch<double>(H, W, true, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0);
+  return 0;
+}
+
+extern "C" size_t ocsc_code_stream_workspace_bytes(int dtype, int H, int W, int K, int B) {
+  const int WH = W / 2 + 1;
+  const int L = H == 266 ? SGeo<float, 266, 266>::L : SGeo<float, 100, 100>::L;
+  const int groups = k_groups(K, B, ceil_div(WH, L));
+  const size_t s = dtype == OCSC_F64 ? 16 : 8;
+  return stream_layout(dtype, H, W, K, B, groups, nullptr, nullptr) + (size_t)B * K * H * WH * s;
+}
+
+extern "C" int ocsc_code_stream(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
+                                const void* den, double beta, double rho, int max_iters, double rel_tol, void* u,
+                                void* work, int32_t* iters, int32_t* status, int poll, void* stream) {
+  if (H <= 0 || W <= 0 || K <= 0 || B < 0) return fail(OCSC_ESHAPE, "code_stream: bad extents");
+  if (!(rho > 0)) return fail(OCSC_EARG, "code_stream: rho must be positive");
+  cudaStream_t s = as_stream(stream);
+  if (dtype == OCSC_F32)
+    return dispatch<float>(H, W, false, K, B, xh, Wh, den, beta, rho, max_iters, rel_tol, u, work, iters, status,
+                           poll, s);
+  if (dtype == OCSC_F64)
+    return dispatch<double>(H, W, false, K, B, xh, Wh, den, beta, rho, max_iters, rel_tol, u, work, iters, status,
+                            poll, s);
+  return fail(OCSC_EARG, "dtype must be 4 or 8");
+}

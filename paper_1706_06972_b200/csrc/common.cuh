@@ -84,6 +84,20 @@ template <typename To, typename From> __device__ __forceinline__ cx<To> ccast(Fr
   return mkc<cx<To>>((To)a.x, (To)a.y);
 }
 
+// ------------------------------------------------------------ cp.async --
+// Asynchronous global -> shared copies (LDGSTS) of 4/8/16 bytes; commit/wait by group.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if constexpr (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(s), "l"(gmem), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // ------------------------------------------------------------ reductions --
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

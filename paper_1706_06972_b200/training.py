@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .coding import CodeBuffers, CodeState, CodingConfig, code_den, code_objectives, infer_codes
+from .coding import (CodeBuffers, CodeState, CodingConfig, code_den, code_objectives, infer_codes,
+                     infer_codes_stream, stream_supported)
 from .dictionary import DictState, HistoryState
 from .errors import DivergenceError, ShapeMismatchError
 from .transforms import SignalShape, _np, half_to_cols_dev, rfft2_dev
@@ -58,6 +59,7 @@ class TrainConfig:
     history_dtype: str = "float64" # history sums and Cholesky
     poll: int = 16                 # code-ADMM convergence poll interval (iterations)
     fused: bool = True             # on-chip cluster kernel when the grid has one (else cuFFT path)
+    stream: bool = True            # streaming FFT kernels for larger grids that have them (else cuFFT)
     history_solver: str = "auto"   # "gj" explicit inverse (K <= 118/167) | "chol" blocked Cholesky | "auto"
 
     def coding(self) -> CodingConfig:
@@ -278,6 +280,7 @@ class OnlineTrainer:
         xh = rfft2_dev(x, self.shape)
         uh = self._uh[:B]
         fused = self.use_fused(B) and not want_z
+        stream = not fused and not want_z and self.config.stream and stream_supported(self.shape, self.dtype)
         if fused:
             obj = self._obj[:B]
             cc = self.coding_config
@@ -285,6 +288,8 @@ class OnlineTrainer:
                       _lib.ptr(self.Wh), _lib.ptr(self.den), cc.beta, cc.rho, cc.max_iters, cc.rel_tol,
                       _lib.ptr(buf.u), None, _lib.ptr(uh), _lib.ptr(obj), None, _lib.ptr(buf.iters),
                       _lib.ptr(buf.status), _lib.stream())
+        elif stream:
+            infer_codes_stream(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
         else:
             infer_codes(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
         if check:

@@ -552,3 +552,27 @@ def test_preprocessing_reference_properties():
     for i in (0, 37, 63):
         ref = O.preprocess(stack[i].astype(np.float64), seed=11 + i)
         assert np.abs(out[i] - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+# ---------------------------------------------- streaming FFT code path (cfg 0/2/3) --
+
+@pytest.mark.parametrize("dtype,H,K,B", [("float64", 100, 6, 2), ("float32", 100, 8, 3), ("float32", 266, 4, 2),
+                                         ("float64", 266, 3, 1)])
+def test_stream_code_path_matches_cufft_path(dtype, H, K, B):
+    from paper_1706_06972_b200.coding import CodeBuffers, infer_codes, infer_codes_stream, stream_supported
+    from paper_1706_06972_b200.transforms import rfft2_dev
+
+    shape = ob.SignalShape((H, H), (11, 11))
+    rdt = torch.float32 if dtype == "float32" else torch.float64
+    assert stream_supported(shape, rdt)
+    tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=K, dtype=dtype, batch_size=B, beta=0.3))
+    x = torch.from_numpy(O.synth_images(B, (H - 10, H - 10), (H, H), 3, seed=5)).to("cuda", rdt)
+    xh = rfft2_dev(x, shape)
+    cc = ob.CodingConfig(beta=0.3, max_iters=60, rel_tol=1e-3)
+    ref, got = CodeBuffers(shape, K, B, rdt), CodeBuffers(shape, K, B, rdt)
+    infer_codes(xh, tr.Wh, tr.den, shape, cc, ref, B, poll=0)
+    infer_codes_stream(xh, tr.Wh, tr.den, shape, cc, got, B, poll=0)
+    tol = 1e-10 if dtype == "float64" else 2e-4
+    assert rel(got.u.cpu().numpy(), ref.u.cpu().numpy()) < tol
+    if dtype == "float64":
+        assert torch.equal(got.iters, ref.iters) and torch.equal(got.status, ref.status)
