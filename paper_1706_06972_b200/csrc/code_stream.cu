@@ -89,26 +89,40 @@ struct Pfa {
   static constexpr int tB = modinv(B_ % A, A), tA = modinv(A % B_, B_);
   __device__ static constexpr int in_pos(int n1, int n2) { return (B_ * n1 + A * n2) % N; }
   __device__ static constexpr int out_pos(int k1, int k2) { return (B_ * tB * k1 + A * tA * k2) % N; }
+  // base + compile-time offset, both in [0, N): one conditional subtract instead of a modulo
+  template <int OFF>
+  __device__ static __forceinline__ int wrap(int base) {
+    const int p = base + OFF % N;
+    return p >= N ? p - N : p;
+  }
 };
 
 template <typename C, int A, int B_, bool INV>
 __device__ __forceinline__ void stage1(C* line, int stride, int n2) {
   using P = Pfa<A, B_>;
+  const int base = (A * n2) % P::N;
   C v[A];
-#pragma unroll
-  for (int n1 = 0; n1 < A; ++n1) v[n1] = line[P::in_pos(n1, n2) * stride];
+  sfft::static_for<0, A>([&](auto I) { v[I.value] = line[P::template wrap<B_ * I.value>(base) * stride]; });
   fft<C, A, INV>(v);
-#pragma unroll
-  for (int n1 = 0; n1 < A; ++n1) line[P::in_pos(n1, n2) * stride] = v[n1];
+  sfft::static_for<0, A>([&](auto I) { line[P::template wrap<B_ * I.value>(base) * stride] = v[I.value]; });
 }
 
 template <typename C, int A, int B_, bool INV>
 __device__ __forceinline__ void stage2_load(const C* line, int stride, int k1, C (&v)[B_]) {
   using P = Pfa<A, B_>;
-#pragma unroll
-  for (int n2 = 0; n2 < B_; ++n2) v[n2] = line[P::in_pos(k1, n2) * stride];
+  const int base = B_ * k1;  // < N
+  sfft::static_for<0, B_>([&](auto I) { v[I.value] = line[P::template wrap<A * I.value>(base) * stride]; });
   fft<C, B_, INV>(v);
 }
+
+// natural-order row of stage-2 output k2 of task k1
+template <int A, int B_>
+struct OutRow {
+  int base;
+  __device__ __forceinline__ explicit OutRow(int k1) : base((B_ * Pfa<A, B_>::tB * k1) % Pfa<A, B_>::N) {}
+  template <int K2>
+  __device__ __forceinline__ int at() const { return Pfa<A, B_>::template wrap<A * Pfa<A, B_>::tA * K2>(base); }
+};
 
 // stage 2 of the row transform in place: every task loads its B-line into registers, the CTA
 // syncs, then the outputs land in natural order (tasks <= threads, one round); ends synced.
@@ -121,8 +135,8 @@ __device__ __forceinline__ void row_stage2(C* SA, int nr, int tid) {
   if (act) stage2_load<C, G::RA, G::RB, INV>(SA + i * PR, 1, k1, v);
   __syncthreads();
   if (act) {
-#pragma unroll
-    for (int k2 = 0; k2 < G::RB; ++k2) SA[i * PR + Pfa<G::RA, G::RB>::out_pos(k1, k2)] = v[k2];
+    const OutRow<G::RA, G::RB> o(k1);
+    sfft::static_for<0, G::RB>([&](auto K2) { SA[i * PR + o.template at<K2.value>()] = v[K2.value]; });
   }
   __syncthreads();
 }
@@ -198,7 +212,7 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   __syncthreads();
   row_stage2<C, G, true>(SA, nr, tid);
   // 4. update: c = (Re z[n], Im z[n]) = (c[2n], c[2n+1]); w' = S(w) + c/P; norms; t' packed into SA
-  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  T sl[4] = {0, 0, 0, 0};  // per-thread partial norms in T; double from the block reduction on
   bool nonfinite = false;
   if (!a.first) {
     cp_async_wait<0>();
@@ -216,11 +230,11 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const T un = shrink(wn[j], a.kappa), gn = wn[j] - un;
-      const double d0 = (double)un - uo[j], d2 = (double)gn - go[j];
-      s[0] += d0 * d0;
-      s[1] += (double)un * un;
-      s[2] += d2 * d2;
-      s[3] += (double)gn * gn;
+      const T d0 = un - uo[j], d2 = gn - go[j];
+      sl[0] = fma(d0, d0, sl[0]);
+      sl[1] = fma(un, un, sl[1]);
+      sl[2] = fma(d2, d2, sl[2]);
+      sl[3] = fma(gn, gn, sl[3]);
       tn[j] = un - gn;
     }
     nonfinite |= !isfinite(wn[0]) || !isfinite(wn[1]);
@@ -228,6 +242,7 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
     SA[i * PR + n] = mkc<C>(tn[0], tn[1]);
   }
   if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(a.bad + b, 1);
+  double s[4] = {(double)sl[0], (double)sl[1], (double)sl[2], (double)sl[3]};
   block_sum<4>(s, scratch);  // (contains __syncthreads)
   if (tid == 0) {
 #pragma unroll
@@ -320,11 +335,8 @@ __global__ void __launch_bounds__(G::NTC) k_cols_f(ColArgs<T, G> a) {
     if (own) {
       C v[G::CB];
       stage2_load<C, G::CA, G::CB, false>(Y + c2, L, q1, v);
-#pragma unroll
-      for (int k2 = 0; k2 < G::CB; ++k2) {
-        const int row = Pfa<G::CA, G::CB>::out_pos(q1, k2);
-        cfma(acc[k2], Dk[row * L + c2], v[k2]);
-      }
+      const OutRow<G::CA, G::CB> o(q1);
+      sfft::static_for<0, G::CB>([&](auto K2) { cfma(acc[K2.value], Dk[o.template at<K2.value>() * L + c2], v[K2.value]); });
     }
   }
   if (own) {
@@ -396,15 +408,14 @@ __global__ void __launch_bounds__(G::NTC) k_cols_i(ColArgs<T, G> a) {
       if (c < nc) {
         // stage 1 with the input conj(D_k) g formed on the fly (positions of this task only)
         using P = Pfa<G::CA, G::CB>;
+        const int base = (G::CA * n2) % P::N;
         C v[G::CA];
-#pragma unroll
-        for (int n1 = 0; n1 < G::CA; ++n1) {
-          const int idx = P::in_pos(n1, n2) * L + c;
-          v[n1] = cmulc(Y[idx], Gs[idx]);
-        }
+        sfft::static_for<0, G::CA>([&](auto I) {
+          const int idx = P::template wrap<G::CB * I.value>(base) * L + c;
+          v[I.value] = cmulc(Y[idx], Gs[idx]);
+        });
         fft<C, G::CA, true>(v);
-#pragma unroll
-        for (int n1 = 0; n1 < G::CA; ++n1) Y[P::in_pos(n1, n2) * L + c] = v[n1];
+        sfft::static_for<0, G::CA>([&](auto I) { Y[P::template wrap<G::CB * I.value>(base) * L + c] = v[I.value]; });
       }
     }
     __syncthreads();
@@ -412,8 +423,8 @@ __global__ void __launch_bounds__(G::NTC) k_cols_i(ColArgs<T, G> a) {
       C v[G::CB];
       stage2_load<C, G::CA, G::CB, true>(Y + c2, L, q1, v);
       C* dst = a.spec + (((int64_t)b * a.K + k) * H) * WH + c0 + c2;
-#pragma unroll
-      for (int k2 = 0; k2 < G::CB; ++k2) dst[(int64_t)Pfa<G::CA, G::CB>::out_pos(q1, k2) * WH] = v[k2];
+      const OutRow<G::CA, G::CB> o(q1);
+      sfft::static_for<0, G::CB>([&](auto K2) { dst[(int64_t)o.template at<K2.value>() * WH] = v[K2.value]; });
     }
   }
 }
