@@ -166,7 +166,7 @@ def run_b200(args, rank, world, local_rank):
     import paper_1706_06972_b200 as ob
     from paper_1706_06972_b200 import _lib
     from paper_1706_06972_b200.coding import infer_codes
-    from paper_1706_06972_b200.parallel import DistributedTrainer
+    from paper_1706_06972_b200.sharded import DistComm, ShardedTrainer
     from paper_1706_06972_b200.transforms import rfft2_dev
 
     torch.cuda.set_device(local_rank)
@@ -177,7 +177,9 @@ def run_b200(args, rank, world, local_rank):
     cfg = ob.TrainConfig(n_filters=CFG["K"], beta=CFG["beta"], rho_code=CFG["rho_code"], rho_dict=CFG["rho_dict"],
                          inner_iters=CFG["J"], seed=0, code_max_iters=CFG["max_iters"], code_rel_tol=CFG["rel_tol"],
                          dtype="float32", history_dtype="float64", batch_size=B, stop_tol=0.0, poll=16)
-    Trainer = (lambda: DistributedTrainer(shape, cfg)) if world > 1 else (lambda: ob.OnlineTrainer(shape, cfg))
+    # N > 1: samples AND spectrum rows sharded (sharded.py: all_to_all of code spectra, one K x M
+    # all-reduce per dictionary round); N = 1: the plain trainer
+    Trainer = (lambda: ShardedTrainer(shape, cfg, DistComm())) if world > 1 else (lambda: ob.OnlineTrainer(shape, cfg))
     nsteps = args.warmup + args.steps
     P = shape.size
     # rank r owns rows [r*B, (r+1)*B) of each global mini-batch of world*B images
@@ -317,8 +319,10 @@ def run_b200(args, rank, world, local_rank):
                 "config": {"workload": WORKLOAD, "global_batch": world * B, "per_gpu_batch": B,
                            "code_iterations_mean": iters_mean,
                            "l2": "flushed between timed steps (256 MiB device write outside the events)",
-                           "parallelism": f"dp{world} (sample-sharded coding, all-gathered code spectra, "
-                                          f"replicated dictionary)"},
+                           "parallelism": (f"dp{world} x freq{world} (sample-sharded coding; history and "
+                                           f"dictionary ADMM sharded by spectrum rows; all_to_all of code "
+                                           f"spectra + K x M all-reduce per round)" if world > 1 else
+                                           "single GPU")},
                 "roofline": {"bound": "hbm",
                              "kernel": ("k_code_fused (cluster per sample, state in SMEM), one ADMM iteration over "
                                         "the mini-batch" if fused else

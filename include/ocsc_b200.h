@@ -208,6 +208,19 @@ int ocsc_crop_normalize_cols(int dtype, int H, int W, int M0, int M1, int K, con
 /* Support (K, M0*M1) -> spectra (K, H, Wh) via the pruned forward DFT (dict_state_from_filters). */
 int ocsc_support_rfft(int dtype, int H, int W, int M0, int M1, int K, const void* alpha, void* Vh,
                       void* stream);
+/* Frequency-sharded projection (SURVEY.md 8(e) exchange B).  A rank owns rows [u0, u1) of
+ * the (H, Wh) half plane; slice arrays are (K, u1-u0, Wh).
+ * ocsc_crop_irfft_rows: apart (K, M0*M1) float64 = this slice's share of
+ *   crop(irfft2(X + Theta)) (Theta may be NULL); summed over all slices (an all-reduce) it is
+ *   the full crop of dictionary.py:149.
+ * ocsc_normalize_support: alpha = apart / max(||apart_k||, 1) (dictionary.py:150-152).
+ * ocsc_support_rfft_rows: V = rfft2(pad(alpha)) on the slice rows; with D and Theta given also
+ *   Theta += D - V there (dictionary.py:153-154, 205-207). */
+int ocsc_crop_irfft_rows(int dtype, int H, int W, int M0, int M1, int K, int u0, int u1, const void* Xh,
+                         const void* Th, double* apart, void* stream);
+int ocsc_normalize_support(int dtype, int M, int K, const double* apart, void* alpha, void* stream);
+int ocsc_support_rfft_rows(int dtype, int H, int W, int M0, int M1, int K, int u0, int u1, const void* alpha,
+                           void* Vh, const void* Dh, void* Th, void* stream);
 /* Tolerance test of the batch dictionary update (dictionary.py:210-214): per filter k,
  * out[2k] = ||D_k - V_k||^2, out[2k+1] = ||D_k||^2 over the full spectrum, from half spectra
  * (K, H, Wh) with Hermitian weights. */

@@ -67,6 +67,9 @@ SIGNATURES = {
     "ocsc_support_rfft": [_I, _I, _I, _I, _I, _I, _P, _P, _P],
     "ocsc_norms2": [_I, _I64, _P, _P, _P, _P],
     "ocsc_dict_gaps": [_I, _I, _I, _I, _P, _P, _P, _P],
+    "ocsc_crop_irfft_rows": [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P],
+    "ocsc_normalize_support": [_I, _I, _I, _P, _P, _P],
+    "ocsc_support_rfft_rows": [_I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P],
     "ocsc_preprocess": [_I, _I, _I, _I, _I, _I, _P, _I, _I, _D, _D, _I, _P, _I64, _D, _D, _P, _P],
     "ocsc_taper_sigmas": [_I64, _I, _D, _D, _P],
 }

@@ -15,14 +15,20 @@
 
 namespace ocsc {
 
-enum ProjMode { PROJECT = 0, CROP_ONLY = 1, SUPPORT_RFFT = 2 };
+// PROJECT, CROP_ONLY, SUPPORT_RFFT act on the whole half plane.  The frequency-sharded
+// trainer (sharded.py) owns rows [u0, u1) of it: CROP_PARTIAL sums the
+// pruned inverse over those rows only (double partial support, all-reduced across ranks),
+// SUPPORT_RFFT evaluates V on those rows only and, with D and Theta given, takes the dual
+// step there.  Slice arrays are (K, u1-u0, Wh).
+enum ProjMode { PROJECT = 0, CROP_ONLY = 1, SUPPORT_RFFT = 2, CROP_PARTIAL = 3 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0, int M1, const cx<T>* __restrict__ Dh,
-                                                 cx<T>* Th, cx<T>* Vh, T* alpha) {
+__global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0, int M1, int u0, int u1,
+                                                 const cx<T>* __restrict__ Dh, cx<T>* Th, cx<T>* Vh, T* alpha,
+                                                 double* apart) {
   using C = cx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int Wh = W / 2 + 1, nf = H * Wh, M = M0 * M1;
+  const int Wh = W / 2 + 1, nf = (u1 - u0) * Wh, M = M0 * M1;
   C* twH = reinterpret_cast<C*>(smem_raw);  // e^{+2 pi i n / H}
   C* twW = twH + H;                         // e^{+2 pi i n / W}
   C* Y = twW + W;                           // [M0][Wh], reused as Q
@@ -50,10 +56,10 @@ __global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0,
     for (int o = threadIdx.x; o < M0 * Wh; o += blockDim.x) {
       const int m0 = o / Wh, v = o % Wh;
       C acc = mkc<C>(0, 0);
-      int idx = 0;
-      for (int u = 0; u < H; ++u) {
-        C x = Dk[(int64_t)u * Wh + v];
-        if (mode == PROJECT) x = cadd(x, Tk[(int64_t)u * Wh + v]);
+      int idx = (int)(((int64_t)u0 * m0) % H);
+      for (int u = u0; u < u1; ++u) {
+        C x = Dk[(int64_t)(u - u0) * Wh + v];
+        if (Tk) x = cadd(x, Tk[(int64_t)(u - u0) * Wh + v]);
         cfma(acc, x, twH[idx]);
         idx += m0;
         if (idx >= H) idx -= H;
@@ -74,10 +80,15 @@ __global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0,
         idx += m1;
         if (idx >= W) idx -= W;
       }
+      if (mode == CROP_PARTIAL) {
+        apart[(int64_t)k * M + o] = acc * invP;
+        continue;
+      }
       const T a = (T)(acc * invP);
       al[o] = a;
       ss[0] += (double)a * a;
     }
+    if (mode == CROP_PARTIAL) return;
     if (mode == PROJECT) {
       block_sum<1>(ss, scratch);
       if (threadIdx.x == 0) norm_s = 1.0 / fmax(sqrt(ss[0]), 1.0);
@@ -108,10 +119,10 @@ __global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0,
     Y[o] = acc;
   }
   __syncthreads();
-  // pruned forward along u over the whole half plane, fused dual step
+  // pruned forward along u over rows [u0, u1), fused dual step
   C* Vk = Vh + (int64_t)k * nf;
   for (int o = threadIdx.x; o < nf; o += blockDim.x) {
-    const int u = o / Wh, v = o % Wh;
+    const int u = o / Wh + u0, v = o % Wh;
     C acc = mkc<C>(0, 0);
     int idx = 0;
     for (int m0 = 0; m0 < M0; ++m0) {
@@ -120,8 +131,27 @@ __global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0,
       if (idx >= H) idx -= H;
     }
     Vk[o] = acc;
-    if (mode == PROJECT) Tk[o] = cadd(Tk[o], csub(Dk[o], acc));
+    if (Tk && Dk) Tk[o] = cadd(Tk[o], csub(Dk[o], acc));
   }
+}
+
+// alpha_k = (T) apart_k / max(||(T) apart_k||, 1): the projection's normalisation (dictionary.py:150-152)
+// applied to the all-reduced partial supports of the sharded trainer
+template <typename T>
+__global__ void k_normalize_support(int M, const double* __restrict__ apart, T* __restrict__ alpha) {
+  __shared__ double scratch[32];
+  __shared__ double sc_s;
+  const int k = blockIdx.x;
+  double ss[1] = {0.0};
+  for (int o = threadIdx.x; o < M; o += blockDim.x) {
+    const T a = (T)apart[(int64_t)k * M + o];
+    ss[0] += (double)a * a;
+  }
+  block_sum<1>(ss, scratch);
+  if (threadIdx.x == 0) sc_s = 1.0 / fmax(sqrt(ss[0]), 1.0);
+  __syncthreads();
+  const T sc = (T)sc_s;
+  for (int o = threadIdx.x; o < M; o += blockDim.x) alpha[(int64_t)k * M + o] = (T)apart[(int64_t)k * M + o] * sc;
 }
 
 // reference columns: padded (P, K) <- crop/normalise of spatial (P, K)
@@ -164,25 +194,27 @@ __global__ void k_norms2(int64_t n, const T* a, const T* b, double* out) {
 }
 
 template <typename T>
-static int launch_project(int mode, int H, int W, int M0, int M1, int K, const void* Dh, void* Th, void* Vh,
-                          void* alpha, cudaStream_t s) {
+static int launch_project(int mode, int H, int W, int M0, int M1, int K, int u0, int u1, const void* Dh, void* Th,
+                          void* Vh, void* alpha, double* apart, cudaStream_t s) {
   const int Wh = W / 2 + 1;
   const size_t smem = sizeof(cx<T>) * ((size_t)H + W + (size_t)M0 * Wh) + sizeof(T) * (size_t)M0 * M1 + 16;
   if (smem > 227 * 1024) return fail(OCSC_EARG, "dict_project: grid too large for the fused projection");
   OCSC_CUDA(cudaFuncSetAttribute(k_project<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_project<T><<<K, 256, smem, s>>>(mode, H, W, M0, M1, (const cx<T>*)Dh, (cx<T>*)Th, (cx<T>*)Vh, (T*)alpha);
+  k_project<T><<<K, 256, smem, s>>>(mode, H, W, M0, M1, u0, u1, (const cx<T>*)Dh, (cx<T>*)Th, (cx<T>*)Vh,
+                                    (T*)alpha, apart);
   OCSC_LAUNCHED("k_project");
   return OCSC_OK;
 }
 
 static int project_dispatch(int dtype, int mode, int H, int W, int M0, int M1, int K, const void* Dh, void* Th,
-                            void* Vh, void* alpha, void* stream) {
-  if (H <= 0 || W <= 0 || M0 <= 0 || M1 <= 0 || M0 > H || M1 > W || K < 0)
+                            void* Vh, void* alpha, void* stream, int u0 = 0, int u1 = -1, double* apart = nullptr) {
+  if (u1 < 0) u1 = H;
+  if (H <= 0 || W <= 0 || M0 <= 0 || M1 <= 0 || M0 > H || M1 > W || K < 0 || u0 < 0 || u1 > H || u0 > u1)
     return fail(OCSC_ESHAPE, "projection: bad extents");
-  if (K == 0) return OCSC_OK;
+  if (K == 0 || u0 == u1) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
-  if (dtype == OCSC_F32) return launch_project<float>(mode, H, W, M0, M1, K, Dh, Th, Vh, alpha, s);
-  if (dtype == OCSC_F64) return launch_project<double>(mode, H, W, M0, M1, K, Dh, Th, Vh, alpha, s);
+  if (dtype == OCSC_F32) return launch_project<float>(mode, H, W, M0, M1, K, u0, u1, Dh, Th, Vh, alpha, apart, s);
+  if (dtype == OCSC_F64) return launch_project<double>(mode, H, W, M0, M1, K, u0, u1, Dh, Th, Vh, alpha, apart, s);
   return fail(OCSC_EARG, "dtype must be 4 or 8");
 }
 
@@ -193,6 +225,35 @@ using namespace ocsc;
 extern "C" int ocsc_dict_project(int dtype, int H, int W, int M0, int M1, int K, const void* Dh, void* Th,
                                  void* Vh, void* alpha, void* stream) {
   return project_dispatch(dtype, PROJECT, H, W, M0, M1, K, Dh, Th, Vh, alpha, stream);
+}
+
+extern "C" int ocsc_crop_irfft_rows(int dtype, int H, int W, int M0, int M1, int K, int u0, int u1,
+                                    const void* Xh, const void* Th, double* apart, void* stream) {
+  if (u0 == u1) {  // an empty slice contributes zero to the all-reduce
+    if (K > 0 && apart) OCSC_CUDA(cudaMemsetAsync(apart, 0, sizeof(double) * K * M0 * M1, as_stream(stream)));
+    return OCSC_OK;
+  }
+  return project_dispatch(dtype, CROP_PARTIAL, H, W, M0, M1, K, Xh, (void*)Th, nullptr, nullptr, stream, u0, u1,
+                          apart);
+}
+
+extern "C" int ocsc_support_rfft_rows(int dtype, int H, int W, int M0, int M1, int K, int u0, int u1,
+                                      const void* alpha, void* Vh, const void* Dh, void* Th, void* stream) {
+  if ((Dh == nullptr) != (Th == nullptr)) return fail(OCSC_EARG, "support_rfft_rows: D and Theta go together");
+  return project_dispatch(dtype, SUPPORT_RFFT, H, W, M0, M1, K, Dh, Th, Vh, (void*)alpha, stream, u0, u1);
+}
+
+extern "C" int ocsc_normalize_support(int dtype, int M, int K, const double* apart, void* alpha, void* stream) {
+  if (K <= 0 || M <= 0) return OCSC_OK;
+  cudaStream_t s = as_stream(stream);
+  if (dtype == OCSC_F32)
+    k_normalize_support<float><<<K, 256, 0, s>>>(M, apart, (float*)alpha);
+  else if (dtype == OCSC_F64)
+    k_normalize_support<double><<<K, 256, 0, s>>>(M, apart, (double*)alpha);
+  else
+    return fail(OCSC_EARG, "dtype must be 4 or 8");
+  OCSC_LAUNCHED("k_normalize_support");
+  return OCSC_OK;
 }
 
 extern "C" int ocsc_crop_irfft(int dtype, int H, int W, int M0, int M1, int K, const void* Xh, void* alpha,

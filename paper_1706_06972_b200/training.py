@@ -179,9 +179,7 @@ class OnlineTrainer:
         self.Dh = self.Wh.clone()
         self.Th = torch.zeros_like(self.Wh)
         self.den = code_den(self.Wh, self.coding_config.rho)
-        # the inverse the J row solves re-read is stored at the arithmetic precision
-        self.history = _HalfHistory(shape, K, config.rho_dict, nfreq=self.nf, dtype=hist_cdtype,
-                                    inv_dtype=self.cdtype, solver=config.history_solver)
+        self.history = self._make_history(hist_cdtype)
         self.rng = np.random.default_rng(config.seed)
         self._prev_code = None
         self._prev_alpha = self.alpha.clone()
@@ -196,6 +194,11 @@ class OnlineTrainer:
         self._fused_ok = {}
 
     # ---------------------------------------------------------- internals --
+    def _make_history(self, hist_cdtype: torch.dtype) -> HistoryState:
+        # the inverse the J row solves re-read is stored at the arithmetic precision
+        return _HalfHistory(self.shape, self.K, self.config.rho_dict, nfreq=self.nf, dtype=hist_cdtype,
+                            inv_dtype=self.cdtype, solver=self.config.history_solver)
+
     def _support_rfft(self, alpha: torch.Tensor, out: torch.Tensor) -> None:
         _lib.call("ocsc_support_rfft", _lib.code(self.dtype), self.H, self.W, self.M0, self.M1, self.K,
                   _lib.ptr(alpha), _lib.ptr(out), _lib.stream())

@@ -160,3 +160,59 @@ def test_taper_sigmas_match_numpy_default_rng():
     for s in (2**32 - 1, 2**32, 2**40 + 5, 2**63 - 1):
         assert taper_sigma(PreprocessSpec(seed=s)) == float(np.random.default_rng(s).uniform(1.0, 3.0))
     assert taper_sigmas(7, 1, (0.5, 4.0))[0] == np.random.default_rng(7).uniform(0.5, 4.0)
+
+
+def test_row_slices_partition():
+    from paper_1706_06972_b200.sharded import row_slices
+
+    for H, G in [(42, 1), (42, 4), (5, 2), (3, 4), (266, 8)]:
+        rows = row_slices(H, G)
+        assert len(rows) == G and rows[0][0] == 0 and rows[-1][1] == H
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        sizes = [b - a for a, b in rows]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def _exchange_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from paper_1706_06972_b200.sharded import DistComm, exchange_codes, row_slices
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        B, K, H, Wh = 2, 3, 5, 4
+        g = torch.Generator().manual_seed(0)
+        uh_all = torch.complex(torch.randn(world * B, K, H, Wh, generator=g, dtype=torch.float64),
+                               torch.randn(world * B, K, H, Wh, generator=g, dtype=torch.float64))
+        xh_all = torch.complex(torch.randn(world * B, H, Wh, generator=g, dtype=torch.float64),
+                               torch.randn(world * B, H, Wh, generator=g, dtype=torch.float64))
+        rows = row_slices(H, world)
+        comm = DistComm()
+        z, x = exchange_codes(uh_all[rank * B:(rank + 1) * B], xh_all[rank * B:(rank + 1) * B], rows, comm)
+        u0, u1 = rows[rank]
+        ok = torch.equal(z, uh_all[:, :, u0:u1].reshape(world * B, K, -1)) and \
+            torch.equal(x, xh_all[:, u0:u1].reshape(world * B, -1))
+        # exchange B: the partial supports sum to the same value on every rank
+        part = torch.full((4,), float(rank + 1), dtype=torch.float64)
+        comm.all_reduce_(part)
+        out.put((rank, bool(ok), float(part[0])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_frequency_exchange():
+    """Exchange A of the frequency-sharded trainer over gloo: each rank receives every sample's
+    spectra restricted to its rows, in rank order (uneven row split 3 + 2)."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[1] for r in res] == [True, True]
+    assert [r[2] for r in res] == [3.0, 3.0]

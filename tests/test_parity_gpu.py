@@ -576,3 +576,134 @@ def test_stream_code_path_matches_cufft_path(dtype, H, K, B):
     assert rel(got.u.cpu().numpy(), ref.u.cpu().numpy()) < tol
     if dtype == "float64":
         assert torch.equal(got.iters, ref.iters) and torch.equal(got.status, ref.status)
+
+
+# ------------------------------------------------- frequency sharding --
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_sharded_projection_slices_tile_the_full_projection(dtype):
+    """Exchange B identities: partial crops over row slices sum to the full crop, and the
+    slice forward DFTs (with the dual step) tile the full projection."""
+    from paper_1706_06972_b200 import _lib
+    from paper_1706_06972_b200.sharded import row_slices
+
+    H, W, M0, M1, K = 14, 12, 5, 4, 3
+    rdt = torch.float32 if dtype == "float32" else torch.float64
+    cdt = torch.complex64 if dtype == "float32" else torch.complex128
+    dt, Wh = _lib.code(rdt), W // 2 + 1
+    g = torch.Generator(device="cuda").manual_seed(3)
+    D = torch.randn(K, H, Wh, dtype=cdt, device="cuda", generator=g)
+    T = torch.randn(K, H, Wh, dtype=cdt, device="cuda", generator=g)
+    # full projection
+    Tf, Vf = T.clone(), torch.empty_like(D)
+    af = torch.empty(K, M0 * M1, dtype=rdt, device="cuda")
+    _lib.call("ocsc_dict_project", dt, H, W, M0, M1, K, _lib.ptr(D), _lib.ptr(Tf), _lib.ptr(Vf), _lib.ptr(af),
+              _lib.stream())
+    for G in (1, 3, 5):
+        rows = row_slices(H, G)
+        total = torch.zeros(K, M0 * M1, dtype=torch.float64, device="cuda")
+        for u0, u1 in rows:
+            part = torch.empty_like(total)
+            Ds, Ts = D[:, u0:u1].contiguous(), T[:, u0:u1].contiguous()  # keep the slices alive
+            _lib.call("ocsc_crop_irfft_rows", dt, H, W, M0, M1, K, u0, u1, _lib.ptr(Ds), _lib.ptr(Ts),
+                      _lib.ptr(part), _lib.stream())
+            total += part
+        alpha = torch.empty_like(af)
+        _lib.call("ocsc_normalize_support", dt, M0 * M1, K, _lib.ptr(total), _lib.ptr(alpha), _lib.stream())
+        tol = 1e-12 if dtype == "float64" else 1e-5
+        assert rel(alpha.cpu().numpy(), af.cpu().numpy()) < tol
+        for u0, u1 in rows:
+            Ds, Ts = D[:, u0:u1].clone(), T[:, u0:u1].clone()  # the dual step updates Ts in place
+            Vs = torch.empty_like(Ds)
+            _lib.call("ocsc_support_rfft_rows", dt, H, W, M0, M1, K, u0, u1, _lib.ptr(af), _lib.ptr(Vs),
+                      _lib.ptr(Ds), _lib.ptr(Ts), _lib.stream())
+            assert torch.equal(Vs, Vf[:, u0:u1]) and torch.equal(Ts, Tf[:, u0:u1])
+
+
+def test_sharded_trainer_world1_equals_online_trainer():
+    """The frequency-sharded code path at world 1 (LocalComm) reproduces OnlineTrainer bit for bit."""
+    from paper_1706_06972_b200.sharded import ShardedTrainer
+
+    shape = ob.SignalShape((18, 12), (3, 3))
+    cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=3, beta=0.3, code_max_iters=80, inner_iters=4)
+    X = O.synth_images(6, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(6, -1)
+    a, b = ob.OnlineTrainer(shape, cfg), ShardedTrainer(shape, cfg)
+    for i in range(2):
+        ra, rb = a.partial_fit(X[3 * i:3 * i + 3]), b.partial_fit(X[3 * i:3 * i + 3])
+        assert np.array_equal(ra.objectives, rb.objectives)
+    assert torch.equal(a.alpha, b.alpha) and torch.equal(a.Wh, b.Wh)
+    assert np.abs(a.final_filters() - b.final_filters()).max() < 1e-13
+
+
+def test_sharded_history_rows_equal_full_history_rows():
+    """Exchange A + slice fold: accumulating a row slice gives exactly those rows of the full fold."""
+    from paper_1706_06972_b200.sharded import LocalComm, exchange_codes, row_slices
+    from paper_1706_06972_b200.training import _HalfHistory
+
+    shape = ob.SignalShape((10, 8), (3, 3))
+    K, B, H, Wh = 4, 5, 10, 5
+    g = torch.Generator(device="cuda").manual_seed(1)
+    uh = torch.randn(B, K, H, Wh, dtype=torch.complex64, device="cuda", generator=g)
+    xh = torch.randn(B, H, Wh, dtype=torch.complex64, device="cuda", generator=g)
+    full = _HalfHistory(shape, K, 1.0, nfreq=H * Wh, dtype=torch.complex128)
+    full.accumulate(uh, (K * H * Wh, H * Wh, 1), xh, (H * Wh, 1), B)
+    for u0, u1 in row_slices(H, 3):
+        nfl = (u1 - u0) * Wh
+        part = _HalfHistory(shape, K, 1.0, nfreq=nfl, dtype=torch.complex128)
+        z, x = exchange_codes(uh, xh, [(u0, u1)], LocalComm())
+        part.accumulate(z, (K * nfl, nfl, 1), x, (nfl, 1), B)
+        assert torch.equal(part.S, full.S[u0 * Wh:u1 * Wh]) and torch.equal(part.c, full.c[u0 * Wh:u1 * Wh])
+
+
+def _sharded_worker(rank, world, port, exchange, out):
+    import torch.distributed as dist
+
+    from paper_1706_06972_b200.sharded import DistComm, ShardedTrainer
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        shape = ob.SignalShape((18, 12), (3, 3))
+        cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=2, beta=0.3, code_max_iters=80, inner_iters=4)
+        X = O.synth_images(8, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(8, -1)
+        tr = ShardedTrainer(shape, cfg, DistComm(), exchange=exchange)
+        objs = []
+        for i in range(2):  # global mini-batches of 4 = 2 ranks x 2
+            g = X[4 * i:4 * i + 4]
+            objs.append(tr.partial_fit(g[2 * rank:2 * rank + 2]).objectives)
+        out.put((rank, tr.alpha.cpu().numpy(), np.concatenate(objs), tr.final_filters(), tr.dict_change))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("exchange", ["all_to_all", "reduce_scatter"])
+def test_sharded_trainer_two_ranks_matches_single_gpu(exchange):
+    """Two frequency-sharded ranks (gloo, host-staged collectives, both on cuda:0 -- no device
+    collective waits on another rank's kernels) reproduce the single-GPU trainer fed the global
+    mini-batches: history rows, per-round K x M all-reduce, exchange C."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    shape = ob.SignalShape((18, 12), (3, 3))
+    cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=4, beta=0.3, code_max_iters=80, inner_iters=4)
+    X = O.synth_images(8, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(8, -1)
+    ref = ob.OnlineTrainer(shape, cfg)
+    ref_obj = np.concatenate([ref.partial_fit(X[4 * i:4 * i + 4]).objectives for i in range(2)])
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, exchange, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in procs), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    for rank, alpha, objs, filt, dchg in res:
+        assert rel(alpha, ref.alpha.cpu().numpy()) < 1e-11
+        mine = np.concatenate([ref_obj[4 * i + 2 * rank:4 * i + 2 * rank + 2] for i in range(2)])
+        assert rel(objs, mine) < 1e-11
+        assert rel(filt, ref.final_filters()) < 1e-11
+        assert abs(dchg - ref.dict_change) <= 1e-9 * abs(ref.dict_change)
