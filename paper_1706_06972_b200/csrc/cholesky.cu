@@ -12,10 +12,12 @@
 // solve then runs two blocked triangular solves per frequency and round:
 //   conj(d) = L^-H L^-1 (c + ridge conj(v - theta)).
 #include "common.cuh"
+#include "fft_small.cuh"
 #include "transforms.cuh"
 
 namespace ocsc {
 
+using sfft::static_for;
 constexpr int CT = 32;  // tile edge
 
 template <typename C>
@@ -23,135 +25,229 @@ __device__ __forceinline__ C* tile_ptr(C* L, int K, int ib, int jb) {
   return L + (int64_t)ib * CT * K + (int64_t)jb * CT;
 }
 
-// A (packed lower, K(K+1)/2 per frequency) + ridge I -> full lower L = chol(A)
+template <typename T>
+__host__ __device__ constexpr int chol_panel_offset() {
+  // L_kk [CT][CT+1] complex + 1/L_jj [CT] real, rounded up to 16 bytes
+  return (int)(((sizeof(cx<T>) * CT * (CT + 1) + sizeof(T) * (CT + 2)) + 15) / 16 * 16);
+}
+
+// four consecutive complex values from 16-byte aligned shared memory
+__device__ __forceinline__ void load4(const float2* p, float2 (&v)[4]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w); v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+}
+__device__ __forceinline__ void load4(const double2* p, double2 (&v)[4]) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) v[r] = p[r];
+}
+
+// acc += a * conj(b) on 2-wide FP32 (FFMA2) / FP64 pairs: acc += a * b.x + (a.y, -a.x) * b.y
+template <typename C>
+__device__ __forceinline__ void cmac_conj2(C& acc, C a, C as, decltype(C::x) bx, decltype(C::x) by) {
+  acc = vfma(a, vsplat<C>(bx), acc);
+  acc = vfma(as, vsplat<C>(by), acc);
+}
+
+// A (packed lower, K(K+1)/2 per frequency) + ridge I -> full-layout lower L = chol(A).
+// One CTA (256 threads) per frequency, right-looking over 32-wide tile columns:
+//   diagonal tile: warp 0, lane = row, the row in registers, 32 shuffle steps (no CTA barrier);
+//   panel:         thread per row, X = A L_kk^-H by substitution against L_kk in SMEM;
+//                  the panel is also written transposed (k-major) into SMEM;
+//   trailing:      A22 -= P P^H over the lower triangle as 64 x 64 block pairs, 16 x 16 threads
+//                  x 4 x 4 complex, two 2-wide FMAs per complex multiply-add (HERK microkernel);
+//                  target values are loaded before the products so their latency overlaps them.
 template <typename T>
 __global__ void __launch_bounds__(256) k_chol_blocked(int K, const cx<T>* __restrict__ S, T ridge, cx<T>* Lall,
                                                       int32_t* info) {
   using C = cx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int LD = CT + 1;
+  C* D = reinterpret_cast<C*>(smem_raw);  // L_kk [CT][LD]
+  T* dinv = reinterpret_cast<T*>(D + CT * LD);   // 1 / L_jj [CT]
+  C* PT = reinterpret_cast<C*>(smem_raw + chol_panel_offset<T>());  // panel, k-major: PT[k][r]
   const int nb = K / CT;
-  C* D = reinterpret_cast<C*>(smem_raw);          // diagonal tile [CT][CT+1]
-  C* Pn = D + CT * (CT + 1);                      // panel tiles [nb][CT][CT+1]
   const int p = blockIdx.x;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
   const C* Sp = S + (int64_t)p * npk;
   C* L = Lall + (int64_t)p * K * K;
-  constexpr int LD = CT + 1;
+  const int PR = K - CT + 64;  // panel row stride: K - CT rows + slack for the last 64-block
 
-  // expand the packed lower triangle (+ ridge) into the full-layout workspace
-  for (int64_t e = tid; e < (int64_t)K * K; e += nt) {
-    const int i = (int)(e / K), j = (int)(e % K);
-    C v = mkc<C>(0, 0);
-    if (j <= i) {
-      v = Sp[packed_index(i, j)];
-      if (i == j) v = mkc<C>(v.x + ridge, (T)0);
+  // expand the packed lower triangle (+ ridge) into the lower half of the full layout
+  for (int i = warp; i < K; i += 8) {
+    const C* src = Sp + packed_index(i, 0);
+    C* dst = L + (int64_t)i * K;
+    for (int j = lane; j <= i; j += 32) {
+      C v = src[j];
+      if (j == i) v = mkc<C>(v.x + ridge, (T)0);
+      dst[j] = v;
     }
-    L[e] = v;
   }
   __syncthreads();
 
   for (int kb = 0; kb < nb; ++kb) {
-    // ---- factor the diagonal tile in shared memory (unblocked, right-looking) ----
-    C* Lkk = tile_ptr(L, K, kb, kb);
-    for (int e = tid; e < CT * CT; e += nt) {
-      const int i = e / CT, j = e % CT;
-      D[i * LD + j] = Lkk[(int64_t)i * K + j];
-    }
-    __syncthreads();
-    for (int j = 0; j < CT; ++j) {
-      if (tid == 0) {
-        T d = D[j * LD + j].x;
+    const int r0 = (kb + 1) * CT;  // first trailing row
+    const int R = K - r0;          // trailing rows
+    // ---- diagonal tile: warp 0, lane i holds row i of the tile ----
+    if (warp == 0) {
+      C a[CT];
+      const C* row = L + (int64_t)(kb * CT + lane) * K + kb * CT;
+#pragma unroll
+      for (int j = 0; j < CT; ++j) a[j] = j <= lane ? row[j] : mkc<C>(0, 0);
+      static_for<0, CT>([&](auto J) {
+        constexpr int j = decltype(J)::value;
+        T d = __shfl_sync(0xffffffffu, a[j].x, j);
         if (!(d > (T)0)) {
-          atomicCAS(info, 0, p + 1);
+          if (lane == 0) atomicCAS(info, 0, p + 1);
           d = (T)NAN;
         }
-        D[j * LD + j] = mkc<C>(sqrt(d), (T)0);
-      }
-      __syncthreads();
-      const T inv = (T)1 / D[j * LD + j].x;
-      for (int i = j + 1 + tid; i < CT; i += nt) D[i * LD + j] = cscale(D[i * LD + j], inv);
-      __syncthreads();
-      for (int e = tid; e < CT * CT; e += nt) {
-        const int i = e / CT, k = e % CT;
-        if (k > j && k <= i) {
-          const C a = D[i * LD + j], bb = D[k * LD + j];
-          C& t = D[i * LD + k];
-          t.x -= a.x * bb.x + a.y * bb.y;  // a conj(b)
-          t.y -= a.y * bb.x - a.x * bb.y;
-        }
-      }
-      __syncthreads();
-    }
-    for (int e = tid; e < CT * CT; e += nt) {
-      const int i = e / CT, j = e % CT;
-      Lkk[(int64_t)i * K + j] = j <= i ? D[i * LD + j] : mkc<C>(0, 0);
-    }
-    // ---- panel: X = A[ib][kb] Lkk^-H, one thread per panel row, in place in shared memory ----
-    const int prow = (nb - kb - 1) * CT;
-    for (int rr = tid; rr < prow; rr += nt) {
-      const int ib = kb + 1 + rr / CT, i = rr % CT;
-      const C* arow = tile_ptr(L, K, ib, kb) + (int64_t)i * K;
-      C* x = Pn + ((ib - kb - 1) * CT + i) * LD;
-      for (int j = 0; j < CT; ++j) x[j] = arow[j];
-    }
-    __syncthreads();
-    for (int rr = tid; rr < prow; rr += nt) {
-      C* x = Pn + rr * LD;
-      // x L^H = a  ->  x_j = (a_j - sum_{k<j} x_k conj(L_jk)) / L_jj
+        const T ljj = sqrt(d), inv = (T)1 / ljj;
+        if (lane == j) a[j] = mkc<C>(ljj, (T)0);
+        else if (lane > j) a[j] = cscale(a[j], inv);
+        if (lane == 0) dinv[j] = inv;
+        static_for<j + 1, CT>([&](auto Kk) {
+          constexpr int k = decltype(Kk)::value;
+          const T lx = __shfl_sync(0xffffffffu, a[j].x, k), ly = __shfl_sync(0xffffffffu, a[j].y, k);
+          if (lane >= k) {  // a[k] -= L[i][j] conj(L[k][j])
+            a[k].x -= a[j].x * lx + a[j].y * ly;
+            a[k].y -= a[j].y * lx - a[j].x * ly;
+          }
+        });
+      });
+      C* out = L + (int64_t)(kb * CT + lane) * K + kb * CT;
+#pragma unroll
       for (int j = 0; j < CT; ++j) {
+        D[lane * LD + j] = a[j];
+        if (j <= lane) out[j] = a[j];
+      }
+    }
+    __syncthreads();
+    if (R == 0) break;
+    // ---- panel: x L_kk^H = a for every trailing row (thread per row) ----
+    for (int rr = tid; rr < R; rr += 256) {
+      C x[CT];
+      C* row = L + (int64_t)(r0 + rr) * K + kb * CT;
+#pragma unroll
+      for (int j = 0; j < CT; ++j) x[j] = row[j];
+      static_for<0, CT>([&](auto J) {
+        constexpr int j = decltype(J)::value;
         C acc = x[j];
-        for (int k = 0; k < j; ++k) {
-          const C l = D[j * LD + k], xk = x[k];
-          acc.x -= xk.x * l.x + xk.y * l.y;
-          acc.y -= xk.y * l.x - xk.x * l.y;
-        }
-        x[j] = cscale(acc, (T)1 / D[j * LD + j].x);
+        static_for<0, j>([&](auto Kk) {  // acc -= x_k conj(L_jk)
+          constexpr int k = decltype(Kk)::value;
+          const C l = D[j * LD + k];
+          acc.x -= x[k].x * l.x + x[k].y * l.y;
+          acc.y -= x[k].y * l.x - x[k].x * l.y;
+        });
+        x[j] = cscale(acc, dinv[j]);
+      });
+#pragma unroll
+      for (int j = 0; j < CT; ++j) {
+        row[j] = x[j];
+        PT[j * PR + rr] = x[j];
       }
     }
     __syncthreads();
-    for (int e = tid; e < prow * CT; e += nt) {  // write the panel back (coalesced)
-      const int rr = e / CT, j = e % CT;
-      const int ib = kb + 1 + rr / CT, i = rr % CT;
-      tile_ptr(L, K, ib, kb)[(int64_t)i * K + j] = Pn[rr * LD + j];
-    }
-    __syncthreads();
-    // ---- trailing update: A[ib][jb] -= P_ib P_jb^H for kb < jb <= ib ----
-    // one warp per 32 x 32 target tile, lane = target column: per k, one own panel value
-    // and 32 broadcast panel values feed 32 complex FMAs
-    const int nrem = nb - kb - 1;
-    const int ntile = nrem * (nrem + 1) / 2;
-    const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
-    for (int t = warp; t < ntile; t += nwarps) {
-      int I = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-      while (I * (I + 1) / 2 > t) --I;
-      while ((I + 1) * (I + 2) / 2 <= t) ++I;
-      const int J = t - I * (I + 1) / 2;  // panel tile indices, J <= I
-      const C* Pi = Pn + I * CT * LD;
-      const C* Pj = Pn + J * CT * LD;
-      C acc[CT];
+    // ---- trailing update A22 -= P P^H, 64 x 64 block pairs (bi >= bj) ----
+    const int nb64 = (R + 63) / 64;
+    const int ty = tid >> 4, tx = tid & 15;
+    for (int pr = 0; pr < nb64 * (nb64 + 1) / 2; ++pr) {
+      int bi = (int)((sqrtf(8.0f * pr + 1.0f) - 1.0f) * 0.5f);
+      while (bi * (bi + 1) / 2 > pr) --bi;
+      while ((bi + 1) * (bi + 2) / 2 <= pr) ++bi;
+      const int bj = pr - bi * (bi + 1) / 2;
+      const int i0 = bi * 64 + ty * 4, j0 = bj * 64 + tx * 4;  // trailing-local rows / cols
+      C acc[4][4], tgt[4][4];
 #pragma unroll
-      for (int i = 0; i < CT; ++i) acc[i] = mkc<C>(0, 0);
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // targets load while the products accumulate from zero
+          const int i = i0 + r, j = j0 + q;
+          tgt[r][q] = (i < R && j <= i) ? L[(int64_t)(r0 + i) * K + r0 + j] : mkc<C>(0, 0);
+          acc[r][q] = mkc<C>(0, 0);
+        }
+      if (i0 < R && j0 <= i0 + 3) {
 #pragma unroll 4
-      for (int k = 0; k < CT; ++k) {
-        const C bj = Pj[lane * LD + k];  // P_jb[lane][k]
+        for (int k = 0; k < CT; ++k) {
+          // rows past R read panel slack: they only feed outputs that are never stored
+          C zi[4], zs[4], zj[4];
+          load4(PT + k * PR + i0, zi);
+          load4(PT + k * PR + j0, zj);
 #pragma unroll
-        for (int i = 0; i < CT; ++i) cfmac(acc[i], bj, Pi[i * LD + k]);  // P_ib[i][k] conj(P_jb[lane][k])
-      }
-      C* tgt = tile_ptr(L, K, kb + 1 + I, kb + 1 + J) + lane;
+          for (int r = 0; r < 4; ++r) zs[r] = mkc<C>(zi[r].y, -zi[r].x);
 #pragma unroll
-      for (int i = 0; i < CT; ++i) {
-        if (I != J || lane <= i) {
-          C& v = tgt[(int64_t)i * K];
-          v = csub(v, acc[i]);
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cmac_conj2(acc[r][q], zi[r], zs[r], -zj[q].x, -zj[q].y);
         }
       }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = i0 + r, j = j0 + q;
+          if (i < R && j <= i) L[(int64_t)(r0 + i) * K + r0 + j] = cadd(tgt[r][q], acc[r][q]);
+        }
     }
     __syncthreads();
   }
 }
 
-// conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)), one CTA per frequency
+// Whole-matrix Cholesky in shared memory for K <= 64 (config 4's K = 64): unblocked
+// right-looking, one column per step, thread per trailing column.  Small CTAs (two warps,
+// <= 65 KB) so many frequencies are in flight per SM; no global traffic besides reading S
+// and writing L once.
+template <typename T>
+__global__ void __launch_bounds__(128) k_chol_smem(int K, const cx<T>* __restrict__ S, T ridge, cx<T>* Lall,
+                                                   int32_t* info) {
+  using C = cx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* A = reinterpret_cast<C*>(smem_raw);  // [K][K+1], lower triangle used
+  const int LD = K + 1;
+  const int p = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int npk = K * (K + 1) / 2;
+  const C* Sp = S + (int64_t)p * npk;
+  for (int e = tid; e < npk; e += nt) {  // flat, coalesced, independent loads of the packed triangle
+    int i = (int)((sqrtf(8.0f * e + 1.0f) - 1.0f) * 0.5f);
+    while (i * (i + 1) / 2 > e) --i;
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    const int j = e - i * (i + 1) / 2;
+    C v = Sp[e];
+    if (i == j) v = mkc<C>(v.x + ridge, (T)0);
+    A[i * LD + j] = v;
+  }
+  __syncthreads();
+  for (int j = 0; j < K; ++j) {
+    T d = A[j * LD + j].x;
+    if (!(d > (T)0)) {
+      if (tid == 0) atomicCAS(info, 0, p + 1);
+      d = (T)NAN;
+    }
+    const T ljj = sqrt(d), inv = (T)1 / ljj;
+    for (int i = j + 1 + tid; i < K; i += nt) A[i * LD + j] = cscale(A[i * LD + j], inv);
+    __syncthreads();
+    if (tid == 0) A[j * LD + j] = mkc<C>(ljj, (T)0);
+    // trailing triangle: thread -> column k, rows i >= k; A[i][j] is a broadcast read and row i's
+    // columns are contiguous across threads; the i loop carries no dependence (unrolled)
+    for (int k = j + 1 + tid; k < K; k += nt) {
+      const C lk = A[k * LD + j];
+#pragma unroll 4
+      for (int i = k; i < K; ++i) {
+        const C lij = A[i * LD + j];
+        C& t = A[i * LD + k];
+        t.x -= lij.x * lk.x + lij.y * lk.y;  // lij conj(lk)
+        t.y -= lij.y * lk.x - lij.x * lk.y;
+      }
+    }
+    __syncthreads();
+  }
+  C* L = Lall + (int64_t)p * K * K;
+  for (int i = 0; i < K; ++i)
+    for (int j = tid; j <= i; j += nt) L[(int64_t)i * K + j] = A[i * LD + j];
+}
+
+// conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)), one CTA per frequency, blocked by 32:
+// forward  y_b = L_bb^-1 (rhs_b - L_b,<b y_<b)     (GEMV by all warps, 32-step solve by warp 0)
+// backward x_b = L_bb^-H (y_b - L_>b,b^H x_>b)     (column GEMV by all warps, 32-step solve)
 template <typename Tc, typename Th>
 __global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __restrict__ Lall,
                                                        const cx<Th>* __restrict__ c, Th ridge,
@@ -160,51 +256,93 @@ __global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __re
   using C = cx<Th>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* y = reinterpret_cast<C*>(smem_raw);  // [K]
-  C* part = y + K;                        // [nt]
+  C* red = y + K;                         // [8][32] warp partials
   const int p = blockIdx.x;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const C* L = Lall + (int64_t)p * K * K;
-  for (int k = tid; k < K; k += nt) {
+  for (int k = tid; k < K; k += 256) {
     const int64_t o = (int64_t)k * sk + (int64_t)p * sp;
     const C v = csub(ccast<Th>(Vh[o]), ccast<Th>(Th_[o]));
     const C ck = c[(int64_t)p * K + k];
     y[k] = mkc<C>(ck.x + ridge * v.x, ck.y - ridge * v.y);
   }
   __syncthreads();
-  // forward: L y = b, row by row; each warp handles rows, lanes split the dot product
-  for (int i = 0; i < K; ++i) {
-    if (warp == 0) {
-      C acc = mkc<C>(0, 0);
-      const C* row = L + (int64_t)i * K;
-      for (int k = lane; k < i; k += 32) cfma(acc, row[k], y[k]);
+  const int nb = K / CT;
+  // ---- forward ----
+  for (int b = 0; b < nb; ++b) {
+    const int r0 = b * CT;
+    if (b > 0) {  // y[r0 + i] -= sum_{k < r0} L[r0+i][k] y[k]; warp w takes rows w, w+8, ...
+      for (int i = warp; i < CT; i += 8) {
+        const C* row = L + (int64_t)(r0 + i) * K;
+        C acc = mkc<C>(0, 0);
+        for (int k = lane; k < r0; k += 32) cfma(acc, row[k], y[k]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        for (int o = 16; o > 0; o >>= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        }
+        if (lane == 0) y[r0 + i] = csub(y[r0 + i], acc);
       }
-      if (lane == 0) y[i] = cscale(csub(y[i], acc), (Th)1 / row[i].x);
+      __syncthreads();
     }
-    __syncwarp();
-  }
-  __syncthreads();
-  // backward: L^H x = y, column-oriented: x_i = y_i / L_ii; y_k -= conj(L_ik) x_i for k < i
-  for (int i = K - 1; i >= 0; --i) {
-    const C* row = L + (int64_t)i * K;
-    const C xi = cscale(y[i], (Th)1 / row[i].x);
-    __syncthreads();
-    for (int k = tid; k < i; k += nt) {
-      const C l = row[k];
-      C& t = y[k];
-      t.x -= l.x * xi.x + l.y * xi.y;  // conj(l) x
-      t.y -= l.x * xi.y - l.y * xi.x;
+    if (warp == 0) {  // L_bb y = rhs: lane i holds row i of the block
+      C li[CT];
+      const C* row = L + (int64_t)(r0 + lane) * K + r0;
+#pragma unroll
+      for (int k = 0; k < CT; ++k) li[k] = k <= lane ? row[k] : mkc<C>(0, 0);
+      C yi = y[r0 + lane];
+      static_for<0, CT>([&](auto J) {
+        constexpr int j = decltype(J)::value;
+        if (lane == j) yi = cscale(yi, (Th)1 / li[j].x);
+        const Th yx = __shfl_sync(0xffffffffu, yi.x, j), yy = __shfl_sync(0xffffffffu, yi.y, j);
+        if (lane > j) {  // yi -= L[i][j] y_j
+          yi.x -= li[j].x * yx - li[j].y * yy;
+          yi.y -= li[j].x * yy + li[j].y * yx;
+        }
+      });
+      y[r0 + lane] = yi;
     }
-    if (tid == 0) y[i] = xi;
     __syncthreads();
   }
-  (void)part;
-  (void)nw;
-  for (int j = tid; j < K; j += nt)
+  // ---- backward ----
+  for (int b = nb - 1; b >= 0; --b) {
+    const int c0 = b * CT;
+    if (b < nb - 1) {  // y[c0 + lane] -= sum_{r >= c0+CT} conj(L[r][c0+lane]) x[r]; warps split r
+      C acc = mkc<C>(0, 0);
+      for (int r = c0 + CT + warp; r < K; r += 8) {
+        const C l = L[(int64_t)r * K + c0 + lane], xr = y[r];
+        acc.x += l.x * xr.x + l.y * xr.y;
+        acc.y += l.x * xr.y - l.y * xr.x;
+      }
+      red[warp * 32 + lane] = acc;
+      __syncthreads();
+      if (warp == 0) {
+        C s = red[lane];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) s = cadd(s, red[w * 32 + lane]);
+        y[c0 + lane] = csub(y[c0 + lane], s);
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {  // L_bb^H x = y: lane k holds column k of L_bb (rows >= k), i.e. L[i][k]
+      C lc[CT];
+#pragma unroll
+      for (int i = 0; i < CT; ++i) lc[i] = i >= lane ? L[(int64_t)(c0 + i) * K + c0 + lane] : mkc<C>(0, 0);
+      C xk = y[c0 + lane];
+      static_for<0, CT>([&](auto Jr) {
+        constexpr int i = CT - 1 - decltype(Jr)::value;
+        if (lane == i) xk = cscale(xk, (Th)1 / lc[i].x);
+        const Th xx = __shfl_sync(0xffffffffu, xk.x, i), xy = __shfl_sync(0xffffffffu, xk.y, i);
+        if (lane < i) {  // x_k -= conj(L[i][k]) x_i
+          xk.x -= lc[i].x * xx + lc[i].y * xy;
+          xk.y -= lc[i].x * xy - lc[i].y * xx;
+        }
+      });
+      y[c0 + lane] = xk;
+    }
+    __syncthreads();
+  }
+  for (int j = tid; j < K; j += 256)
     Dh[(int64_t)j * sk + (int64_t)p * sp] = mkc<cx<Tc>>((Tc)y[j].x, (Tc)-y[j].y);
 }
 
@@ -225,7 +363,24 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
   if (nfreq == 0) return OCSC_OK;
   const int nb = K / CT;
   const size_t cs = dtype_hist == OCSC_F64 ? 16 : 8;
-  const size_t smem = cs * (size_t)CT * (CT + 1) * (size_t)nb;  // diagonal + up to nb-1 panel tiles
+  const size_t whole = cs * (size_t)K * (K + 1);
+  if (K <= 64) {  // small K: the whole matrix in one CTA's shared memory, many CTAs per SM
+    const int threads = 64;
+    if (dtype_hist == OCSC_F32) {
+      OCSC_CUDA(cudaFuncSetAttribute(k_chol_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)whole));
+      k_chol_smem<float><<<nfreq, threads, whole, s>>>(K, (const float2*)S, (float)ridge, (float2*)L, info);
+    } else if (dtype_hist == OCSC_F64) {
+      OCSC_CUDA(cudaFuncSetAttribute(k_chol_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)whole));
+      k_chol_smem<double><<<nfreq, threads, whole, s>>>(K, (const double2*)S, ridge, (double2*)L, info);
+    } else {
+      return fail(OCSC_EARG, "dtype must be 4 or 8");
+    }
+    OCSC_LAUNCHED("k_chol_smem");
+    return OCSC_OK;
+  }
+  (void)nb;
+  const size_t smem = (dtype_hist == OCSC_F64 ? (size_t)chol_panel_offset<double>() : (size_t)chol_panel_offset<float>()) +
+                      cs * (size_t)CT * (K - CT + 64);  // L_kk + 1/L_jj + panel with slack
   if (smem > 227 * 1024) return fail(OCSC_EARG, "history_factor: panel exceeds shared memory for this K/dtype");
   if (dtype_hist == OCSC_F32) {
     OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -246,6 +401,7 @@ extern "C" int ocsc_dict_rowsolve_chol(int dtype, int dtype_hist, int K, int nfr
   if (K <= 0 || nfreq < 0) return fail(OCSC_ESHAPE, "dict_rowsolve_chol: bad extents");
   if (nfreq == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
+  if (K % CT) return fail(OCSC_EARG, "dict_rowsolve_chol: K must be a multiple of 32");
   const size_t smem = (dtype_hist == OCSC_F64 ? 16 : 8) * ((size_t)K + 256);
 #define RC(TC, TH)                                                                                          \
   k_rowsolve_chol<TC, TH><<<nfreq, 256, smem, s>>>(K, (const cx<TH>*)L, (const cx<TH>*)c, (TH)ridge,        \

@@ -90,6 +90,104 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
   }
 }
 
+// Tiled accumulation for float32 code spectra (the trainer's float32 mode, BASELINE config 4):
+// per frequency, S += Z Z^H is a K x K x B complex GEMM; one CTA computes a 64 x 64 block
+// (I >= J) of the lower triangle, 16 x 16 threads x 4 x 4 complex in registers, samples staged
+// through shared memory 32 at a time.  Each complex multiply-add is two FP32x2 FMAs
+// (acc += zi * zj.x + (zi.y, -zi.x) * zj.y), the form that reaches the FP32 pipe's full rate.
+// The diagonal-block CTAs also accumulate the cross term c for their 64 rows.  Chunk sums of
+// <= 32 samples are added to a float64 history per chunk (as k_hist_accum), to a float32
+// history once at the end.
+constexpr int HT = 64, HCH = 32;
+
+template <typename Th>
+__global__ void __launch_bounds__(256) k_hist_accum_tiled(int K, int B, const float2* __restrict__ z, int64_t z_sb,
+                                                          int64_t z_sk, int64_t z_sp, const float2* __restrict__ x,
+                                                          int64_t x_sb, int64_t x_sp, cx<Th>* S, cx<Th>* c,
+                                                          int pairs) {
+  __shared__ __align__(16) float2 Zi[HCH][HT];
+  __shared__ __align__(16) float2 Zj[HCH][HT];
+  __shared__ float2 Xs[HCH];
+  // all block pairs of one frequency are consecutive CTAs, so its codes are re-read from L2
+  const int p = blockIdx.x / pairs, tp = blockIdx.x - (blockIdx.x / pairs) * pairs;
+  int I = (int)((sqrtf(8.0f * tp + 1.0f) - 1.0f) * 0.5f);
+  while (I * (I + 1) / 2 > tp) --I;
+  while ((I + 1) * (I + 2) / 2 <= tp) ++I;
+  const int J = tp - I * (I + 1) / 2;
+  const bool diag = I == J;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int64_t npk = (int64_t)K * (K + 1) / 2;
+  float2 acc[4][4];
+  float2 cacc = make_float2(0.f, 0.f);
+  auto zero = [&]() {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[r][q] = make_float2(0.f, 0.f);
+  };
+  auto flush = [&]() {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = I * HT + ty * 4 + r;
+      if (i >= K) continue;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = J * HT + tx * 4 + q;
+        if (j > i) continue;
+        cx<Th>& dst = S[(int64_t)p * npk + packed_index(i, j)];
+        dst = mkc<cx<Th>>(dst.x + (Th)acc[r][q].x, dst.y + (Th)acc[r][q].y);
+      }
+    }
+    if (diag && tid < HT && I * HT + tid < K) {
+      cx<Th>& dst = c[(int64_t)p * K + I * HT + tid];
+      dst = mkc<cx<Th>>(dst.x + (Th)cacc.x, dst.y + (Th)cacc.y);
+    }
+  };
+  zero();
+  for (int b0 = 0; b0 < B; b0 += HCH) {
+    const int bc = min(HCH, B - b0);
+    for (int e = tid; e < HCH * HT; e += 256) {
+      const int bb = e / HT, k = e % HT;
+      const int ki = I * HT + k, kj = J * HT + k;
+      const int64_t base = (int64_t)(b0 + bb) * z_sb + (int64_t)p * z_sp;
+      Zi[bb][k] = (bb < bc && ki < K) ? z[base + (int64_t)ki * z_sk] : make_float2(0.f, 0.f);
+      if (!diag) Zj[bb][k] = (bb < bc && kj < K) ? z[base + (int64_t)kj * z_sk] : make_float2(0.f, 0.f);
+    }
+    if (diag && tid < HCH) Xs[tid] = tid < bc ? x[(int64_t)(b0 + tid) * x_sb + (int64_t)p * x_sp] : make_float2(0.f, 0.f);
+    __syncthreads();
+    const float2(*ZJ)[HT] = diag ? Zi : Zj;
+#pragma unroll 4
+    for (int bb = 0; bb < bc; ++bb) {
+      const float4* ri = reinterpret_cast<const float4*>(&Zi[bb][ty * 4]);
+      const float4* rj = reinterpret_cast<const float4*>(&ZJ[bb][tx * 4]);
+      const float4 i01 = ri[0], i23 = ri[1], j01 = rj[0], j23 = rj[1];
+      const float2 zi[4] = {make_float2(i01.x, i01.y), make_float2(i01.z, i01.w), make_float2(i23.x, i23.y),
+                            make_float2(i23.z, i23.w)};
+      const float2 zj[4] = {make_float2(j01.x, j01.y), make_float2(j01.z, j01.w), make_float2(j23.x, j23.y),
+                            make_float2(j23.z, j23.w)};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float2 zs = make_float2(zi[r].y, -zi[r].x);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[r][q] = vfma(zi[r], make_float2(zj[q].x, zj[q].x), acc[r][q]);
+          acc[r][q] = vfma(zs, make_float2(zj[q].y, zj[q].y), acc[r][q]);
+        }
+      }
+    }
+    if (diag && tid < HT) {
+      for (int bb = 0; bb < bc; ++bb) cfmac(cacc, Xs[bb], Zi[bb][tid]);  // conj(x) z
+    }
+    __syncthreads();
+    if (sizeof(Th) == 8) {  // float64 history: add each chunk's float32 sums
+      flush();
+      zero();
+      cacc = make_float2(0.f, 0.f);
+    }
+  }
+  if (sizeof(Th) == 4) flush();
+}
+
 // -------------------------------------------------------------- inversion --
 // One CTA per frequency: A = S + ridge I expanded to a full K x K Hermitian matrix in shared
 // memory, inverted in place by Gauss-Jordan elimination (A is Hermitian positive definite,
@@ -322,6 +420,23 @@ extern "C" int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int 
   if (K <= 0 || nfreq < 0 || B < 0) return fail(OCSC_ESHAPE, "history_accumulate: bad extents");
   if (nfreq == 0 || B == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
+  if (dtype_in == OCSC_F32 && K >= 48) {
+    const int nb = (K + HT - 1) / HT, pairs = nb * (nb + 1) / 2;
+    const int64_t grid = (int64_t)nfreq * pairs;
+    if (grid > 0x7fffffff) return fail(OCSC_EARG, "history_accumulate: too many blocks");
+    if (dtype_hist == OCSC_F32)
+      k_hist_accum_tiled<float><<<(unsigned)grid, 256, 0, s>>>(K, B, (const float2*)z, z_sb, z_sk, z_sp,
+                                                                (const float2*)x, x_sb, x_sp, (float2*)S, (float2*)c,
+                                                                pairs);
+    else if (dtype_hist == OCSC_F64)
+      k_hist_accum_tiled<double><<<(unsigned)grid, 256, 0, s>>>(K, B, (const float2*)z, z_sb, z_sk, z_sp,
+                                                                 (const float2*)x, x_sb, x_sp, (double2*)S,
+                                                                 (double2*)c, pairs);
+    else
+      return fail(OCSC_EARG, "history_accumulate: unsupported dtype pair");
+    OCSC_LAUNCHED("k_hist_accum_tiled");
+    return OCSC_OK;
+  }
   const size_t cs = csize(dtype_in);
   int BC = (int)((160 * 1024) / (cs * (K + 1)));
   if (BC > 32) BC = 32;
