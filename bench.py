@@ -72,20 +72,26 @@ def make_images(n, start, seed=0):
 
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
+    """nvidia-smi clocks/throttle reasons every 20 ms; `stop()` summarises the samples that
+    arrived inside the marked window(s) (the timed region), so idle samples before/after it
+    do not dilute the median."""
+
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, interval_ms=20):
         self.gpu = gpu_index
-        self.rows = []
+        self.interval = interval_ms
+        self.rows = []      # (host time, fields)
+        self.windows = []   # (t0, t1) host times of timed regions
         self.proc = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.interval)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
@@ -93,8 +99,11 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            if len(parts) == 7:
+                self.rows.append((time.perf_counter(), parts))
+
+    def mark(self, t0, t1):
+        self.windows.append((t0, t1))
 
     def stop(self):
         if self.proc:
@@ -103,13 +112,23 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-        if not self.rows:
+        inside = [r for t, r in self.rows if any(a <= t <= b for a, b in self.windows)]
+        rows = inside or [r for _, r in self.rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower().startswith("active")})
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [x for x in (num(r[0]) for r in rows) if x is not None]
+        mx = [x for x in (num(r[1]) for r in rows) if x is not None]
+        pw = [x for x in (num(r[6]) for r in rows) if x is not None]
+        reasons = sorted({n for r in rows for n, v in zip(self.NAMES, r[2:6]) if v.lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "in_timed_region": bool(inside),
+                "power_w_median": statistics.median(pw) if pw else None}
 
 
 # --------------------------------------------------------------- CPU legs --
@@ -207,21 +226,22 @@ def run_b200(args, rank, world, local_rank):
     barrier()
     sampler = ClockSampler(local_rank)
     sampler.start()
-    time.sleep(0.4)
+    time.sleep(0.2)
     stream = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.ocsc_kernel_launches()
     torch.cuda.synchronize()
     barrier()
+    t_on = time.perf_counter()
     for i in range(args.steps):
         flush.zero_()
         evs[i][0].record(stream)
         res = trainer.partial_fit(Xd[args.warmup + i])
         evs[i][1].record(stream)
     torch.cuda.synchronize()
+    sampler.mark(t_on, time.perf_counter())
     barrier()
     launches = lib.ocsc_kernel_launches() - launches0
-    clocks = sampler.stop()
     total_ms = sum(a.elapsed_time(b) for a, b in evs)
     total_ms = max_over_ranks(total_ms)
     value = world * B * args.steps / (total_ms / 1e3)
@@ -270,8 +290,6 @@ def run_b200(args, rank, world, local_rank):
     except OSError:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 2 * float(sm_mhz) * 1e6 / 1e12
     traffic = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
@@ -297,8 +315,14 @@ def run_b200(args, rank, world, local_rank):
         t0 = time.perf_counter()
         r2 = trainer2.partial_fit(Xh[args.warmup + i])
         _ = float(r2.objectives.sum())
-        e2e_s += time.perf_counter() - t0
+        t1 = time.perf_counter()
+        sampler.mark(t0, t1)
+        e2e_s += t1 - t0
     barrier()
+    clocks = sampler.stop()
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 2 * float(sm_mhz) * 1e6 / 1e12
+    achieved_tf = B * flops_per_img_iter / (it_ms / 1e3) / 1e12   # TFLOP/s
     e2e_s = max_over_ranks(e2e_s)
     e2e = world * B * args.steps / e2e_s
 
@@ -337,7 +361,8 @@ def run_b200(args, rank, world, local_rank):
                 "roofline_fp32": {"achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
                                   "frac": achieved_tf / fp32_peak,
                                   "flops": "SURVEY 8(d): 2K*2.5*P*log2(P) + 16*Ph*K + 8*P*K per image-iteration",
-                                  "peak_source": "148 SMs x 128 FMA/clk x 2 x median SM clock (nominal, not measured)"},
+                                  "peak_source": "148 SMs x 128 FMA/clk x 2 x median SM clock sampled in the timed "
+                                                 "region (nominal FP32 rate at the clock the kernel ran at)"},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * P * 4,
                         "d2h_bytes_per_step": (2 * B + 4) * 8},
