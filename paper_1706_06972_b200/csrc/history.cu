@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* rowk = reinterpret_cast<C*>(smem_raw);
   C* colk = rowk + K;
+  __shared__ Th piv_s;  // 1 / pivot, computed once by the pivot's owner
   const int p = blockIdx.x;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
   const C* Sp = S + (int64_t)p * npk;
@@ -297,8 +298,14 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
       for (int ii = 0; ii < BI; ++ii)
         if (i0 + ii == k)
 #pragma unroll
-          for (int jj = 0; jj < BJ; ++jj)
+          for (int jj = 0; jj < BJ; ++jj) {
             if (j0 + jj < K) rowk[j0 + jj] = a[ii][jj];
+            if (j0 + jj == k) {  // pivot owner: one reciprocal per step for the whole CTA
+              const Th d = a[ii][jj].x;
+              piv_s = (Th)1 / d;
+              if (!(d > (Th)0)) atomicCAS(info, 0, p + 1);
+            }
+          }
     }
     if (own_col) {
 #pragma unroll
@@ -309,8 +316,7 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
             if (i0 + ii < K) colk[i0 + ii] = a[ii][jj];
     }
     __syncthreads();
-    const Th pinv = (Th)1 / rowk[k].x;
-    if (t == 0 && !(rowk[k].x > (Th)0)) atomicCAS(info, 0, p + 1);
+    const Th pinv = piv_s;
     // generic rank-1 update with row/column k masked out (ci = 0 on row k, rs = 0 on column k)
     C rs[BJ];
 #pragma unroll

@@ -707,3 +707,21 @@ def test_sharded_trainer_two_ranks_matches_single_gpu(exchange):
         assert rel(objs, mine) < 1e-11
         assert rel(filt, ref.final_filters()) < 1e-11
         assert abs(dchg - ref.dict_change) <= 1e-9 * abs(ref.dict_change)
+
+
+def test_train_online_ragged_and_empty_batches():
+    """N not divisible by the mini-batch (ragged last batch, training.py:193-198 order) and an
+    empty corpus (no records, the initial filters), against the oracle in float64."""
+    shape = ob.SignalShape((14, 12), (3, 3))
+    X = O.synth_images(7, (12, 10), (14, 12), 2, filter_dims=(3, 3), seed=4).reshape(7, -1)
+    kw = dict(K=3, beta=0.4, rho_code=1.0, rho_dict=2.0, inner_iters=3, seed=5, code_max_iters=60,
+              code_rel_tol=1e-3, stop_tol=0.0)
+    ref = O.train_online(X, (14, 12), (3, 3), batch_size=3, max_passes=2, **kw)
+    cfg = ob.TrainConfig(n_filters=3, beta=0.4, rho_code=1.0, rho_dict=2.0, inner_iters=3, seed=5,
+                         code_max_iters=60, stop_tol=0.0, max_passes=2, batch_size=3, dtype="float64")
+    rep = ob.train_online(X, shape, cfg)
+    assert [r.index for r in rep.records] == [1, 2]
+    assert np.allclose([r.train_obj for r in rep.records], [o for _, o in ref["records"]], rtol=1e-9, atol=0)
+    assert rel(rep.filters, ref["filters"]) < 1e-9
+    empty = ob.train_online(np.zeros((0, shape.size)), shape, cfg)
+    assert empty.records == [] and np.allclose(empty.filters, ob.init_dictionary(shape, 3, 5))
