@@ -291,8 +291,10 @@ def run_b200(args, rank, world, local_rank):
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     traffic = None
+    pipe = None
     try:
         tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        pipe = tj.get("fused_ncu_set_full") if fused else None
         key = ("fused_bytes_per_batch_iter" if fused else
                f"stream{H}_bytes_per_batch_iter" if streamed else "generic_bytes_per_batch_iter")
         traffic = tj.get(key)
@@ -362,7 +364,9 @@ def run_b200(args, rank, world, local_rank):
                                   "frac": achieved_tf / fp32_peak,
                                   "flops": "SURVEY 8(d): 2K*2.5*P*log2(P) + 16*Ph*K + 8*P*K per image-iteration",
                                   "peak_source": "148 SMs x 128 FMA/clk x 2 x median SM clock sampled in the timed "
-                                                 "region (nominal FP32 rate at the clock the kernel ran at)"},
+                                                 "region (nominal FP32 rate at the clock the kernel ran at)",
+                                  "ncu_fma_pipe_active_pct": pipe and pipe.get("sm__pipe_fma_cycles_active_pct_of_peak_active"),
+                                  "ncu_source": pipe and pipe.get("source")},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * P * 4,
                         "d2h_bytes_per_step": (2 * B + 4) * 8},
