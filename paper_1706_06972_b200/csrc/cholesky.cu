@@ -56,9 +56,11 @@ __device__ __forceinline__ void cmac_conj2(C& acc, C a, C as, decltype(C::x) bx,
 //   trailing:      A22 -= P P^H over the lower triangle as 64 x 64 block pairs, 16 x 16 threads
 //                  x 4 x 4 complex, two 2-wide FMAs per complex multiply-add (HERK microkernel);
 //                  target values are loaded before the products so their latency overlaps them.
-template <typename T>
-__global__ void __launch_bounds__(256) k_chol_blocked(int K, const cx<T>* __restrict__ S, T ridge, cx<T>* Lall,
-                                                      int32_t* info) {
+// NT = 256 (8 warps; two CTAs per SM where shared memory allows) or 512 (16 warps, two 64 x 64
+// block pairs of the trailing update at a time: K = 512, where one CTA fills the SM anyway)
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT) k_chol_blocked(int K, const cx<T>* __restrict__ S, T ridge, cx<T>* Lall,
+                                                          int32_t* info) {
   using C = cx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LD = CT + 1;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(256) k_chol_blocked(int K, const cx<T>* __rest
   const int PR = K - CT + 64;  // panel row stride: K - CT rows + slack for the last 64-block
 
   // expand the packed lower triangle (+ ridge) into the lower half of the full layout
-  for (int i = warp; i < K; i += 8) {
+  for (int i = warp; i < K; i += NT / 32) {
     const C* src = Sp + packed_index(i, 0);
     C* dst = L + (int64_t)i * K;
     for (int j = lane; j <= i; j += 32) {
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(256) k_chol_blocked(int K, const cx<T>* __rest
     __syncthreads();
     if (R == 0) break;
     // ---- panel: x L_kk^H = a for every trailing row (thread per row) ----
-    for (int rr = tid; rr < R; rr += 256) {
+    for (int rr = tid; rr < R; rr += NT) {
       C x[CT];
       C* row = L + (int64_t)(r0 + rr) * K + kb * CT;
 #pragma unroll
@@ -149,8 +151,8 @@ __global__ void __launch_bounds__(256) k_chol_blocked(int K, const cx<T>* __rest
     __syncthreads();
     // ---- trailing update A22 -= P P^H, 64 x 64 block pairs (bi >= bj) ----
     const int nb64 = (R + 63) / 64;
-    const int ty = tid >> 4, tx = tid & 15;
-    for (int pr = 0; pr < nb64 * (nb64 + 1) / 2; ++pr) {
+    const int half = tid >> 8, ty = (tid & 255) >> 4, tx = tid & 15;
+    for (int pr = half; pr < nb64 * (nb64 + 1) / 2; pr += NT / 256) {
       int bi = (int)((sqrtf(8.0f * pr + 1.0f) - 1.0f) * 0.5f);
       while (bi * (bi + 1) / 2 > pr) --bi;
       while ((bi + 1) * (bi + 2) / 2 <= pr) ++bi;
@@ -382,12 +384,15 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
   const size_t smem = (dtype_hist == OCSC_F64 ? (size_t)chol_panel_offset<double>() : (size_t)chol_panel_offset<float>()) +
                       cs * (size_t)CT * (K - CT + 64);  // L_kk + 1/L_jj + panel with slack
   if (smem > 227 * 1024) return fail(OCSC_EARG, "history_factor: panel exceeds shared memory for this K/dtype");
-  if (dtype_hist == OCSC_F32) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<float><<<nfreq, 256, smem, s>>>(K, (const float2*)S, (float)ridge, (float2*)L, info);
+  if (dtype_hist == OCSC_F32 && K >= 384) {
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_chol_blocked<float, 512><<<nfreq, 512, smem, s>>>(K, (const float2*)S, (float)ridge, (float2*)L, info);
+  } else if (dtype_hist == OCSC_F32) {
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_chol_blocked<float, 256><<<nfreq, 256, smem, s>>>(K, (const float2*)S, (float)ridge, (float2*)L, info);
   } else if (dtype_hist == OCSC_F64) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<double><<<nfreq, 256, smem, s>>>(K, (const double2*)S, ridge, (double2*)L, info);
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<double, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_chol_blocked<double, 256><<<nfreq, 256, smem, s>>>(K, (const double2*)S, ridge, (double2*)L, info);
   } else {
     return fail(OCSC_EARG, "dtype must be 4 or 8");
   }
