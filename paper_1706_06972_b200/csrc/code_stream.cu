@@ -71,7 +71,7 @@ __device__ __forceinline__ T shrink(T a, T kappa) {
 }
 template <typename T>
 __device__ __forceinline__ T clip(T a, T kappa) {
-  return a > kappa ? kappa : (a < -kappa ? -kappa : a);
+  return fmin(fmax(a, -kappa), kappa);  // a NaN w gives a finite clip; S(w) = w - clip(w) stays NaN
 }
 
 struct Flags {
@@ -212,37 +212,36 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   __syncthreads();
   row_stage2<C, G, true>(SA, nr, tid);
   // 4. update: c = (Re z[n], Im z[n]) = (c[2n], c[2n+1]); w' = S(w) + c/P; norms; t' packed into SA
-  T sl[4] = {0, 0, 0, 0};  // per-thread partial norms in T; double from the block reduction on
+  // (x, y) pairs run as 2-wide arithmetic; Gamma = clip(w) by min/max, U = w - Gamma
+  C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};  // per-thread partial norms
   bool nonfinite = false;
   if (!a.first) {
     cp_async_wait<0>();
     __syncthreads();
   }
+  const C ip2 = mkc<C>(a.invP, a.invP);
   for (int e = tid; e < nr * NR; e += G::NTR) {
     const int i = e / NR, n = e - i * NR;
     const C z = SA[i * PR + n];
     C* wp = reinterpret_cast<C*>(w + (int64_t)i * W) + n;
     const C wo = a.first ? mkc<C>(0, 0) : WB[e];
-    T uo[2] = {shrink(wo.x, a.kappa), shrink(wo.y, a.kappa)};
-    T go[2] = {wo.x - uo[0], wo.y - uo[1]};
-    T wn[2] = {uo[0] + z.x * a.invP, uo[1] + z.y * a.invP};
-    T tn[2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const T un = shrink(wn[j], a.kappa), gn = wn[j] - un;
-      const T d0 = un - uo[j], d2 = gn - go[j];
-      sl[0] = fma(d0, d0, sl[0]);
-      sl[1] = fma(un, un, sl[1]);
-      sl[2] = fma(d2, d2, sl[2]);
-      sl[3] = fma(gn, gn, sl[3]);
-      tn[j] = un - gn;
-    }
-    nonfinite |= !isfinite(wn[0]) || !isfinite(wn[1]);
-    *wp = mkc<C>(wn[0], wn[1]);
-    SA[i * PR + n] = mkc<C>(tn[0], tn[1]);
+    const C go = mkc<C>(clip(wo.x, a.kappa), clip(wo.y, a.kappa));
+    const C uo = vsub(wo, go);
+    const C wn = vfma(z, ip2, uo);
+    const C gn = mkc<C>(clip(wn.x, a.kappa), clip(wn.y, a.kappa));
+    const C un = vsub(wn, gn);  // S(w') (NaN propagates through w')
+    const C d0 = vsub(un, uo), d2 = vsub(gn, go);
+    sl[0] = vfma(d0, d0, sl[0]);
+    sl[1] = vfma(un, un, sl[1]);
+    sl[2] = vfma(d2, d2, sl[2]);
+    sl[3] = vfma(gn, gn, sl[3]);
+    nonfinite |= !isfinite(wn.x) || !isfinite(wn.y);
+    *wp = wn;
+    SA[i * PR + n] = vsub(un, gn);
   }
   if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(a.bad + b, 1);
-  double s[4] = {(double)sl[0], (double)sl[1], (double)sl[2], (double)sl[3]};
+  double s[4] = {(double)sl[0].x + sl[0].y, (double)sl[1].x + sl[1].y, (double)sl[2].x + sl[2].y,
+                 (double)sl[3].x + sl[3].y};
   block_sum<4>(s, scratch);  // (contains __syncthreads)
   if (tid == 0) {
 #pragma unroll
