@@ -51,9 +51,10 @@ TRAIN_CFGS = {
         "BASELINE config 2: seeded synthetic 100x100 images (no padding), K=100 filters 11x11, beta=1, rho=1, "
         "J=10, <=300 code iterations, float32 (history float64), mini-batch 10 per GPU"),
     3: (dict(dims0=(256, 256), grid=(266, 266), fdims=(11, 11), K0=64, K=256, beta=0.5, rho_code=1.0,
-             rho_dict=1.0, J=10, max_iters=300, rel_tol=1e-3, B=32),
+             rho_dict=1.0, J=10, max_iters=300, rel_tol=1e-3, B=32, history="float32"),
         "BASELINE config 3: seeded synthetic 256x256 images zero-padded to 266x266, K=256 filters 11x11, "
-        "beta=0.5, rho=1, J=10, <=300 code iterations, float32 (history float64), mini-batch 32 per GPU"),
+        "beta=0.5, rho=1, J=10, <=300 code iterations, float32 with the complex64 history BASELINE sizes "
+        "(9.4 GB packed half spectrum), mini-batch 32 per GPU"),
 }
 
 
@@ -195,7 +196,8 @@ def run_b200(args, rank, world, local_rank):
     shape = ob.SignalShape(CFG["grid"], CFG["fdims"])
     cfg = ob.TrainConfig(n_filters=CFG["K"], beta=CFG["beta"], rho_code=CFG["rho_code"], rho_dict=CFG["rho_dict"],
                          inner_iters=CFG["J"], seed=0, code_max_iters=CFG["max_iters"], code_rel_tol=CFG["rel_tol"],
-                         dtype="float32", history_dtype="float64", batch_size=B, stop_tol=0.0, poll=16)
+                         dtype="float32", history_dtype=CFG.get("history", "float64"), batch_size=B, stop_tol=0.0,
+                         poll=16)
     # N > 1: samples AND spectrum rows sharded (sharded.py: all_to_all of code spectra, one K x M
     # all-reduce per dictionary round); N = 1: the plain trainer
     Trainer = (lambda: ShardedTrainer(shape, cfg, DistComm())) if world > 1 else (lambda: ob.OnlineTrainer(shape, cfg))

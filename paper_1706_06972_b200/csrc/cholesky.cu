@@ -247,20 +247,25 @@ __global__ void __launch_bounds__(128) k_chol_smem(int K, const cx<T>* __restric
     for (int j = tid; j <= i; j += nt) L[(int64_t)i * K + j] = A[i * LD + j];
 }
 
-// conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)), one CTA per frequency, blocked by 32:
-// forward  y_b = L_bb^-1 (rhs_b - L_b,<b y_<b)     (GEMV by all warps, 32-step solve by warp 0)
-// backward x_b = L_bb^-H (y_b - L_>b,b^H x_>b)     (column GEMV by all warps, 32-step solve)
+// conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)), one CTA (256 threads) per frequency,
+// blocked by 32.  Forward: y_b -= L_b,<b y_<b as a tile GEMV (thread = row r, 4 columns of every
+// tile to the left; all its tile loads issue back to back, 8 threads per row reduce by
+// shuffles), then L_bb y_b = rhs_b by warp 0 from a shared-memory copy of the tile.  Backward:
+// y_b -= L_>b,b^H x_>b as the transposed tile GEMV (column sums through shared memory), then
+// L_bb^H x_b = y_b by warp 0.  Every element of L is read once per direction.
 template <typename Tc, typename Th>
 __global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __restrict__ Lall,
                                                        const cx<Th>* __restrict__ c, Th ridge,
                                                        const cx<Tc>* __restrict__ Vh, const cx<Tc>* __restrict__ Th_,
                                                        int64_t sk, int64_t sp, cx<Tc>* Dh) {
   using C = cx<Th>;
+  constexpr int LD = CT + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* y = reinterpret_cast<C*>(smem_raw);  // [K]
-  C* red = y + K;                         // [8][32] warp partials
+  C* Ld = y + K;                          // [CT][LD] diagonal tile / column-sum staging
   const int p = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tr = tid >> 3, tq = (tid & 7) * 4;  // tile row, first of 4 tile columns
   const C* L = Lall + (int64_t)p * K * K;
   for (int k = tid; k < K; k += 256) {
     const int64_t o = (int64_t)k * sk + (int64_t)p * sp;
@@ -270,74 +275,84 @@ __global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __re
   }
   __syncthreads();
   const int nb = K / CT;
-  // ---- forward ----
+  // ---- forward: L y = rhs ----
   for (int b = 0; b < nb; ++b) {
     const int r0 = b * CT;
-    if (b > 0) {  // y[r0 + i] -= sum_{k < r0} L[r0+i][k] y[k]; warp w takes rows w, w+8, ...
-      for (int i = warp; i < CT; i += 8) {
-        const C* row = L + (int64_t)(r0 + i) * K;
-        C acc = mkc<C>(0, 0);
-        for (int k = lane; k < r0; k += 32) cfma(acc, row[k], y[k]);
+    const C* lrow = L + (int64_t)(r0 + tr) * K + tq;
+    C acc = mkc<C>(0, 0);
+#pragma unroll 4
+    for (int m = 0; m < b; ++m) {
+      const C* t = lrow + m * CT;
+      const C* ym = y + m * CT + tq;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-        }
-        if (lane == 0) y[r0 + i] = csub(y[r0 + i], acc);
-      }
-      __syncthreads();
+      for (int q = 0; q < 4; ++q) cfma(acc, t[q], ym[q]);
     }
-    if (warp == 0) {  // L_bb y = rhs: lane i holds row i of the block
-      C li[CT];
-      const C* row = L + (int64_t)(r0 + lane) * K + r0;
 #pragma unroll
-      for (int k = 0; k < CT; ++k) li[k] = k <= lane ? row[k] : mkc<C>(0, 0);
+    for (int o = 1; o < 8; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    const C* dt = lrow + r0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Ld[tr * LD + tq + q] = dt[q];
+    if ((tid & 7) == 0) y[r0 + tr] = csub(y[r0 + tr], acc);
+    __syncthreads();
+    if (warp == 0) {  // lane i: row i of the tile
       C yi = y[r0 + lane];
       static_for<0, CT>([&](auto J) {
         constexpr int j = decltype(J)::value;
-        if (lane == j) yi = cscale(yi, (Th)1 / li[j].x);
+        if (lane == j) yi = cscale(yi, (Th)1 / Ld[j * LD + j].x);
         const Th yx = __shfl_sync(0xffffffffu, yi.x, j), yy = __shfl_sync(0xffffffffu, yi.y, j);
         if (lane > j) {  // yi -= L[i][j] y_j
-          yi.x -= li[j].x * yx - li[j].y * yy;
-          yi.y -= li[j].x * yy + li[j].y * yx;
+          const C l = Ld[lane * LD + j];
+          yi.x -= l.x * yx - l.y * yy;
+          yi.y -= l.x * yy + l.y * yx;
         }
       });
       y[r0 + lane] = yi;
     }
     __syncthreads();
   }
-  // ---- backward ----
+  // ---- backward: L^H x = y ----
   for (int b = nb - 1; b >= 0; --b) {
     const int c0 = b * CT;
-    if (b < nb - 1) {  // y[c0 + lane] -= sum_{r >= c0+CT} conj(L[r][c0+lane]) x[r]; warps split r
-      C acc = mkc<C>(0, 0);
-      for (int r = c0 + CT + warp; r < K; r += 8) {
-        const C l = L[(int64_t)r * K + c0 + lane], xr = y[r];
-        acc.x += l.x * xr.x + l.y * xr.y;
-        acc.y += l.x * xr.y - l.y * xr.x;
-      }
-      red[warp * 32 + lane] = acc;
-      __syncthreads();
-      if (warp == 0) {
-        C s = red[lane];
+    C acc[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};
+#pragma unroll 4
+    for (int m = b + 1; m < nb; ++m) {  // acc[q] += conj(L[m*CT+tr][c0+tq+q]) x[m*CT+tr]
+      const C* t = L + (int64_t)(m * CT + tr) * K + c0 + tq;
+      const C xr = y[m * CT + tr];
 #pragma unroll
-        for (int w = 1; w < 8; ++w) s = cadd(s, red[w * 32 + lane]);
-        y[c0 + lane] = csub(y[c0 + lane], s);
+      for (int q = 0; q < 4; ++q) {
+        const C l = t[q];
+        acc[q].x += l.x * xr.x + l.y * xr.y;
+        acc[q].y += l.x * xr.y - l.y * xr.x;
       }
-      __syncthreads();
     }
-    if (warp == 0) {  // L_bb^H x = y: lane k holds column k of L_bb (rows >= k), i.e. L[i][k]
-      C lc[CT];
 #pragma unroll
-      for (int i = 0; i < CT; ++i) lc[i] = i >= lane ? L[(int64_t)(c0 + i) * K + c0 + lane] : mkc<C>(0, 0);
+    for (int q = 0; q < 4; ++q) Ld[tr * LD + tq + q] = acc[q];
+    __syncthreads();
+    if (warp == 0) {
+      C s = mkc<C>(0, 0);
+      for (int r = 0; r < CT; ++r) s = cadd(s, Ld[r * LD + lane]);
+      y[c0 + lane] = csub(y[c0 + lane], s);
+    }
+    __syncthreads();
+    {  // the diagonal tile, for the warp solve
+      const C* dt = L + (int64_t)(c0 + tr) * K + c0 + tq;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Ld[tr * LD + tq + q] = dt[q];
+    }
+    __syncthreads();
+    if (warp == 0) {  // lane k: x_k; L_bb^H x = y, rows from the bottom
       C xk = y[c0 + lane];
       static_for<0, CT>([&](auto Jr) {
         constexpr int i = CT - 1 - decltype(Jr)::value;
-        if (lane == i) xk = cscale(xk, (Th)1 / lc[i].x);
+        if (lane == i) xk = cscale(xk, (Th)1 / Ld[i * LD + i].x);
         const Th xx = __shfl_sync(0xffffffffu, xk.x, i), xy = __shfl_sync(0xffffffffu, xk.y, i);
         if (lane < i) {  // x_k -= conj(L[i][k]) x_i
-          xk.x -= lc[i].x * xx + lc[i].y * xy;
-          xk.y -= lc[i].x * xy - lc[i].y * xx;
+          const C l = Ld[i * LD + lane];
+          xk.x -= l.x * xx + l.y * xy;
+          xk.y -= l.x * xy - l.y * xx;
         }
       });
       y[c0 + lane] = xk;
@@ -407,7 +422,7 @@ extern "C" int ocsc_dict_rowsolve_chol(int dtype, int dtype_hist, int K, int nfr
   if (nfreq == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
   if (K % CT) return fail(OCSC_EARG, "dict_rowsolve_chol: K must be a multiple of 32");
-  const size_t smem = (dtype_hist == OCSC_F64 ? 16 : 8) * ((size_t)K + 256);
+  const size_t smem = (dtype_hist == OCSC_F64 ? 16 : 8) * ((size_t)K + CT * (CT + 1));
 #define RC(TC, TH)                                                                                          \
   k_rowsolve_chol<TC, TH><<<nfreq, 256, smem, s>>>(K, (const cx<TH>*)L, (const cx<TH>*)c, (TH)ridge,        \
                                                    (const cx<TC>*)Vh, (const cx<TC>*)Th, sk, sp, (cx<TC>*)Dh)
