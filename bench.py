@@ -568,6 +568,9 @@ def main():
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local_rank = _env_int("LOCAL_RANK", 0)
+    if os.environ.get("OCSC_BENCH_BACKEND", "nccl") != "nccl":
+        import torch
+        local_rank %= max(torch.cuda.device_count(), 1)
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -575,7 +578,13 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # OCSC_BENCH_BACKEND=gloo is a functional check of the N > 1 code path on a box with fewer
+        # GPUs than ranks (host-staged collectives; never a reported number)
+        backend = os.environ.get("OCSC_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         if args.config == 4:
             run_history_microbench(args, rank, world, local_rank)
