@@ -10,6 +10,8 @@
 // Algebra: ((1/t)S + rho P I)^-1 = t (S + t rho P I)^-1, so the row solve
 // d = (conj(c/t) + rho P (v - theta)) . inv_gram  becomes
 // conj(d) = (S + t rho P I)^-1 (c + t rho P conj(v - theta)).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "transforms.cuh"
 
@@ -99,6 +101,17 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
 // <= 32 samples are added to a float64 history per chunk (as k_hist_accum), to a float32
 // history once at the end.
 constexpr int HT = 64, HCH = 32;
+
+// tensor-core (3xTF32 tcgen05) accumulation, history_tc.cu; OCSC_HIST_TC=0 selects the FP32x2 kernel
+int history_accumulate_tc(int dtype_hist, int K, int nfreq, int B, const void* z, int64_t z_sb, int64_t z_sk,
+                          int64_t z_sp, const void* x, int64_t x_sb, int64_t x_sp, void* S, void* c, cudaStream_t s);
+static bool use_tensor_cores() {
+  static const bool on = [] {
+    const char* e = getenv("OCSC_HIST_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 template <typename Th>
 __global__ void __launch_bounds__(256) k_hist_accum_tiled(int K, int B, const float2* __restrict__ z, int64_t z_sb,
@@ -426,6 +439,8 @@ extern "C" int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int 
   if (K <= 0 || nfreq < 0 || B < 0) return fail(OCSC_ESHAPE, "history_accumulate: bad extents");
   if (nfreq == 0 || B == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
+  if (dtype_in == OCSC_F32 && K >= 96 && use_tensor_cores())
+    return history_accumulate_tc(dtype_hist, K, nfreq, B, z, z_sb, z_sk, z_sp, x, x_sb, x_sp, S, c, s);
   if (dtype_in == OCSC_F32 && K >= 48) {
     const int nb = (K + HT - 1) / HT, pairs = nb * (nb + 1) / 2;
     const int64_t grid = (int64_t)nfreq * pairs;
