@@ -47,11 +47,13 @@ using sfft::modinv;
 template <typename T, int H_, int W_> struct SGeo;
 
 template <typename T> struct SGeo<T, 100, 100> {
+  static constexpr bool PLANE = true;  // a half-spectrum plane fits one CTA: k_plane
   static constexpr int H = 100, W = 100, RA = 2, RB = 25, CA = 4, CB = 25;
   static constexpr int R = 64, NTR = 128;
   static constexpr int L = 17, NTC = 96;
 };
 template <typename T> struct SGeo<T, 266, 266> {
+  static constexpr bool PLANE = false;
   static constexpr int H = 266, W = 266, RA = 7, RB = 19, CA = 14, CB = 19;
   static constexpr int R = 16, NTR = 128;
   static constexpr int L = 8, NTC = 128;
@@ -428,6 +430,189 @@ __global__ void __launch_bounds__(G::NTC) k_cols_i(ColArgs<T, G> a) {
   }
 }
 
+// ------------------------------------------------------------ plane-resident --
+// For grids whose half-spectrum plane fits one CTA's shared memory (100 x 100: 41 KB) the whole
+// iteration of a (sample, filter) plane stays on chip: conj(D_k) g -> column IFFT -> row IFFT ->
+// update of w (row-major, prefetched by cp.async) -> row FFT of t' -> column FFT -> times D_k,
+// summed in registers over the CTA's filter group.  HBM per plane and iteration: w read + write
+// and the group partial (vs six passes over the spectrum for the row/column kernels).
+template <typename T, class G>
+struct PlaneArgs {
+  int K, B, groups, kper;
+  T kappa, invP;
+  T* w;                 // (B, K, H, W) state
+  const cx<T>* Wh;      // (K, H, WH)
+  const cx<T>* g;       // (B, H, WH)
+  cx<T>* part;          // (B, groups, H, WH)
+  const cx<T>* tw;      // (WH,) e^{-2 pi i k / W}
+  double* acc;          // (B, 4)
+  int32_t* bad;
+  Flags fl;
+  int first;
+};
+
+template <typename T, class G>
+constexpr int plane_nt() { return 256; }
+
+template <typename T, class G>
+__global__ void __launch_bounds__(256, 2) k_plane(PlaneArgs<T, G> a) {
+  using C = cx<T>;
+  using D = Derived<G>;
+  constexpr int H = G::H, W = G::W, NR = D::NR, WH = D::WH, PR = D::PR, NF = D::NF, NT = 256;
+  static_assert(H * G::RA <= NT && WH * G::CA <= NT, "stage-2 tasks must fit one pass");
+  extern __shared__ __align__(16) unsigned char smraw[];
+  C* SA = reinterpret_cast<C*>(smraw);  // [H][PR] plane
+  C* WB = SA + H * PR;                  // [H][NR] state plane (pairs)
+  __shared__ double scratch[4 * 32];
+  const int b = blockIdx.y, grp = blockIdx.x;
+  if (*a.fl.all_done || a.fl.done[b]) return;
+  const int tid = threadIdx.x;
+  const int k0 = grp * a.kper, k1 = min(a.K, k0 + a.kper);
+  const C* gb = a.g + (int64_t)b * NF;
+  C* part = a.part + ((int64_t)b * a.groups + grp) * NF;  // this CTA's partial (L2-resident)
+  C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};
+  bool nonfinite = false;
+  const C ip2 = mkc<C>(a.invP, a.invP);
+  for (int k = k0; k < k1; ++k) {
+    C* wpl = reinterpret_cast<C*>(a.w + ((int64_t)b * a.K + k) * H * W);  // H x NR pairs
+    const C* dk = a.Wh + (int64_t)k * NF;
+    if (!a.first) {
+      for (int e = tid; e < H * NR; e += NT) cp_async<sizeof(C)>(WB + e, wpl + e);
+      cp_async_commit();
+    }
+    // (a) inverse input conj(D_k) g
+    for (int f = tid; f < NF; f += NT) {
+      const int u = f / WH, v = f - u * WH;
+      SA[u * PR + v] = cmulc(dk[f], gb[f]);
+    }
+    __syncthreads();
+    // (b) column IFFT (length H along u, WH columns)
+    for (int e = tid; e < G::CB * WH; e += NT) {
+      const int n2 = e / WH, c = e - n2 * WH;
+      stage1<C, G::CA, G::CB, true>(SA + c, PR, n2);
+    }
+    __syncthreads();
+    {
+      const int c = tid % WH, q1 = tid / WH;
+      const bool act = q1 < G::CA;
+      C v[G::CB];
+      if (act) stage2_load<C, G::CA, G::CB, true>(SA + c, PR, q1, v);
+      __syncthreads();
+      if (act) {
+        const OutRow<G::CA, G::CB> o(q1);
+        sfft::static_for<0, G::CB>([&](auto K2) { SA[o.template at<K2.value>() * PR + c] = v[K2.value]; });
+      }
+      __syncthreads();
+    }
+    // (c) Hermitian pre-processing of every row, (d) row IFFT
+    for (int e = tid; e < H * (NR / 2 + 1); e += NT) {
+      const int i = e / (NR / 2 + 1), kk = e - i * (NR / 2 + 1);
+      const int k2 = NR - kk;
+      C* row = SA + i * PR;
+      const C x1 = row[kk], x2 = row[k2];
+      const C t1 = a.tw[kk], t2 = a.tw[k2];
+      const C s1 = mkc<C>(x1.x + x2.x, x1.y - x2.y), d1 = mkc<C>(x1.x - x2.x, x1.y + x2.y);
+      const C r1 = mkc<C>(d1.x * t1.x + d1.y * t1.y, d1.y * t1.x - d1.x * t1.y);
+      const C s2 = mkc<C>(x2.x + x1.x, x2.y - x1.y), d2 = mkc<C>(x2.x - x1.x, x2.y + x1.y);
+      const C r2 = mkc<C>(d2.x * t2.x + d2.y * t2.y, d2.y * t2.x - d2.x * t2.y);
+      row[kk] = mkc<C>(s1.x - r1.y, s1.y + r1.x);
+      if (kk != 0 && k2 != kk) row[k2] = mkc<C>(s2.x - r2.y, s2.y + r2.x);
+    }
+    __syncthreads();
+    for (int e = tid; e < H * G::RB; e += NT) {
+      const int i = e / G::RB, n2 = e - i * G::RB;
+      stage1<C, G::RA, G::RB, true>(SA + i * PR, 1, n2);
+    }
+    __syncthreads();
+    row_stage2<C, G, true>(SA, H, tid);
+    // (e) update w (pairs), norms, t' packed
+    if (!a.first) {
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    for (int e = tid; e < H * NR; e += NT) {
+      const int i = e / NR, n = e - i * NR;
+      const C z = SA[i * PR + n];
+      const C wo = a.first ? mkc<C>(0, 0) : WB[e];
+      const C go = mkc<C>(clip(wo.x, a.kappa), clip(wo.y, a.kappa));
+      const C uo = vsub(wo, go);
+      const C wn = vfma(z, ip2, uo);
+      const C gn = mkc<C>(clip(wn.x, a.kappa), clip(wn.y, a.kappa));
+      const C un = vsub(wn, gn);
+      const C d0 = vsub(un, uo), d2 = vsub(gn, go);
+      sl[0] = vfma(d0, d0, sl[0]);
+      sl[1] = vfma(un, un, sl[1]);
+      sl[2] = vfma(d2, d2, sl[2]);
+      sl[3] = vfma(gn, gn, sl[3]);
+      nonfinite |= !isfinite(wn.x) || !isfinite(wn.y);
+      wpl[e] = wn;
+      SA[i * PR + n] = vsub(un, gn);
+    }
+    __syncthreads();
+    // (f) row FFT of t', (g) post-processing in place (pairs k, NR-k; X[NR] into the pad slot)
+    for (int e = tid; e < H * G::RB; e += NT) {
+      const int i = e / G::RB, n2 = e - i * G::RB;
+      stage1<C, G::RA, G::RB, false>(SA + i * PR, 1, n2);
+    }
+    __syncthreads();
+    row_stage2<C, G, false>(SA, H, tid);
+    for (int e = tid; e < H * (NR / 2 + 1); e += NT) {
+      const int i = e / (NR / 2 + 1), kk = e - i * (NR / 2 + 1);
+      const int k2 = NR - kk;  // kk = 0: k2 = NR -> X[0] and X[NR] from Z[0]
+      C* row = SA + i * PR;
+      const C za = row[kk], zb = row[kk == 0 ? 0 : k2];
+      auto post = [&](C z1, C z2, int kx) {
+        const C s1 = mkc<C>((z1.x + z2.x) * (T)0.5, (z1.y - z2.y) * (T)0.5);
+        const C d1 = mkc<C>((z1.x - z2.x) * (T)0.5, (z1.y + z2.y) * (T)0.5);
+        const C q = mkc<C>(d1.y, -d1.x);
+        const C t = a.tw[kx];
+        return mkc<C>(s1.x + q.x * t.x - q.y * t.y, s1.y + q.x * t.y + q.y * t.x);
+      };
+      const C xa = post(za, zb, kk);  // X[kk] = f(Z[kk], Z[NR-kk])
+      const C xb = post(zb, za, k2);  // X[NR-kk] = f(Z[NR-kk], Z[kk])
+      row[kk] = xa;
+      if (k2 != kk) row[k2] = xb;
+    }
+    __syncthreads();
+    // (h) column FFT
+    for (int e = tid; e < G::CB * WH; e += NT) {
+      const int n2 = e / WH, c = e - n2 * WH;
+      stage1<C, G::CA, G::CB, false>(SA + c, PR, n2);
+    }
+    __syncthreads();
+    {
+      const int c = tid % WH, q1 = tid / WH;
+      const bool act = q1 < G::CA;
+      C v[G::CB];
+      if (act) stage2_load<C, G::CA, G::CB, false>(SA + c, PR, q1, v);
+      __syncthreads();
+      if (act) {
+        const OutRow<G::CA, G::CB> o(q1);
+        sfft::static_for<0, G::CB>([&](auto K2) { SA[o.template at<K2.value>() * PR + c] = v[K2.value]; });
+      }
+      __syncthreads();
+    }
+    // (i) synthesis partial: part[f] += D_k[f] T_k[f] (each thread revisits the same f: no race)
+    for (int f = tid; f < NF; f += NT) {
+      const int u = f / WH, v = f - u * WH;
+      C acc = k == k0 ? mkc<C>(0, 0) : part[f];
+      cfma(acc, dk[f], SA[u * PR + v]);
+      part[f] = acc;
+    }
+    __syncthreads();  // SA / WB are rewritten by the next plane
+  }
+  if (k1 <= k0)  // empty group: contributes zero
+    for (int f = tid; f < NF; f += NT) part[f] = mkc<C>(0, 0);
+  if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(a.bad + b, 1);
+  double sn[4] = {(double)sl[0].x + sl[0].y, (double)sl[1].x + sl[1].y, (double)sl[2].x + sl[2].y,
+                  (double)sl[3].x + sl[3].y};
+  block_sum<4>(sn, scratch);
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) atomicAdd(a.acc + 4 * b + j, sn[j]);
+  }
+}
+
 // final pass: u = S(w) in place
 template <typename T>
 __global__ void k_shrink_inplace(int64_t n, T kappa, T* __restrict__ u) {
@@ -450,6 +635,14 @@ int k_groups(int K, int B, int ncb) {
   int g = ceil_div(4 * 148, (int64_t)B * ncb);
   g = std::max(1, std::min(g, K / 4));
   return g;
+}
+
+int plane_groups(int K, int B) {
+  // two CTAs per SM over the whole batch, at least one filter per CTA
+  int g = ceil_div(2 * 148, (int64_t)B);
+  g = std::max(1, std::min(g, K));
+  const int kper = ceil_div(K, g);
+  return ceil_div(K, kper);
 }
 
 size_t stream_layout(int dtype, int H, int W, int K, int B, int groups, StreamWork* w, char* base) {
@@ -500,7 +693,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   constexpr int H = G::H, W = G::W, WH = D::WH, NF = D::NF;
   const int dtype = sizeof(T) == 4 ? OCSC_F32 : OCSC_F64;
   const int ncb = ceil_div(WH, G::L);
-  const int groups = k_groups(K, B, ncb);
+  const int groups = G::PLANE ? plane_groups(K, B) : k_groups(K, B, ncb);
   const int kper = ceil_div(K, groups);
   StreamWork sw;
   stream_layout(dtype, H, W, K, B, groups, &sw, (char*)work);
@@ -538,9 +731,23 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
     OCSC_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
     OCSC_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   }
+  PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
+                     (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
+  const size_t plane_smem = (size_t)H * (D::PR + D::NR) * sizeof(cx<T>);
+  if constexpr (G::PLANE)
+    OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
   int rc = OCSC_OK, chunk = 0;
   bool stop = false;
   for (int it = 1; it <= max_iters && !stop; ++it) {
+    if constexpr (G::PLANE) {
+      // g from the previous iteration's group partials (none at the cold start: T = 0)
+      k_gsum<T><<<ggrid, 256, 0, s>>>(B, NF, groups, (const cx<T>*)xh, (const T*)den,
+                                      it > 1 ? (const cx<T>*)sw.part : nullptr, (cx<T>*)sw.g, fl);
+      pa.first = it == 1;
+      k_plane<T, G><<<dim3(groups, B), 256, plane_smem, s>>>(pa);
+      k_decide<<<1, 256, 0, s>>>(B, rel_tol, sw.acc, sw.flags, iters, status);
+      count_launches(3);
+    } else {
     if (it > 1) {
       k_cols_f<T, G><<<cgrid, G::NTC, colf_smem, s>>>(ca);  // groups == 1: writes g itself
       count_launches(1);
@@ -558,6 +765,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
     k_rows<T, G><<<rgrid, G::NTR, row_smem, s>>>(ra);
     k_decide<<<1, 256, 0, s>>>(B, rel_tol, sw.acc, sw.flags, iters, status);
     count_launches(3);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { rc = cuda_fail(e, "code_stream launch"); break; }
     if (host && it % poll == 0 && it < max_iters) {
@@ -612,7 +820,7 @@ extern "C" int ocsc_code_stream_supported(int dtype, int H, int W) {
 extern "C" size_t ocsc_code_stream_workspace_bytes(int dtype, int H, int W, int K, int B) {
   const int WH = W / 2 + 1;
   const int L = H == 266 ? SGeo<float, 266, 266>::L : SGeo<float, 100, 100>::L;
-  const int groups = k_groups(K, B, ceil_div(WH, L));
+  const int groups = std::max(k_groups(K, B, ceil_div(WH, L)), plane_groups(K, B));
   const size_t s = dtype == OCSC_F64 ? 16 : 8;
   return stream_layout(dtype, H, W, K, B, groups, nullptr, nullptr) + (size_t)B * K * H * WH * s;
 }
