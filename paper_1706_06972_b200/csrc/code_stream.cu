@@ -47,7 +47,8 @@ using sfft::modinv;
 template <typename T, int H_, int W_> struct SGeo;
 
 template <typename T> struct SGeo<T, 100, 100> {
-  static constexpr bool PLANE = true;  // a half-spectrum plane fits one CTA: k_plane
+  // float: plane + state + partial (122 KB) fit one CTA -> k_plane; double -> row/column kernels
+  static constexpr bool PLANE = sizeof(T) == 4;
   static constexpr int H = 100, W = 100, RA = 2, RB = 25, CA = 4, CB = 25;
   static constexpr int R = 64, NTR = 128;
   static constexpr int L = 17, NTC = 96;
@@ -451,25 +452,25 @@ struct PlaneArgs {
   int first;
 };
 
-template <typename T, class G>
-constexpr int plane_nt() { return 256; }
+constexpr int PLANE_NT = 512;  // one CTA per SM: plane + state + partial in shared memory
 
 template <typename T, class G>
-__global__ void __launch_bounds__(256, 2) k_plane(PlaneArgs<T, G> a) {
+__global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   using C = cx<T>;
   using D = Derived<G>;
-  constexpr int H = G::H, W = G::W, NR = D::NR, WH = D::WH, PR = D::PR, NF = D::NF, NT = 256;
+  constexpr int H = G::H, W = G::W, NR = D::NR, WH = D::WH, PR = D::PR, NF = D::NF, NT = PLANE_NT;
   static_assert(H * G::RA <= NT && WH * G::CA <= NT, "stage-2 tasks must fit one pass");
   extern __shared__ __align__(16) unsigned char smraw[];
   C* SA = reinterpret_cast<C*>(smraw);  // [H][PR] plane
   C* WB = SA + H * PR;                  // [H][NR] state plane (pairs)
+  C* PT = WB + H * NR;                  // [NF] the group's synthesis partial
   __shared__ double scratch[4 * 32];
   const int b = blockIdx.y, grp = blockIdx.x;
   if (*a.fl.all_done || a.fl.done[b]) return;
   const int tid = threadIdx.x;
   const int k0 = grp * a.kper, k1 = min(a.K, k0 + a.kper);
   const C* gb = a.g + (int64_t)b * NF;
-  C* part = a.part + ((int64_t)b * a.groups + grp) * NF;  // this CTA's partial (L2-resident)
+  for (int f = tid; f < NF; f += NT) PT[f] = mkc<C>(0, 0);
   C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};
   bool nonfinite = false;
   const C ip2 = mkc<C>(a.invP, a.invP);
@@ -592,17 +593,16 @@ __global__ void __launch_bounds__(256, 2) k_plane(PlaneArgs<T, G> a) {
       }
       __syncthreads();
     }
-    // (i) synthesis partial: part[f] += D_k[f] T_k[f] (each thread revisits the same f: no race)
+    // (i) synthesis partial: PT[f] += D_k[f] T_k[f] (each thread revisits the same f: no race)
+#pragma unroll 4
     for (int f = tid; f < NF; f += NT) {
       const int u = f / WH, v = f - u * WH;
-      C acc = k == k0 ? mkc<C>(0, 0) : part[f];
-      cfma(acc, dk[f], SA[u * PR + v]);
-      part[f] = acc;
+      cfma(PT[f], dk[f], SA[u * PR + v]);
     }
     __syncthreads();  // SA / WB are rewritten by the next plane
   }
-  if (k1 <= k0)  // empty group: contributes zero
-    for (int f = tid; f < NF; f += NT) part[f] = mkc<C>(0, 0);
+  C* part = a.part + ((int64_t)b * a.groups + grp) * NF;
+  for (int f = tid; f < NF; f += NT) part[f] = PT[f];
   if (__syncthreads_or(nonfinite) && tid == 0) atomicOr(a.bad + b, 1);
   double sn[4] = {(double)sl[0].x + sl[0].y, (double)sl[1].x + sl[1].y, (double)sl[2].x + sl[2].y,
                   (double)sl[3].x + sl[3].y};
@@ -638,8 +638,8 @@ int k_groups(int K, int B, int ncb) {
 }
 
 int plane_groups(int K, int B) {
-  // two CTAs per SM over the whole batch, at least one filter per CTA
-  int g = ceil_div(2 * 148, (int64_t)B);
+  // one CTA per SM over the whole batch (at most one wave), at least one filter per CTA
+  int g = std::max(1, 148 / std::max(B, 1));
   g = std::max(1, std::min(g, K));
   const int kper = ceil_div(K, g);
   return ceil_div(K, kper);
@@ -733,7 +733,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   }
   PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
                      (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
-  const size_t plane_smem = (size_t)H * (D::PR + D::NR) * sizeof(cx<T>);
+  const size_t plane_smem = ((size_t)H * (D::PR + D::NR) + NF) * sizeof(cx<T>);
   if constexpr (G::PLANE)
     OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
   int rc = OCSC_OK, chunk = 0;
@@ -744,7 +744,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
       k_gsum<T><<<ggrid, 256, 0, s>>>(B, NF, groups, (const cx<T>*)xh, (const T*)den,
                                       it > 1 ? (const cx<T>*)sw.part : nullptr, (cx<T>*)sw.g, fl);
       pa.first = it == 1;
-      k_plane<T, G><<<dim3(groups, B), 256, plane_smem, s>>>(pa);
+      k_plane<T, G><<<dim3(groups, B), PLANE_NT, plane_smem, s>>>(pa);
       k_decide<<<1, 256, 0, s>>>(B, rel_tol, sw.acc, sw.flags, iters, status);
       count_launches(3);
     } else {
