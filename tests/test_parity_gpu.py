@@ -725,3 +725,29 @@ def test_train_online_ragged_and_empty_batches():
     assert rel(rep.filters, ref["filters"]) < 1e-9
     empty = ob.train_online(np.zeros((0, shape.size)), shape, cfg)
     assert empty.records == [] and np.allclose(empty.filters, ob.init_dictionary(shape, 3, 5))
+
+
+@pytest.mark.parametrize("K,B,hist", [(128, 40, "complex128"), (256, 13, "complex64"), (100, 50, "complex128")])
+def test_tensor_core_history_accumulation_keeps_float32_accuracy(K, B, hist):
+    """The tcgen05 3xTF32 accumulation (history_tc.cu) against a float64 reference: the split
+    precision must keep float32-level accuracy (the north_star's condition for tensor cores)."""
+    from paper_1706_06972_b200.dictionary import HistoryState
+
+    nf = 37
+    g = torch.Generator(device="cuda").manual_seed(K + B)
+    z = torch.complex(torch.randn(B, nf, K, device="cuda", generator=g),
+                      torch.randn(B, nf, K, device="cuda", generator=g))  # complex64, layout (B, P, K)
+    x = torch.complex(torch.randn(B, nf, device="cuda", generator=g), torch.randn(B, nf, device="cuda", generator=g))
+    cdt = torch.complex128 if hist == "complex128" else torch.complex64
+    h = HistoryState(ob.SignalShape((nf,), (1,)), K, 1.0, nfreq=nf, dtype=cdt)
+    h.accumulate(z, (nf * K, 1, K), x, (nf, 1), B)
+    zz = z.cpu().numpy().astype(np.complex128)
+    xx = x.cpu().numpy().astype(np.complex128)
+    S = np.einsum("bpi,bpj->pij", zz, zz.conj())
+    il, jl = np.tril_indices(K)
+    want = S[:, il, jl]
+    got = h.S.cpu().numpy()
+    tol = 3e-6 if hist == "complex128" else 1e-5
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < tol
+    want_c = np.einsum("bp,bpk->pk", xx.conj(), zz)
+    assert np.linalg.norm(h.c.cpu().numpy() - want_c) / np.linalg.norm(want_c) < tol
