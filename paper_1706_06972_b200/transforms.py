@@ -243,7 +243,9 @@ def crop_filter_cols(padded, shape: SignalShape) -> np.ndarray:
 
 
 def circular_convolve(d, z, shape: SignalShape) -> np.ndarray:
-    """Circular convolution of an (M,) filter with a (P,) signal (transforms.py:137-141)."""
-    df = forward_dft(pad_filter(d, shape), shape)
-    zf = forward_dft(z, shape)
-    return inverse_dft(df * zf, shape)
+    """Circular convolution of an (M,) filter with a (P,) signal (transforms.py:137-141):
+    both spectra, their product and the inverse stay on the device."""
+    pd = _dev(pad_filter(d, shape).reshape(shape.size, 1))
+    zs = _dev(_signal(z, shape).reshape(shape.size, 1))
+    prod = dft_cols_dev(pd, shape) * dft_cols_dev(zs, shape)
+    return _np(inverse_cols_dev(prod, shape)).reshape(shape.size)

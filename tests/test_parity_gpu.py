@@ -751,3 +751,21 @@ def test_tensor_core_history_accumulation_keeps_float32_accuracy(K, B, hist):
     assert np.linalg.norm(got - want) / np.linalg.norm(want) < tol
     want_c = np.einsum("bp,bpk->pk", xx.conj(), zz)
     assert np.linalg.norm(h.c.cpu().numpy() - want_c) / np.linalg.norm(want_c) < tol
+
+
+def test_circular_convolve_matches_direct_sum():
+    """transforms.py:137-141: circular convolution of a filter with a signal (2-D and 1-D)."""
+    rng = np.random.default_rng(3)
+    for dims, fd in [((9, 8), (3, 2)), ((16,), (5,))]:
+        shape = ob.SignalShape(dims, fd)
+        H, W = shape.grid
+        M0, M1 = shape.support
+        d = rng.normal(size=shape.filter_size)
+        z = rng.normal(size=shape.size)
+        got = ob.circular_convolve(d, z, shape).reshape(H, W)
+        dd, zz = d.reshape(M0, M1), z.reshape(H, W)
+        want = np.zeros((H, W))
+        for a in range(M0):
+            for b in range(M1):
+                want += dd[a, b] * np.roll(np.roll(zz, a, axis=0), b, axis=1)
+        assert np.abs(got - want).max() < 1e-12 * max(np.abs(want).max(), 1.0)
