@@ -25,6 +25,8 @@
 #include <map>
 #include <tuple>
 
+#include <mutex>
+
 #include "common.cuh"
 #include "fft_small.cuh"
 
@@ -577,7 +579,9 @@ static FusedPlan plan_for(int K, int B) {
 
 template <typename T, int N>
 static const FusedPlan& cached_plan(int K, int B) {
-  static std::map<std::tuple<int, int, int>, FusedPlan> cache;
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, FusedPlan> cache;  // map nodes are stable
+  std::lock_guard<std::mutex> lk(mu);
   int dev = 0;
   cudaGetDevice(&dev);
   auto key = std::make_tuple(dev, K, B);

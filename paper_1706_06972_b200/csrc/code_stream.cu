@@ -661,11 +661,14 @@ size_t stream_layout(int dtype, int H, int W, int K, int B, int groups, StreamWo
 }
 
 template <typename T>
-const cx<T>* twiddles(int W) {
+const cx<T>* twiddles(int W) {  // per (device, W) table of e^{-2 pi i k / W}, k <= W/2
   static std::mutex mu;
-  static std::map<int, void*> cache;
+  static std::map<std::pair<int, int>, void*> cache;
   std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(W);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(dev, W);
+  auto it = cache.find(key);
   if (it != cache.end()) return (const cx<T>*)it->second;
   const int n = W / 2 + 1;
   std::vector<cx<T>> h(n);
@@ -676,7 +679,7 @@ const cx<T>* twiddles(int W) {
   void* d = nullptr;
   if (cudaMalloc(&d, n * sizeof(cx<T>)) != cudaSuccess) return nullptr;
   if (cudaMemcpy(d, h.data(), n * sizeof(cx<T>), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  cache[W] = d;
+  cache[key] = d;
   return (const cx<T>*)d;
 }
 
