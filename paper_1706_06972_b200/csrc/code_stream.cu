@@ -179,13 +179,31 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   C* WB = SA + R * PR;
   if (!a.first) {
     const C* wsrc = reinterpret_cast<const C*>(w);
-    for (int e = tid; e < nr * NR; e += G::NTR) cp_async<sizeof(C)>(WB + e, wsrc + e);
+    if constexpr (sizeof(C) == 8) {  // 16-byte copies (two complex)
+      const int n = nr * NR;
+      for (int e = 2 * tid; e < n; e += 2 * G::NTR) {
+        if (e + 1 < n) cp_async<16>(WB + e, wsrc + e);
+        else cp_async<8>(WB + e, wsrc + e);
+      }
+    } else {
+      for (int e = tid; e < nr * NR; e += G::NTR) cp_async<sizeof(C)>(WB + e, wsrc + e);
+    }
     cp_async_commit();
   }
-  // 1. spectrum rows -> SA
-  for (int e = tid; e < nr * WH; e += G::NTR) {
-    const int i = e / WH, k = e - i * WH;
-    SA[i * PR + k] = spec[(int64_t)i * WH + k];
+  // 1. spectrum rows -> SA (the row pitch equals WH: one contiguous block)
+  if constexpr (PR == WH && sizeof(C) == 8) {
+    const int n = nr * WH;
+    for (int e = 2 * tid; e < n; e += 2 * G::NTR) {
+      if (e + 1 < n) cp_async<16>(SA + e, spec + e);
+      else cp_async<8>(SA + e, spec + e);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  } else {
+    for (int e = tid; e < nr * WH; e += G::NTR) {
+      const int i = e / WH, k = e - i * WH;
+      SA[i * PR + k] = spec[(int64_t)i * WH + k];
+    }
   }
   __syncthreads();
   // 2. Hermitian pre-processing (pairs k, NR-k): Z = (X_k + X*_{NR-k}) + i e^{+i 2pi k/W}(X_k - X*_{NR-k})
@@ -286,9 +304,20 @@ struct ColArgs {
 // async copy of one plane's L-column block (H rows, row stride WH) into a [H][L] tile
 template <typename C, int H, int L, int NT>
 __device__ __forceinline__ void fetch_block(C* dst, const C* src, int WH, int nc, int tid) {
-  for (int e = tid; e < H * L; e += NT) {
-    const int h = e / L, c = e - h * L;
-    if (c < nc) cp_async<sizeof(C)>(dst + h * L + c, src + (int64_t)h * WH + c);
+  if constexpr (sizeof(C) == 8 && L % 2 == 0) {
+    // complex64: 16-byte copies of column pairs (tiles and spectrum rows are 16-byte aligned;
+    // an odd trailing column goes alone)
+    constexpr int L2 = L / 2;
+    for (int e = tid; e < H * L2; e += NT) {
+      const int h = e / L2, c = 2 * (e - h * L2);
+      if (c + 1 < nc) cp_async<16>(dst + h * L + c, src + (int64_t)h * WH + c);
+      else if (c < nc) cp_async<8>(dst + h * L + c, src + (int64_t)h * WH + c);
+    }
+  } else {
+    for (int e = tid; e < H * L; e += NT) {
+      const int h = e / L, c = e - h * L;
+      if (c < nc) cp_async<sizeof(C)>(dst + h * L + c, src + (int64_t)h * WH + c);
+    }
   }
   cp_async_commit();
 }
@@ -478,7 +507,11 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
     C* wpl = reinterpret_cast<C*>(a.w + ((int64_t)b * a.K + k) * H * W);  // H x NR pairs
     const C* dk = a.Wh + (int64_t)k * NF;
     if (!a.first) {
-      for (int e = tid; e < H * NR; e += NT) cp_async<sizeof(C)>(WB + e, wpl + e);
+      if constexpr (sizeof(C) == 8) {  // 16-byte copies (two complex; H * NR is even)
+        for (int e = 2 * tid; e < H * NR; e += 2 * NT) cp_async<16>(WB + e, wpl + e);
+      } else {
+        for (int e = tid; e < H * NR; e += NT) cp_async<sizeof(C)>(WB + e, wpl + e);
+      }
       cp_async_commit();
     }
     // (a) inverse input conj(D_k) g
