@@ -360,6 +360,9 @@ def run_b200(args, rank, world, local_rank):
                 "roofline": {"bound": "hbm",
                              "kernel": ("k_code_fused (cluster per sample, state in SMEM), one ADMM iteration over "
                                         "the mini-batch" if fused else
+                                        "plane-resident streaming code ADMM (k_plane: one CTA per (sample, filter "
+                                        "group), planes in SMEM), one iteration over the mini-batch"
+                                        if streamed and (H, W) == (100, 100) else
                                         "streaming code ADMM (k_rows + k_cols_f + k_cols_i), one iteration over the "
                                         "mini-batch" if streamed else "cuFFT code-ADMM iteration over the mini-batch"),
                              "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -47,7 +47,7 @@ using sfft::modinv;
 template <typename T, int H_, int W_> struct SGeo;
 
 template <typename T> struct SGeo<T, 100, 100> {
-  // float: plane + state + partial (122 KB) fit one CTA -> k_plane; double -> row/column kernels
+  // float: two planes + state + partial (164 KB) fit one CTA -> k_plane; double -> row/column kernels
   static constexpr bool PLANE = sizeof(T) == 4;
   static constexpr int H = 100, W = 100, RA = 2, RB = 25, CA = 4, CB = 25;
   static constexpr int R = 64, NTR = 128;
@@ -140,6 +140,20 @@ __device__ __forceinline__ void row_stage2(C* SA, int nr, int tid) {
   if (act) {
     const OutRow<G::RA, G::RB> o(k1);
     sfft::static_for<0, G::RB>([&](auto K2) { SA[i * PR + o.template at<K2.value>()] = v[K2.value]; });
+  }
+  __syncthreads();
+}
+
+// stage 2 of the row transform out of place (src -> dst, natural order); ends synced
+template <typename C, class G, bool INV>
+__device__ __forceinline__ void row_stage2_oop(const C* src, C* dst, int nr, int tid) {
+  constexpr int PR = Derived<G>::PR;
+  for (int e = tid; e < nr * G::RA; e += blockDim.x) {
+    const int i = e / G::RA, k1 = e - i * G::RA;
+    C v[G::RB];
+    stage2_load<C, G::RA, G::RB, INV>(src + i * PR, 1, k1, v);
+    const OutRow<G::RA, G::RB> o(k1);
+    sfft::static_for<0, G::RB>([&](auto K2) { dst[i * PR + o.template at<K2.value>()] = v[K2.value]; });
   }
   __syncthreads();
 }
@@ -483,6 +497,11 @@ struct PlaneArgs {
 
 constexpr int PLANE_NT = 512;  // one CTA per SM: plane + state + partial in shared memory
 
+// debug: clock64 stamps of CTA (0, 0) over its first 4 planes (scripts/plane_prof.py)
+__device__ long long* g_plane_prof = nullptr;
+#define PLANE_STAMP(slot) \
+  if (prof && k - k0 < 4) prof[(k - k0) * 16 + (slot)] = clock64();
+
 template <typename T, class G>
 __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   using C = cx<T>;
@@ -491,7 +510,8 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   static_assert(H * G::RA <= NT && WH * G::CA <= NT, "stage-2 tasks must fit one pass");
   extern __shared__ __align__(16) unsigned char smraw[];
   C* SA = reinterpret_cast<C*>(smraw);  // [H][PR] plane
-  C* WB = SA + H * PR;                  // [H][NR] state plane (pairs)
+  C* SB = SA + H * PR;                  // [H][PR] second plane: stage-2 passes run out of place
+  C* WB = SB + H * PR;                  // [H][NR] state plane (pairs)
   C* PT = WB + H * NR;                  // [NF] the group's synthesis partial
   __shared__ double scratch[4 * 32];
   const int b = blockIdx.y, grp = blockIdx.x;
@@ -503,7 +523,9 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};
   bool nonfinite = false;
   const C ip2 = mkc<C>(a.invP, a.invP);
+  long long* prof = (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ? g_plane_prof : nullptr;
   for (int k = k0; k < k1; ++k) {
+    PLANE_STAMP(0)
     C* wpl = reinterpret_cast<C*>(a.w + ((int64_t)b * a.K + k) * H * W);  // H x NR pairs
     const C* dk = a.Wh + (int64_t)k * NF;
     if (!a.first) {
@@ -520,29 +542,30 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
       SA[u * PR + v] = cmulc(dk[f], gb[f]);
     }
     __syncthreads();
+    PLANE_STAMP(1)
     // (b) column IFFT (length H along u, WH columns)
     for (int e = tid; e < G::CB * WH; e += NT) {
       const int n2 = e / WH, c = e - n2 * WH;
       stage1<C, G::CA, G::CB, true>(SA + c, PR, n2);
     }
     __syncthreads();
+    PLANE_STAMP(2)
     {
       const int c = tid % WH, q1 = tid / WH;
-      const bool act = q1 < G::CA;
-      C v[G::CB];
-      if (act) stage2_load<C, G::CA, G::CB, true>(SA + c, PR, q1, v);
-      __syncthreads();
-      if (act) {
+      if (q1 < G::CA) {
+        C v[G::CB];
+        stage2_load<C, G::CA, G::CB, true>(SA + c, PR, q1, v);
         const OutRow<G::CA, G::CB> o(q1);
-        sfft::static_for<0, G::CB>([&](auto K2) { SA[o.template at<K2.value>() * PR + c] = v[K2.value]; });
+        sfft::static_for<0, G::CB>([&](auto K2) { SB[o.template at<K2.value>() * PR + c] = v[K2.value]; });
       }
       __syncthreads();
     }
+    PLANE_STAMP(3)
     // (c) Hermitian pre-processing of every row, (d) row IFFT
     for (int e = tid; e < H * (NR / 2 + 1); e += NT) {
       const int i = e / (NR / 2 + 1), kk = e - i * (NR / 2 + 1);
       const int k2 = NR - kk;
-      C* row = SA + i * PR;
+      C* row = SB + i * PR;
       const C x1 = row[kk], x2 = row[k2];
       const C t1 = a.tw[kk], t2 = a.tw[k2];
       const C s1 = mkc<C>(x1.x + x2.x, x1.y - x2.y), d1 = mkc<C>(x1.x - x2.x, x1.y + x2.y);
@@ -553,17 +576,21 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
       if (kk != 0 && k2 != kk) row[k2] = mkc<C>(s2.x - r2.y, s2.y + r2.x);
     }
     __syncthreads();
+    PLANE_STAMP(4)
     for (int e = tid; e < H * G::RB; e += NT) {
       const int i = e / G::RB, n2 = e - i * G::RB;
-      stage1<C, G::RA, G::RB, true>(SA + i * PR, 1, n2);
+      stage1<C, G::RA, G::RB, true>(SB + i * PR, 1, n2);
     }
     __syncthreads();
-    row_stage2<C, G, true>(SA, H, tid);
+    PLANE_STAMP(5)
+    row_stage2_oop<C, G, true>(SB, SA, H, tid);
+    PLANE_STAMP(6)
     // (e) update w (pairs), norms, t' packed
     if (!a.first) {
       cp_async_wait<0>();
       __syncthreads();
     }
+    PLANE_STAMP(7)
     for (int e = tid; e < H * NR; e += NT) {
       const int i = e / NR, n = e - i * NR;
       const C z = SA[i * PR + n];
@@ -583,17 +610,20 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
       SA[i * PR + n] = vsub(un, gn);
     }
     __syncthreads();
+    PLANE_STAMP(8)
     // (f) row FFT of t', (g) post-processing in place (pairs k, NR-k; X[NR] into the pad slot)
     for (int e = tid; e < H * G::RB; e += NT) {
       const int i = e / G::RB, n2 = e - i * G::RB;
       stage1<C, G::RA, G::RB, false>(SA + i * PR, 1, n2);
     }
     __syncthreads();
-    row_stage2<C, G, false>(SA, H, tid);
+    PLANE_STAMP(9)
+    row_stage2_oop<C, G, false>(SA, SB, H, tid);
+    PLANE_STAMP(10)
     for (int e = tid; e < H * (NR / 2 + 1); e += NT) {
       const int i = e / (NR / 2 + 1), kk = e - i * (NR / 2 + 1);
       const int k2 = NR - kk;  // kk = 0: k2 = NR -> X[0] and X[NR] from Z[0]
-      C* row = SA + i * PR;
+      C* row = SB + i * PR;
       const C za = row[kk], zb = row[kk == 0 ? 0 : k2];
       auto post = [&](C z1, C z2, int kx) {
         const C s1 = mkc<C>((z1.x + z2.x) * (T)0.5, (z1.y - z2.y) * (T)0.5);
@@ -608,24 +638,25 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
       if (k2 != kk) row[k2] = xb;
     }
     __syncthreads();
+    PLANE_STAMP(11)
     // (h) column FFT
     for (int e = tid; e < G::CB * WH; e += NT) {
       const int n2 = e / WH, c = e - n2 * WH;
-      stage1<C, G::CA, G::CB, false>(SA + c, PR, n2);
+      stage1<C, G::CA, G::CB, false>(SB + c, PR, n2);
     }
     __syncthreads();
+    PLANE_STAMP(12)
     {
       const int c = tid % WH, q1 = tid / WH;
-      const bool act = q1 < G::CA;
-      C v[G::CB];
-      if (act) stage2_load<C, G::CA, G::CB, false>(SA + c, PR, q1, v);
-      __syncthreads();
-      if (act) {
+      if (q1 < G::CA) {
+        C v[G::CB];
+        stage2_load<C, G::CA, G::CB, false>(SB + c, PR, q1, v);
         const OutRow<G::CA, G::CB> o(q1);
         sfft::static_for<0, G::CB>([&](auto K2) { SA[o.template at<K2.value>() * PR + c] = v[K2.value]; });
       }
       __syncthreads();
     }
+    PLANE_STAMP(13)
     // (i) synthesis partial: PT[f] += D_k[f] T_k[f] (each thread revisits the same f: no race)
 #pragma unroll 4
     for (int f = tid; f < NF; f += NT) {
@@ -633,6 +664,7 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
       cfma(PT[f], dk[f], SA[u * PR + v]);
     }
     __syncthreads();  // SA / WB are rewritten by the next plane
+    PLANE_STAMP(14)
   }
   C* part = a.part + ((int64_t)b * a.groups + grp) * NF;
   for (int f = tid; f < NF; f += NT) part[f] = PT[f];
@@ -769,7 +801,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   }
   PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
                      (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
-  const size_t plane_smem = ((size_t)H * (D::PR + D::NR) + NF) * sizeof(cx<T>);
+  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + NF) * sizeof(cx<T>);
   if constexpr (G::PLANE)
     OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
   int rc = OCSC_OK, chunk = 0;
@@ -874,4 +906,10 @@ extern "C" int ocsc_code_stream(int dtype, int H, int W, int K, int B, const voi
     return dispatch<double>(H, W, false, K, B, xh, Wh, den, beta, rho, max_iters, rel_tol, u, work, iters, status,
                             poll, s);
   return fail(OCSC_EARG, "dtype must be 4 or 8");
+}
+
+extern "C" int ocsc_debug_plane_profile(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  OCSC_CUDA(cudaMemcpyToSymbol(ocsc::g_plane_prof, &p, sizeof(p)));
+  return OCSC_OK;
 }

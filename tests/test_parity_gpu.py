@@ -556,8 +556,8 @@ def test_preprocessing_reference_properties():
 
 # ---------------------------------------------- streaming FFT code path (cfg 0/2/3) --
 
-@pytest.mark.parametrize("dtype,H,K,B", [("float64", 100, 6, 2), ("float32", 100, 8, 3), ("float32", 266, 4, 2),
-                                         ("float64", 266, 3, 1)])
+@pytest.mark.parametrize("dtype,H,K,B", [("float64", 100, 6, 2), ("float32", 100, 8, 3), ("float32", 100, 40, 12),
+                                         ("float32", 266, 4, 2), ("float64", 266, 3, 1)])
 def test_stream_code_path_matches_cufft_path(dtype, H, K, B):
     from paper_1706_06972_b200.coding import CodeBuffers, infer_codes, infer_codes_stream, stream_supported
     from paper_1706_06972_b200.transforms import rfft2_dev
