@@ -158,6 +158,74 @@ __device__ __forceinline__ void row_stage2_oop(const C* src, C* dst, int nr, int
   __syncthreads();
 }
 
+// Rows with RA = 2 (W = 100): the Hermitian pre-/post-processing that maps a half spectrum to
+// the packed NR-point complex transform pairs bin k with bin NR - k.  Stage-1 task n2 touches
+// bins {2 n2, 2 n2 + RB} and task RB - n2 their partners, so one thread runs both tasks with the
+// pre-processing fused in; every stage-2 task holds both bins of each pair in registers, so the
+// post-processing is fused into its stores.
+template <typename C>
+__device__ __forceinline__ C herm_pre(C x1, C x2, C t) {  // Z[k] from X[k], X[NR-k]
+  const C s = mkc<C>(x1.x + x2.x, x1.y - x2.y), d = mkc<C>(x1.x - x2.x, x1.y + x2.y);
+  const C r = mkc<C>(d.x * t.x + d.y * t.y, d.y * t.x - d.x * t.y);
+  return mkc<C>(s.x - r.y, s.y + r.x);
+}
+template <typename C>
+__device__ __forceinline__ C herm_post(C z1, C z2, C t) {  // X[k] from Z[k], Z[NR-k]
+  using T = decltype(C::x);
+  const C s = mkc<C>((z1.x + z2.x) * (T)0.5, (z1.y - z2.y) * (T)0.5);
+  const C q = mkc<C>((z1.y + z2.y) * (T)0.5, -(z1.x - z2.x) * (T)0.5);
+  return mkc<C>(s.x + q.x * t.x - q.y * t.y, s.y + q.x * t.y + q.y * t.x);
+}
+
+// Hermitian pre-processing + inverse row stage 1, in place on rows of S; ends synced
+template <typename C, class G>
+__device__ __forceinline__ void row_stage1_inv_pre(C* S, const C* tws, int nr, int tid) {
+  static_assert(G::RA == 2 && G::RB % 2 == 1, "pair fusion needs RA = 2");
+  constexpr int NR = Derived<G>::NR, PR = Derived<G>::PR, RB = G::RB, TPR = RB / 2 + 1;
+  for (int e = tid; e < nr * TPR; e += blockDim.x) {
+    const int i = e / TPR, n2 = e - i * TPR;
+    C* row = S + i * PR;
+    if (n2 == 0) {  // bins 0 (partner: the X[NR] slot) and RB = NR / 2 (its own partner)
+      const C a0 = row[0], b0 = row[NR], a1 = row[RB];
+      const C z0 = herm_pre(a0, b0, tws[0]), z1 = herm_pre(a1, a1, tws[RB]);
+      row[0] = vadd(z0, z1);
+      row[RB] = vsub(z0, z1);
+    } else {
+      const int p0 = 2 * n2, p1 = 2 * n2 + RB, q0 = NR - p0, q1 = NR - p1;
+      const C a0 = row[p0], a1 = row[p1], b0 = row[q0], b1 = row[q1];
+      const C za0 = herm_pre(a0, b0, tws[p0]), za1 = herm_pre(a1, b1, tws[p1]);
+      const C zb0 = herm_pre(b0, a0, tws[q0]), zb1 = herm_pre(b1, a1, tws[q1]);
+      row[p0] = vadd(za0, za1);
+      row[p1] = vsub(za0, za1);
+      row[q0] = vadd(zb0, zb1);
+      row[q1] = vsub(zb0, zb1);
+    }
+  }
+  __syncthreads();
+}
+
+// forward row stage 2 out of place (src -> dst) with the post-processing fused in: dst rows hold
+// the half spectrum X[0..NR] in natural order; ends synced
+template <typename C, class G>
+__device__ __forceinline__ void row_stage2_fwd_post(const C* src, C* dst, const C* tws, int nr, int tid) {
+  static_assert(G::RA == 2, "pair fusion needs RA = 2");
+  constexpr int NR = Derived<G>::NR, PR = Derived<G>::PR, RB = G::RB;
+  for (int e = tid; e < nr * G::RA; e += blockDim.x) {
+    const int i = e / G::RA, k1 = e - i * G::RA;
+    C v[RB];
+    stage2_load<C, G::RA, RB, false>(src + i * PR, 1, k1, v);
+    const OutRow<G::RA, RB> o(k1);
+    C* row = dst + i * PR;
+    sfft::static_for<0, RB>([&](auto K2) {
+      constexpr int k2 = K2.value, kp = (RB - k2) % RB;  // bin NR - k of bin k
+      const int k = o.template at<k2>();
+      row[k] = herm_post(v[k2], v[kp], tws[k]);
+    });
+    if (k1 == 0) row[NR] = herm_post(v[0], v[0], tws[NR]);
+  }
+  __syncthreads();
+}
+
 // ----------------------------------------------------------------- row pass --
 template <typename T, class G>
 struct RowArgs {
@@ -514,12 +582,14 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   C* WB = SB + H * PR;                  // [H][NR] state plane (pairs)
   C* PT = WB + H * NR;                  // [NF] the group's synthesis partial
   __shared__ double scratch[4 * 32];
+  __shared__ C tws[NR + 1];  // e^{-2 pi i k / W}, k <= NR
   const int b = blockIdx.y, grp = blockIdx.x;
   if (*a.fl.all_done || a.fl.done[b]) return;
   const int tid = threadIdx.x;
   const int k0 = grp * a.kper, k1 = min(a.K, k0 + a.kper);
   const C* gb = a.g + (int64_t)b * NF;
   for (int f = tid; f < NF; f += NT) PT[f] = mkc<C>(0, 0);
+  for (int i = tid; i <= NR; i += NT) tws[i] = a.tw[i];
   C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};
   bool nonfinite = false;
   const C ip2 = mkc<C>(a.invP, a.invP);
@@ -561,27 +631,9 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
       __syncthreads();
     }
     PLANE_STAMP(3)
-    // (c) Hermitian pre-processing of every row, (d) row IFFT
-    for (int e = tid; e < H * (NR / 2 + 1); e += NT) {
-      const int i = e / (NR / 2 + 1), kk = e - i * (NR / 2 + 1);
-      const int k2 = NR - kk;
-      C* row = SB + i * PR;
-      const C x1 = row[kk], x2 = row[k2];
-      const C t1 = a.tw[kk], t2 = a.tw[k2];
-      const C s1 = mkc<C>(x1.x + x2.x, x1.y - x2.y), d1 = mkc<C>(x1.x - x2.x, x1.y + x2.y);
-      const C r1 = mkc<C>(d1.x * t1.x + d1.y * t1.y, d1.y * t1.x - d1.x * t1.y);
-      const C s2 = mkc<C>(x2.x + x1.x, x2.y - x1.y), d2 = mkc<C>(x2.x - x1.x, x2.y + x1.y);
-      const C r2 = mkc<C>(d2.x * t2.x + d2.y * t2.y, d2.y * t2.x - d2.x * t2.y);
-      row[kk] = mkc<C>(s1.x - r1.y, s1.y + r1.x);
-      if (kk != 0 && k2 != kk) row[k2] = mkc<C>(s2.x - r2.y, s2.y + r2.x);
-    }
-    __syncthreads();
+    // (c) Hermitian pre-processing of every row fused into (d) row IFFT stage 1
+    row_stage1_inv_pre<C, G>(SB, tws, H, tid);
     PLANE_STAMP(4)
-    for (int e = tid; e < H * G::RB; e += NT) {
-      const int i = e / G::RB, n2 = e - i * G::RB;
-      stage1<C, G::RA, G::RB, true>(SB + i * PR, 1, n2);
-    }
-    __syncthreads();
     PLANE_STAMP(5)
     row_stage2_oop<C, G, true>(SB, SA, H, tid);
     PLANE_STAMP(6)
@@ -618,26 +670,9 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
     }
     __syncthreads();
     PLANE_STAMP(9)
-    row_stage2_oop<C, G, false>(SA, SB, H, tid);
+    // (g) post-processing fused into row stage 2: SB = forward half spectrum rows
+    row_stage2_fwd_post<C, G>(SA, SB, tws, H, tid);
     PLANE_STAMP(10)
-    for (int e = tid; e < H * (NR / 2 + 1); e += NT) {
-      const int i = e / (NR / 2 + 1), kk = e - i * (NR / 2 + 1);
-      const int k2 = NR - kk;  // kk = 0: k2 = NR -> X[0] and X[NR] from Z[0]
-      C* row = SB + i * PR;
-      const C za = row[kk], zb = row[kk == 0 ? 0 : k2];
-      auto post = [&](C z1, C z2, int kx) {
-        const C s1 = mkc<C>((z1.x + z2.x) * (T)0.5, (z1.y - z2.y) * (T)0.5);
-        const C d1 = mkc<C>((z1.x - z2.x) * (T)0.5, (z1.y + z2.y) * (T)0.5);
-        const C q = mkc<C>(d1.y, -d1.x);
-        const C t = a.tw[kx];
-        return mkc<C>(s1.x + q.x * t.x - q.y * t.y, s1.y + q.x * t.y + q.y * t.x);
-      };
-      const C xa = post(za, zb, kk);  // X[kk] = f(Z[kk], Z[NR-kk])
-      const C xb = post(zb, za, k2);  // X[NR-kk] = f(Z[NR-kk], Z[kk])
-      row[kk] = xa;
-      if (k2 != kk) row[k2] = xb;
-    }
-    __syncthreads();
     PLANE_STAMP(11)
     // (h) column FFT
     for (int e = tid; e < G::CB * WH; e += NT) {
