@@ -22,6 +22,7 @@
 // produces F(U) (needed by the history), the code U, and the objective.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <map>
 #include <tuple>
 
@@ -540,10 +541,13 @@ static FusedPlan plan_for(int K, int B) {
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k_code_fused<T, N>) != cudaSuccess) return plan;
-  FusedShape shapes[4];
+  FusedShape shapes[16];
   int ns = 0;
-  for (int cs : {2, 4, 8, 16}) {
+  const char* force = getenv("OCSC_FUSED_CS");  // dev knob: a single cluster size, no tail
+  const int fcs = force ? atoi(force) : 0;
+  for (int cs = 2; cs <= 16; ++cs) {
     if (cs > K) break;
+    if (fcs && cs != fcs) continue;
     FusedShape sh;
     sh.cs = cs;
     sh.nk = (K + cs - 1) / cs;

@@ -330,7 +330,27 @@ def test_fused_kernel_is_selected_for_config1():
     tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=100, dtype="float32", batch_size=50))
     assert tr.use_fused(50)
     from paper_1706_06972_b200 import _lib
-    assert _lib.load().ocsc_code_fused_cluster(4, 42, 42, 100, 50) in (2, 4, 8, 16)
+    assert 2 <= _lib.load().ocsc_code_fused_cluster(4, 42, 42, 100, 50) <= 16
+
+
+@pytest.mark.parametrize("cs", [3, 5, 9, 15])
+def test_fused_any_cluster_size_equals_cufft_path(cs, monkeypatch):
+    """Non-power-of-two cluster shapes (uneven filter split, slices, DSMEM reduction) match the
+    cuFFT path; OCSC_FUSED_CS pins the shape of a (K, B) plan that is new to this process."""
+    dims, K, B = (30, 30), 4 * cs + 1, 2
+    monkeypatch.setenv("OCSC_FUSED_CS", str(cs))
+    from paper_1706_06972_b200 import _lib
+    assert _lib.load().ocsc_code_fused_cluster(8, 30, 30, K, B) == cs
+    shape = ob.SignalShape(dims, (3, 3))
+    X = O.synth_images(B, dims, dims, 3, filter_dims=(3, 3), seed=11, density=0.05).reshape(B, -1)
+    kw = dict(n_filters=K, beta=0.3, rho_code=1.0, rho_dict=1.0, inner_iters=2, seed=4, code_max_iters=60,
+              batch_size=B, stop_tol=0.0)
+    a = ob.OnlineTrainer(shape, ob.TrainConfig(fused=True, **kw))
+    b = ob.OnlineTrainer(shape, ob.TrainConfig(fused=False, **kw))
+    ra, rb = a.partial_fit(X), b.partial_fit(X)
+    assert np.array_equal(ra.iterations, rb.iterations)
+    assert np.allclose(ra.objectives, rb.objectives, rtol=1e-11, atol=0)
+    assert rel(ra.codes.cpu().numpy(), rb.codes.cpu().numpy()) < 1e-10
 
 
 def test_fused_minibatch_matches_composed_reference(golden):
