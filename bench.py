@@ -132,6 +132,19 @@ class ClockSampler:
                 "power_w_median": statistics.median(pw) if pw else None}
 
 
+def fp32_peak_tflops(sms, sm_mhz):
+    """(peak, source): the measured FMA-chain rate (profiles/r1_fma_peaks.json, scripts/fma_peak.cu)
+    scaled to the clock the kernel ran at; the nominal 128 FMA/clk/SM if the file is absent."""
+    try:
+        m = json.load(open(os.path.join(ROOT, "profiles", "r1_fma_peaks.json")))
+        per_clk = float(m["ffma_tflops"]) * 1e12 / (int(m["sms"]) * float(m["sm_mhz"]) * 1e6)
+        return (sms * per_clk * float(sm_mhz) * 1e6 / 1e12,
+                f"measured FFMA chain rate ({per_clk:.0f} flop/clk/SM, profiles/r1_fma_peaks.json, "
+                f"scripts/fma_peak.cu) x median SM clock in the timed region")
+    except (OSError, KeyError, ValueError):
+        return sms * 128 * 2 * float(sm_mhz) * 1e6 / 1e12, "nominal 128 FMA/clk/SM x 2 x median SM clock"
+
+
 # --------------------------------------------------------------- CPU legs --
 def cpu_threads():
     try:
@@ -325,7 +338,7 @@ def run_b200(args, rank, world, local_rank):
     barrier()
     clocks = sampler.stop()
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 2 * float(sm_mhz) * 1e6 / 1e12
+    fp32_peak, fp32_src = fp32_peak_tflops(torch.cuda.get_device_properties(dev).multi_processor_count, sm_mhz)
     achieved_tf = B * flops_per_img_iter / (it_ms / 1e3) / 1e12   # TFLOP/s
     e2e_s = max_over_ranks(e2e_s)
     e2e = world * B * args.steps / e2e_s
@@ -374,8 +387,7 @@ def run_b200(args, rank, world, local_rank):
                 "roofline_fp32": {"achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
                                   "frac": achieved_tf / fp32_peak,
                                   "flops": "SURVEY 8(d): 2K*2.5*P*log2(P) + 16*Ph*K + 8*P*K per image-iteration",
-                                  "peak_source": "148 SMs x 128 FMA/clk x 2 x median SM clock sampled in the timed "
-                                                 "region (nominal FP32 rate at the clock the kernel ran at)",
+                                  "peak_source": fp32_src,
                                   "ncu_fma_pipe_active_pct": pipe and pipe.get("sm__pipe_fma_cycles_active_pct_of_peak_active"),
                                   "ncu_source": pipe and pipe.get("source")},
                 "cpu_baseline": cpu,
@@ -408,7 +420,7 @@ def run_history_microbench(args, rank, world, local_rank):
     except OSError:
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    fp32 = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * 2 * 1965e6 / 1e12
+    fp32, _ = fp32_peak_tflops(torch.cuda.get_device_properties(dev).multi_processor_count, 1965.0)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     shape = ob.SignalShape((P,), (1,))
