@@ -280,9 +280,11 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
                                                             cx<Ti>* inv, int32_t* info) {
   using C = cx<Th>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* rowk = reinterpret_cast<C*>(smem_raw);
-  C* colk = rowk + K;
-  __shared__ Th piv_s;  // 1 / pivot, computed once by the pivot's owner
+  // row k / column k / 1 / pivot, double-buffered by step parity: the owners of step k + 1
+  // publish while the others may still read step k's copies, so one barrier per step suffices
+  C* rowb = reinterpret_cast<C*>(smem_raw);  // [2][K]
+  C* colb = rowb + 2 * K;                    // [2][K]
+  __shared__ Th piv_b[2];
   const int p = blockIdx.x;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
   const C* Sp = S + (int64_t)p * npk;
@@ -304,6 +306,8 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
       a[ii][jj] = v;
     }
   for (int k = 0; k < K; ++k) {
+    C* rowk = rowb + (k & 1) * K;
+    C* colk = colb + (k & 1) * K;
     const bool own_row = k >= i0 && k < i0 + BI, own_col = k >= j0 && k < j0 + BJ;
     // publish row k and column k (only their owners)
     if (own_row) {
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
             if (j0 + jj < K) rowk[j0 + jj] = a[ii][jj];
             if (j0 + jj == k) {  // pivot owner: one reciprocal per step for the whole CTA
               const Th d = a[ii][jj].x;
-              piv_s = (Th)1 / d;
+              piv_b[k & 1] = (Th)1 / d;
               if (!(d > (Th)0)) atomicCAS(info, 0, p + 1);
             }
           }
@@ -329,7 +333,7 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
             if (i0 + ii < K) colk[i0 + ii] = a[ii][jj];
     }
     __syncthreads();
-    const Th pinv = piv_s;
+    const Th pinv = piv_b[k & 1];
     // generic rank-1 update with row/column k masked out (ci = 0 on row k, rs = 0 on column k)
     C rs[BJ];
 #pragma unroll
@@ -364,7 +368,6 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
           for (int ii = 0; ii < BI; ++ii)
             if (i0 + ii != k && i0 + ii < K) a[ii][jj] = cscale(colk[i0 + ii], -pinv);
     }
-    __syncthreads();
   }
   cx<Ti>* out = inv + (int64_t)p * npk;
 #pragma unroll
@@ -484,7 +487,7 @@ static int launch_invert(int K, int nfreq, const void* S, double ridge, double s
   if (K > 32 && K <= 100) {
     // register-blocked path: 4 x 5 blocks, ceil(K/4) * ceil(K/5) <= 500 threads
     const int threads = ((((K + 3) / 4) * ((K + 4) / 5)) + 31) / 32 * 32;
-    const size_t sm = sizeof(cx<Th>) * 2 * (size_t)K;
+    const size_t sm = sizeof(cx<Th>) * 4 * (size_t)K;
     k_hist_invert_reg<Th, Ti, 4, 5><<<nfreq, threads, sm, s>>>(K, (const cx<Th>*)S, (Th)ridge, (Th)scale,
                                                               (cx<Ti>*)inv, info);
     OCSC_LAUNCHED("k_hist_invert_reg");
