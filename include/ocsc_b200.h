@@ -166,6 +166,16 @@ int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int nfreq, int 
  * info (device int32): 0, or 1 + a frequency whose matrix was not positive definite. */
 int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfreq, const void* S, double ridge,
                         double scale, void* inv, int32_t* info, void* stream);
+/* Low-rank refresh of a packed inverse (Woodbury): out_p = (A_p + U_p U_p^H)^-1 from
+ * inv_in_p = A_p^-1 (packed complex128, e.g. ocsc_history_invert with dtype_inv = f64), U_p the
+ * K x nb code spectra z element (b,k,p) at z[b*z_sb + k*z_sk + p*z_sp], nb <= 32; out packed as
+ * dtype_out.  Lets a trainer invert S plus most of a mini-batch while the rest is still being
+ * coded, then fold the remainder in O(K^2 nb) (no reference counterpart; same result as
+ * ocsc_history_invert of the full sum).  info as ocsc_history_invert (capacitance matrix). */
+int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, const void* inv_in,
+                          const void* z, int64_t z_sb, int64_t z_sk, int64_t z_sp, void* out,
+                          int32_t* info, void* stream);
+size_t ocsc_history_woodbury_smem(int K, int nb);
 /* Large K (multiple of 32; BASELINE configs 3-4): blocked right-looking Cholesky of
  * S_p + ridge I per frequency (one CTA per frequency, 32x32 tiles, panel staged in shared
  * memory, one warp per trailing tile).  L is written full (nfreq, K, K), lower triangle;

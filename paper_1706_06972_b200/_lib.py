@@ -56,6 +56,8 @@ SIGNATURES = {
     "ocsc_synthesize": [_I, _I, _I, _I, _P, _P, _P, _P],
     "ocsc_history_accumulate": [_I, _I, _I, _I, _I, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P],
     "ocsc_history_invert": [_I, _I, _I, _I, _P, _D, _D, _P, _P, _P],
+    "ocsc_history_woodbury": [_I, _I, _I, _I, _I, _P, _P, _I64, _I64, _I64, _P, _P, _P],
+    "ocsc_history_woodbury_smem": [_I, _I],
     "ocsc_packed_to_full": [_I, _I, _I, _P, _D, _P, _P],
     "ocsc_history_factor_bytes": [_I, _I, _I],
     "ocsc_history_factor": [_I, _I, _I, _P, _D, _P, _P, _P],
@@ -76,6 +78,7 @@ SIGNATURES = {
 }
 _RESTYPES = {"ocsc_last_error": ctypes.c_char_p, "ocsc_code_workspace_bytes": _SZ,
              "ocsc_code_stream_workspace_bytes": _SZ, "ocsc_history_factor_bytes": _SZ,
+             "ocsc_history_woodbury_smem": _SZ,
              "ocsc_kernel_launches": ctypes.c_int64}
 
 _lib = None

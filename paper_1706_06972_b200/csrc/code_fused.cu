@@ -528,11 +528,11 @@ static int max_active_clusters(const FusedShape& sh, int B) {
   return n;
 }
 
-// Choose cluster shapes.  Per-cluster time ~ nk (filters per CTA); a wave runs `active`
-// clusters at once.  The main shape maximises samples per unit time; a remainder smaller
-// than the main shape's wave goes to the shape that finishes it soonest (usually a wider
-// cluster: BASELINE config 1 runs 45 samples as 3 waves of 15 eight-CTA clusters and the last
-// 5 as sixteen-CTA clusters instead of a mostly idle fourth wave).
+// Choose cluster shapes.  A wave runs `active` clusters at once and lasts ~ nk + const
+// (nk = filters per CTA).  The plan minimises the modelled makespan over (main shape, tail
+// shape) pairs: BASELINE config 1 runs 45 samples as 3 waves of 15 nine-CTA clusters and the
+// last 5 on fifteen-CTA clusters instead of a mostly idle fourth wave; a batch smaller than one
+// wave takes the shape that finishes soonest (the widest cluster that holds it).
 template <typename T, int N>
 static FusedPlan plan_for(int K, int B) {
   FusedPlan plan;
@@ -558,24 +558,34 @@ static FusedPlan plan_for(int K, int B) {
     if (sh.active > 0) shapes[ns++] = sh;
   }
   if (!ns) return plan;
-  // main shape: most samples per unit time (ties -> smaller cluster)
-  int best = 0;
-  for (int i = 1; i < ns; ++i)
-    if ((double)shapes[i].active / shapes[i].nk > (double)shapes[best].active / shapes[best].nk * 1.02) best = i;
-  plan.main = shapes[best];
-  const int full = (B / plan.main.active) * plan.main.active;
-  const int rem = B - full;
-  plan.b_main = B;
-  if (rem > 0 && full > 0) {
-    // finish the remainder with whichever shape completes it first
-    double best_t = (double)plan.main.nk;  // one more (partial) wave of the main shape
-    for (int i = 0; i < ns; ++i) {
-      const double t = (double)((rem + shapes[i].active - 1) / shapes[i].active) * shapes[i].nk;
-      if (t < best_t * 0.95) {
-        best_t = t;
-        plan.tail = shapes[i];
-        plan.b_main = full;
-      }
+  // makespan model: a wave of a shape costs (nk + 3.5) units (filters per CTA plus a fixed
+  // per-iteration cluster overhead; fitted to scripts/cluster_sweep.py on a B200).  Take the
+  // main shape and optional tail shape with the smallest total: full waves of the main shape,
+  // then the remainder either as one more main wave or on the tail shape's waves.
+  auto cost = [](const FusedShape& sh) { return (double)sh.nk + 3.5; };
+  double best_t = 1e300;
+  for (int m = 0; m < ns; ++m) {
+    const FusedShape& M = shapes[m];
+    const int nfull = B / M.active, rem = B - nfull * M.active;
+    double t = nfull * cost(M);
+    int tail = -1;
+    if (rem > 0) {
+      double tr = cost(M);
+      if (nfull > 0)
+        for (int i = 0; i < ns; ++i) {
+          const double ti = (double)((rem + shapes[i].active - 1) / shapes[i].active) * cost(shapes[i]);
+          if (ti < tr * 0.98) {
+            tr = ti;
+            tail = i;
+          }
+        }
+      t += tr;
+    }
+    if (t < best_t * 0.999) {
+      best_t = t;
+      plan.main = M;
+      plan.tail = tail >= 0 ? shapes[tail] : FusedShape{};
+      plan.b_main = tail >= 0 ? nfull * M.active : B;
     }
   }
   return plan;

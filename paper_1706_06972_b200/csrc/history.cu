@@ -436,6 +436,127 @@ using namespace ocsc;
 
 static size_t csize(int dtype) { return dtype == OCSC_F64 ? 16 : 8; }
 
+// Low-rank refresh of a packed Hermitian inverse (Woodbury):
+//   (A + U U^H)^-1 = A^-1 - W (I + U^H W)^-1 W^H,  W = A^-1 U,  U = the nb new code spectra (K x nb)
+// One CTA per frequency; A^-1 (packed, f64) is staged in shared memory, the nb x nb capacitance
+// matrix is inverted by one thread (nb is a mini-batch remainder, <= 32).  Lets the trainer
+// invert S + (most of the batch) while the rest of the batch is still being coded.
+template <typename Tz, typename To>
+__global__ void __launch_bounds__(256) k_hist_woodbury(int K, int nb, const double2* __restrict__ inv_in,
+                                                      const typename Cx<Tz>::type* __restrict__ z, int64_t zb,
+                                                      int64_t zk, int64_t zp, typename Cx<To>::type* out,
+                                                      int32_t* info) {
+  using C = double2;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int p = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const int64_t npk = (int64_t)K * (K + 1) / 2;
+  C* A = reinterpret_cast<C*>(smraw);  // packed A^-1
+  C* U = A + npk;                      // [K][nb]
+  C* Wm = U + K * nb;                  // [K][nb]  W = A^-1 U, then X = W Cinv
+  C* X = Wm + K * nb;                  // [K][nb]
+  C* Cm = X + K * nb;                  // [nb][nb] capacitance, inverted in place
+  const double2* Ap = inv_in + (int64_t)p * npk;
+  for (int64_t e = tid; e < npk; e += nt) A[e] = Ap[e];
+  for (int e = tid; e < K * nb; e += nt) {
+    const int k = e / nb, j = e - k * nb;
+    const auto v = z[j * zb + k * zk + p * zp];
+    U[e] = make_double2((double)v.x, (double)v.y);
+  }
+  __syncthreads();
+  auto a_at = [&](int i, int k) -> C {  // A^-1[i][k] from the lower packed triangle
+    return i >= k ? A[packed_index(i, k)] : cconj(A[packed_index(k, i)]);
+  };
+  for (int e = tid; e < K * nb; e += nt) {
+    const int i = e / nb, j = e - i * nb;
+    C acc = make_double2(0, 0);
+    for (int k = 0; k < K; ++k) cfma(acc, a_at(i, k), U[k * nb + j]);
+    Wm[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += nt) {  // C = I + U^H W
+    const int a = e / nb, b = e - a * nb;
+    C acc = make_double2(a == b ? 1.0 : 0.0, 0);
+    for (int k = 0; k < K; ++k) {
+      const C u = U[k * nb + a], w = Wm[k * nb + b];
+      acc.x += u.x * w.x + u.y * w.y;  // conj(u) w
+      acc.y += u.x * w.y - u.y * w.x;
+    }
+    Cm[e] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {  // in-place Gauss-Jordan of the nb x nb HPD capacitance matrix
+    for (int k = 0; k < nb; ++k) {
+      const double d = Cm[k * nb + k].x;
+      if (!(d > 0)) atomicCAS(info, 0, p + 1);
+      const double pinv = 1.0 / d;
+      for (int j = 0; j < nb; ++j) Cm[k * nb + j] = cscale(Cm[k * nb + j], pinv);
+      Cm[k * nb + k] = make_double2(pinv, 0);
+      for (int i = 0; i < nb; ++i) {
+        if (i == k) continue;
+        const C f = Cm[i * nb + k];
+        for (int j = 0; j < nb; ++j) {
+          if (j == k) continue;
+          const C r = Cm[k * nb + j];
+          Cm[i * nb + j] = make_double2(Cm[i * nb + j].x - (f.x * r.x - f.y * r.y),
+                                        Cm[i * nb + j].y - (f.x * r.y + f.y * r.x));
+        }
+        Cm[i * nb + k] = make_double2(-(f.x * pinv), -(f.y * pinv));
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < K * nb; e += nt) {  // X = W Cinv
+    const int i = e / nb, j = e - i * nb;
+    C acc = make_double2(0, 0);
+    for (int m = 0; m < nb; ++m) cfma(acc, Wm[i * nb + m], Cm[m * nb + j]);
+    X[e] = acc;
+  }
+  __syncthreads();
+  typename Cx<To>::type* o = out + (int64_t)p * npk;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  for (int i = warp; i < K; i += nw)
+    for (int j = lane; j <= i; j += 32) {  // out[i][j] = A^-1[i][j] - sum_m X[i][m] conj(W[j][m])
+      C acc = A[packed_index(i, j)];
+      for (int m = 0; m < nb; ++m) {
+        const C x = X[i * nb + m], w = Wm[j * nb + m];
+        acc.x -= x.x * w.x + x.y * w.y;
+        acc.y -= x.y * w.x - x.x * w.y;
+      }
+      o[packed_index(i, j)] = ccast<To>(acc);
+    }
+}
+
+extern "C" size_t ocsc_history_woodbury_smem(int K, int nb) {
+  return sizeof(double2) * ((size_t)K * (K + 1) / 2 + 3 * (size_t)K * nb + (size_t)nb * nb);
+}
+
+extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, const void* inv_in,
+                                     const void* z, int64_t z_sb, int64_t z_sk, int64_t z_sp, void* out,
+                                     int32_t* info, void* stream) {
+  if (K <= 0 || nfreq < 0 || nb < 0 || nb > 32) return fail(OCSC_ESHAPE, "history_woodbury: bad extents (nb <= 32)");
+  cudaStream_t s = as_stream(stream);
+  OCSC_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
+  if (nfreq == 0) return OCSC_OK;
+  const size_t sm = ocsc_history_woodbury_smem(K, nb);
+  if (sm > 227 * 1024) return fail(OCSC_EARG, "history_woodbury: K too large for the shared-memory inverse");
+#define OCSC_WB(TZ, TO)                                                                                        \
+  do {                                                                                                         \
+    OCSC_CUDA(cudaFuncSetAttribute(k_hist_woodbury<TZ, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                                   (int)sm));                                                                  \
+    k_hist_woodbury<TZ, TO><<<nfreq, 256, sm, s>>>(K, nb, (const double2*)inv_in,                               \
+                                                   (const typename Cx<TZ>::type*)z, z_sb, z_sk, z_sp,           \
+                                                   (typename Cx<TO>::type*)out, info);                         \
+  } while (0)
+  if (dtype_z == OCSC_F32 && dtype_out == OCSC_F32) OCSC_WB(float, float);
+  else if (dtype_z == OCSC_F32 && dtype_out == OCSC_F64) OCSC_WB(float, double);
+  else if (dtype_z == OCSC_F64 && dtype_out == OCSC_F64) OCSC_WB(double, double);
+  else if (dtype_z == OCSC_F64 && dtype_out == OCSC_F32) OCSC_WB(double, float);
+  else return fail(OCSC_EARG, "history_woodbury: dtype must be 4 or 8");
+#undef OCSC_WB
+  OCSC_LAUNCHED("k_hist_woodbury");
+  return OCSC_OK;
+}
+
 extern "C" int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int nfreq, int B, const void* z,
                                        int64_t z_sb, int64_t z_sk, int64_t z_sp, const void* x, int64_t x_sb,
                                        int64_t x_sp, void* S, void* c, void* stream) {

@@ -17,6 +17,7 @@ fold F(U) into the history, J rounds of dictionary ADMM, Wh <- F(V).
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import time
 from dataclasses import dataclass, field, replace
@@ -61,6 +62,8 @@ class TrainConfig:
     fused: bool = True             # on-chip cluster kernel when the grid has one (else cuFFT path)
     stream: bool = True            # streaming FFT kernels for larger grids that have them (else cuFFT)
     history_solver: str = "auto"   # "gj" explicit inverse (K <= 118/167) | "chol" blocked Cholesky | "auto"
+    overlap: bool = True           # fused plan with a tail: invert the history of the main part on a
+                                   # side stream while the tail is coded, then a Woodbury refresh
 
     def coding(self) -> CodingConfig:
         return CodingConfig(beta=self.beta, rho=self.rho_code, max_iters=self.code_max_iters,
@@ -192,6 +195,8 @@ class OnlineTrainer:
         self._x = None
         self._obj = None
         self._fused_ok = {}
+        self._side = None          # side stream + scratch of the overlapped history inverse
+        self._tl = None            # dev aid: list collecting (label, timing event) of the overlap
 
     # ---------------------------------------------------------- internals --
     def _make_history(self, hist_cdtype: torch.dtype) -> HistoryState:
@@ -220,6 +225,92 @@ class OnlineTrainer:
             self._fused_ok[key] = _lib.load().ocsc_code_fused_cluster(_lib.code(self.dtype), self.H, self.W,
                                                                       self.K, B) > 0
         return self._fused_ok[key]
+
+    def _split_plan(self, B: int) -> int:
+        """b_main when the fused plan codes B samples on two cluster shapes (main waves + a tail
+        of <= 32 samples) and the history inverse can overlap the tail; 0 otherwise."""
+        key = ("split", B)
+        if key not in self._fused_ok:
+            info = (ctypes.c_int32 * 8)()
+            lib = _lib.load()
+            lib.ocsc_code_fused_info(_lib.code(self.dtype), self.H, self.W, self.K, B, info)
+            b1 = int(info[5])
+            h = self.history
+            ok = (self.config.overlap and 0 < b1 < B and B - b1 <= 32 and info[6] > 0
+                  and type(self)._fold is OnlineTrainer._fold and h.solver == "gj"
+                  and h.S.dtype == torch.complex128
+                  and lib.ocsc_history_woodbury_smem(self.K, B - b1) <= 227 * 1024)
+            self._fused_ok[key] = b1 if ok else 0
+        return self._fused_ok[key]
+
+    def _code_fused(self, xh, buf, uh, obj, b0: int, b1: int) -> None:
+        """ocsc_code_fused on samples [b0, b1) of the mini-batch (pointer offsets; own plan)."""
+        n = b1 - b0
+        if n <= 0:
+            return
+        cc = self.coding_config
+        P, nf = self.H * self.W, self.nf
+        es, ce = buf.u.element_size(), uh.element_size()
+        _lib.call("ocsc_code_fused", _lib.code(self.dtype), self.H, self.W, self.K, n,
+                  xh.data_ptr() + b0 * nf * xh.element_size(), _lib.ptr(self.Wh), _lib.ptr(self.den), cc.beta,
+                  cc.rho, cc.max_iters, cc.rel_tol, buf.u.data_ptr() + b0 * self.K * P * es, None,
+                  uh.data_ptr() + b0 * self.K * nf * ce, obj.data_ptr() + b0 * obj.element_size(), None,
+                  buf.iters.data_ptr() + b0 * 4, buf.status.data_ptr() + b0 * 4, _lib.stream())
+
+    def _mark(self, label: str) -> None:
+        if self._tl is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._tl.append((label, ev))
+
+    def _side_state(self) -> dict:
+        h = self.history
+        if self._side is None or self._side["S"].shape != h.S.shape:
+            self._side = {"stream": torch.cuda.Stream(device=self.dev),
+                          "hi": torch.cuda.Stream(device=self.dev, priority=-8),
+                          "S": torch.empty_like(h.S), "c": torch.empty_like(h.c), "inv": torch.empty_like(h.S),
+                          "info": torch.zeros(2, dtype=torch.int32, device=self.dev)}
+        return self._side
+
+    def _prefold_side(self, uh, xh, b1: int, B: int, ready: torch.cuda.Event) -> torch.cuda.Event:
+        """Side stream, after `ready`: S' = S + (samples [0, b1)), c' likewise, and the f64 inverse
+        of S' + t_final rho P I; the history itself is untouched (a divergence found after the
+        tail leaves it as it was)."""
+        h, nf, K = self.history, self.nf, self.K
+        sd = self._side_state()
+        with torch.cuda.stream(sd["stream"]):
+            sd["stream"].wait_event(ready)
+            self._mark("side start")
+            sd["S"].copy_(h.S)
+            sd["c"].copy_(h.c)
+            _lib.call("ocsc_history_accumulate", _lib.code(uh.dtype), _lib.code(h.S.dtype), K, nf, b1, _lib.ptr(uh),
+                      K * nf, nf, 1, _lib.ptr(xh), nf, 1, _lib.ptr(sd["S"]), _lib.ptr(sd["c"]), _lib.stream())
+            _lib.call("ocsc_history_invert", _lib.code(h.S.dtype), _lib.code(h.S.dtype), K, nf, _lib.ptr(sd["S"]),
+                      (h.count + B) * h.ridge, 1.0, _lib.ptr(sd["inv"]), _lib.ptr(sd["info"]), _lib.stream())
+            self._mark("side end")
+            done = torch.cuda.Event()
+            done.record()
+        return done
+
+    def _fold_overlapped(self, uh, xh, b1: int, B: int, side_done: torch.cuda.Event) -> None:
+        """Main stream: fold the tail samples into S', Woodbury-refresh the inverse, adopt S'/c'."""
+        h, nf, K, sd = self.history, self.nf, self.K, self._side
+        torch.cuda.current_stream().wait_event(side_done)
+        nb = B - b1
+        ce = uh.element_size()
+        _lib.call("ocsc_history_accumulate", _lib.code(uh.dtype), _lib.code(h.S.dtype), K, nf, nb,
+                  uh.data_ptr() + b1 * K * nf * ce, K * nf, nf, 1, xh.data_ptr() + b1 * nf * xh.element_size(),
+                  nf, 1, _lib.ptr(sd["S"]), _lib.ptr(sd["c"]), _lib.stream())
+        if h._inv is None:
+            h._inv = torch.empty(h.S.shape, dtype=h.inv_dtype, device=h.S.device)
+        _lib.call("ocsc_history_woodbury", _lib.code(uh.dtype), _lib.code(h.inv_dtype), K, nf, nb, _lib.ptr(sd["inv"]),
+                  uh.data_ptr() + b1 * K * nf * ce, K * nf, nf, 1, _lib.ptr(h._inv), _lib.ptr(sd["info"][1:]),
+                  _lib.stream())
+        h.S, sd["S"] = sd["S"], h.S
+        h.c, sd["c"] = sd["c"], h.c
+        h.count += B
+        h._inv_count = h.count  # (the hot path's row solves run with check=False, as before)
+        self._mark("fold end")
 
     def _load(self, X) -> tuple[torch.Tensor, int]:
         P = self.shape.size
@@ -284,13 +375,29 @@ class OnlineTrainer:
         uh = self._uh[:B]
         fused = self.use_fused(B) and not want_z
         stream = not fused and not want_z and self.config.stream and stream_supported(self.shape, self.dtype)
+        split = self._split_plan(B) if fused else 0
         if fused:
             obj = self._obj[:B]
-            cc = self.coding_config
-            _lib.call("ocsc_code_fused", _lib.code(self.dtype), self.H, self.W, self.K, B, _lib.ptr(xh),
-                      _lib.ptr(self.Wh), _lib.ptr(self.den), cc.beta, cc.rho, cc.max_iters, cc.rel_tol,
-                      _lib.ptr(buf.u), None, _lib.ptr(uh), _lib.ptr(obj), None, _lib.ptr(buf.iters),
-                      _lib.ptr(buf.status), _lib.stream())
+            if split:
+                # main waves on the trainer's stream; the tail on a high-priority stream so its
+                # clusters are placed before the side stream's history kernels fill the free SMs
+                self._mark("main start")
+                self._code_fused(xh, buf, uh, obj, 0, split)
+                main_done = torch.cuda.Event()
+                main_done.record()
+                self._mark("main end")
+                sd = self._side_state()
+                with torch.cuda.stream(sd["hi"]):
+                    sd["hi"].wait_event(main_done)
+                    self._mark("tail start")
+                    self._code_fused(xh, buf, uh, obj, split, B)
+                    tail_done = torch.cuda.Event()
+                    tail_done.record()
+                    self._mark("tail end")
+                side_done = self._prefold_side(uh, xh, split, B, main_done)
+                torch.cuda.current_stream().wait_event(tail_done)
+            else:
+                self._code_fused(xh, buf, uh, obj, 0, B)
         elif stream:
             infer_codes_stream(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
         else:
@@ -302,7 +409,10 @@ class OnlineTrainer:
                 raise DivergenceError(f"code solver diverged at iteration {it}")
         if not fused:
             obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
-        self._fold(uh, xh, B)
+        if split:
+            self._fold_overlapped(uh, xh, split, B, side_done)
+        else:
+            self._fold(uh, xh, B)
         self._dictionary_update()
         track = self.config.stop_tol > 0
         if track:

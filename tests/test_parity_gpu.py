@@ -416,6 +416,45 @@ def test_fused_float32_matches_oracle_42x42():
     assert rel(tr.final_filters(), ora.final_filters()) < 1e-3
 
 
+def test_woodbury_refresh_matches_direct_inverse():
+    """ocsc_history_woodbury: (A + U U^H)^-1 from A^-1 equals the Gauss-Jordan inverse of the sum."""
+    from paper_1706_06972_b200 import _lib
+    K, nf, nb = 40, 7, 5
+    g = torch.Generator(device="cuda").manual_seed(3)
+    Z = torch.randn(nf, K, 2 * K, dtype=torch.complex128, device="cuda", generator=g)
+    A = Z @ Z.conj().transpose(1, 2) + 3.0 * torch.eye(K, dtype=torch.complex128, device="cuda")
+    z = torch.randn(nb, K, nf, dtype=torch.complex64, device="cuda", generator=g)  # (b, k, p) like the codes
+    ii, jj = torch.tril_indices(K, K)
+    inv_a = torch.linalg.inv(A)[:, ii, jj].contiguous()
+    out = torch.empty(nf, K * (K + 1) // 2, dtype=torch.complex128, device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("ocsc_history_woodbury", _lib.F32, _lib.F64, K, nf, nb, _lib.ptr(inv_a), _lib.ptr(z), K * nf, nf, 1,
+              _lib.ptr(out), _lib.ptr(info), _lib.stream())
+    U = z.to(torch.complex128).permute(2, 1, 0)  # (p, k, b)
+    want = torch.linalg.inv(A + U @ U.conj().transpose(1, 2))[:, ii, jj]
+    assert int(info.item()) == 0
+    assert rel(out.cpu().numpy(), want.cpu().numpy()) < 1e-12
+
+
+def test_overlapped_history_inverse_matches_serial_path():
+    """Config-1 shapes: the tail-overlapped inverse (side-stream Gauss-Jordan of the main part +
+    Woodbury refresh with the tail) trains like the serial accumulate-then-invert path."""
+    c = O.CONFIGS[1]
+    B = 50
+    X = O.synth_images(2 * B, c["dims0"], c["grid"], c["K0"], seed=21).reshape(2 * B, -1)
+    kw = dict(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0, inner_iters=10)
+    shape = ob.SignalShape(c["grid"], (11, 11))
+    a = ob.OnlineTrainer(shape, ob.TrainConfig(overlap=True, **kw))
+    b = ob.OnlineTrainer(shape, ob.TrainConfig(overlap=False, **kw))
+    assert a._split_plan(B) > 0 and b._split_plan(B) == 0
+    for m in range(2):
+        ra, rb = a.partial_fit(X[m * B:(m + 1) * B]), b.partial_fit(X[m * B:(m + 1) * B])
+        assert np.max(np.abs(ra.objectives - rb.objectives) / np.abs(rb.objectives)) < 1e-5
+    assert a.history.count == b.history.count == 2 * B
+    assert rel(a.history.inverse().cpu().numpy(), b.history.inverse().cpu().numpy()) < 1e-5
+    assert rel(a.final_filters(), b.final_filters()) < 1e-5
+
+
 def test_fused_divergence_raises():
     shape = ob.SignalShape((14, 14), (3, 3))
     tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=4, batch_size=2))
