@@ -168,7 +168,7 @@ int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfreq, const v
                         double scale, void* inv, int32_t* info, void* stream);
 /* Low-rank refresh of a packed inverse (Woodbury): out_p = (A_p + U_p U_p^H)^-1 from
  * inv_in_p = A_p^-1 (packed complex128, e.g. ocsc_history_invert with dtype_inv = f64), U_p the
- * K x nb code spectra z element (b,k,p) at z[b*z_sb + k*z_sk + p*z_sp], nb <= 32; out packed as
+ * K x nb code spectra z element (b,k,p) at z[b*z_sb + k*z_sk + p*z_sp], nb <= 16; out packed as
  * dtype_out.  Lets a trainer invert S plus most of a mini-batch while the rest is still being
  * coded, then fold the remainder in O(K^2 nb) (no reference counterpart; same result as
  * ocsc_history_invert of the full sum).  info as ocsc_history_invert (capacitance matrix). */

@@ -442,18 +442,18 @@ static size_t csize(int dtype) { return dtype == OCSC_F64 ? 16 : 8; }
 // matrix is inverted by one thread (nb is a mini-batch remainder, <= 32).  Lets the trainer
 // invert S + (most of the batch) while the rest of the batch is still being coded.
 template <typename Tz, typename To>
-__global__ void __launch_bounds__(256) k_hist_woodbury(int K, int nb, const double2* __restrict__ inv_in,
-                                                      const typename Cx<Tz>::type* __restrict__ z, int64_t zb,
-                                                      int64_t zk, int64_t zp, typename Cx<To>::type* out,
-                                                      int32_t* info) {
+__global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const double2* __restrict__ inv_in,
+                                                         const typename Cx<Tz>::type* __restrict__ z, int64_t zb,
+                                                         int64_t zk, int64_t zp, typename Cx<To>::type* out,
+                                                         int32_t* info) {
   using C = double2;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int p = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
   C* A = reinterpret_cast<C*>(smraw);  // packed A^-1
   C* U = A + npk;                      // [K][nb]
-  C* Wm = U + K * nb;                  // [K][nb]  W = A^-1 U, then X = W Cinv
-  C* X = Wm + K * nb;                  // [K][nb]
+  C* Wm = U + K * nb;                  // [K][nb]  W = A^-1 U
+  C* X = Wm + K * nb;                  // [K][nb]  X = W Cinv
   C* Cm = X + K * nb;                  // [nb][nb] capacitance, inverted in place
   const double2* Ap = inv_in + (int64_t)p * npk;
   for (int64_t e = tid; e < npk; e += nt) A[e] = Ap[e];
@@ -463,45 +463,76 @@ __global__ void __launch_bounds__(256) k_hist_woodbury(int K, int nb, const doub
     U[e] = make_double2((double)v.x, (double)v.y);
   }
   __syncthreads();
-  auto a_at = [&](int i, int k) -> C {  // A^-1[i][k] from the lower packed triangle
-    return i >= k ? A[packed_index(i, k)] : cconj(A[packed_index(k, i)]);
-  };
+  // W[t][j] = sum_{k<=t} A[t][k] U[k][j] + sum_{i>t} conj(A[i][t]) U[i][j]: the packed row of t,
+  // then its packed column (K terms for every t, branch-free), two interleaved accumulators
   for (int e = tid; e < K * nb; e += nt) {
-    const int i = e / nb, j = e - i * nb;
-    C acc = make_double2(0, 0);
-    for (int k = 0; k < K; ++k) cfma(acc, a_at(i, k), U[k * nb + j]);
-    Wm[e] = acc;
-  }
-  __syncthreads();
-  for (int e = tid; e < nb * nb; e += nt) {  // C = I + U^H W
-    const int a = e / nb, b = e - a * nb;
-    C acc = make_double2(a == b ? 1.0 : 0.0, 0);
-    for (int k = 0; k < K; ++k) {
-      const C u = U[k * nb + a], w = Wm[k * nb + b];
-      acc.x += u.x * w.x + u.y * w.y;  // conj(u) w
-      acc.y += u.x * w.y - u.y * w.x;
+    const int t = e / nb, j = e - t * nb;
+    C a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+    const C* row = A + packed_index(t, 0);
+    int k = 0;
+    for (; k + 1 <= t; k += 2) {
+      cfma(a0, row[k], U[k * nb + j]);
+      cfma(a1, row[k + 1], U[(k + 1) * nb + j]);
     }
-    Cm[e] = acc;
+    if (k <= t) cfma(a0, row[k], U[k * nb + j]);
+    int i = t + 1;
+    int64_t q = packed_index(i, t);  // packed (i, t): advances by i + 1 per row
+    for (; i + 1 < K; i += 2) {
+      cfma(a0, cconj(A[q]), U[i * nb + j]);
+      q += i + 1;
+      cfma(a1, cconj(A[q]), U[(i + 1) * nb + j]);
+      q += i + 2;
+    }
+    if (i < K) cfma(a0, cconj(A[q]), U[i * nb + j]);
+    Wm[e] = make_double2(a0.x + a1.x, a0.y + a1.y);
   }
   __syncthreads();
-  if (tid == 0) {  // in-place Gauss-Jordan of the nb x nb HPD capacitance matrix
+  {  // C = I + U^H W: one warp per entry, lanes split the K-sum, shuffle reduction
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int e = warp; e < nb * nb; e += nw) {
+      const int a = e / nb, b = e - a * nb;
+      double ax = 0, ay = 0;
+      for (int k = lane; k < K; k += 32) {
+        const C u = U[k * nb + a], w = Wm[k * nb + b];
+        ax += u.x * w.x + u.y * w.y;  // conj(u) w
+        ay += u.x * w.y - u.y * w.x;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ax += __shfl_xor_sync(0xffffffffu, ax, o);
+        ay += __shfl_xor_sync(0xffffffffu, ay, o);
+      }
+      if (lane == 0) Cm[e] = make_double2(ax + (a == b ? 1.0 : 0.0), ay);
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {  // in-place Gauss-Jordan of the nb x nb HPD capacitance matrix, one warp
+    constexpr int PER = 8;  // entries per lane (nb <= 16)
     for (int k = 0; k < nb; ++k) {
       const double d = Cm[k * nb + k].x;
-      if (!(d > 0)) atomicCAS(info, 0, p + 1);
+      if (tid == 0 && !(d > 0)) atomicCAS(info, 0, p + 1);
       const double pinv = 1.0 / d;
-      for (int j = 0; j < nb; ++j) Cm[k * nb + j] = cscale(Cm[k * nb + j], pinv);
-      Cm[k * nb + k] = make_double2(pinv, 0);
-      for (int i = 0; i < nb; ++i) {
-        if (i == k) continue;
-        const C f = Cm[i * nb + k];
-        for (int j = 0; j < nb; ++j) {
-          if (j == k) continue;
-          const C r = Cm[k * nb + j];
-          Cm[i * nb + j] = make_double2(Cm[i * nb + j].x - (f.x * r.x - f.y * r.y),
-                                        Cm[i * nb + j].y - (f.x * r.y + f.y * r.x));
-        }
-        Cm[i * nb + k] = make_double2(-(f.x * pinv), -(f.y * pinv));
+      C nv[PER];
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int e = tid + 32 * r;
+        if (e >= nb * nb) break;
+        const int i = e / nb, j = e - i * nb;
+        const C cij = Cm[e], cik = Cm[i * nb + k], ckj = Cm[k * nb + j];
+        if (i == k && j == k) nv[r] = make_double2(pinv, 0);
+        else if (i == k) nv[r] = cscale(ckj, pinv);
+        else if (j == k) nv[r] = cscale(cik, -pinv);
+        else nv[r] = make_double2(cij.x - pinv * (cik.x * ckj.x - cik.y * ckj.y),
+                                  cij.y - pinv * (cik.x * ckj.y + cik.y * ckj.x));
       }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int e = tid + 32 * r;
+        if (e >= nb * nb) break;
+        Cm[e] = nv[r];
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -533,7 +564,7 @@ extern "C" size_t ocsc_history_woodbury_smem(int K, int nb) {
 extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, const void* inv_in,
                                      const void* z, int64_t z_sb, int64_t z_sk, int64_t z_sp, void* out,
                                      int32_t* info, void* stream) {
-  if (K <= 0 || nfreq < 0 || nb < 0 || nb > 32) return fail(OCSC_ESHAPE, "history_woodbury: bad extents (nb <= 32)");
+  if (K <= 0 || nfreq < 0 || nb < 0 || nb > 16) return fail(OCSC_ESHAPE, "history_woodbury: bad extents (nb <= 16)");
   cudaStream_t s = as_stream(stream);
   OCSC_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (nfreq == 0) return OCSC_OK;
@@ -543,7 +574,7 @@ extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfre
   do {                                                                                                         \
     OCSC_CUDA(cudaFuncSetAttribute(k_hist_woodbury<TZ, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                    (int)sm));                                                                  \
-    k_hist_woodbury<TZ, TO><<<nfreq, 256, sm, s>>>(K, nb, (const double2*)inv_in,                               \
+    k_hist_woodbury<TZ, TO><<<nfreq, 512, sm, s>>>(K, nb, (const double2*)inv_in,                               \
                                                    (const typename Cx<TZ>::type*)z, z_sb, z_sk, z_sp,           \
                                                    (typename Cx<TO>::type*)out, info);                         \
   } while (0)

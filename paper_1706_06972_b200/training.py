@@ -228,7 +228,7 @@ class OnlineTrainer:
 
     def _split_plan(self, B: int) -> int:
         """b_main when the fused plan codes B samples on two cluster shapes (main waves + a tail
-        of <= 32 samples) and the history inverse can overlap the tail; 0 otherwise."""
+        of <= 16 samples) and the history inverse can overlap the tail; 0 otherwise."""
         key = ("split", B)
         if key not in self._fused_ok:
             info = (ctypes.c_int32 * 8)()
@@ -236,7 +236,7 @@ class OnlineTrainer:
             lib.ocsc_code_fused_info(_lib.code(self.dtype), self.H, self.W, self.K, B, info)
             b1 = int(info[5])
             h = self.history
-            ok = (self.config.overlap and 0 < b1 < B and B - b1 <= 32 and info[6] > 0
+            ok = (self.config.overlap and 0 < b1 < B and B - b1 <= 16 and info[6] > 0
                   and type(self)._fold is OnlineTrainer._fold and h.solver == "gj"
                   and h.S.dtype == torch.complex128
                   and lib.ocsc_history_woodbury_smem(self.K, B - b1) <= 227 * 1024)
@@ -296,11 +296,13 @@ class OnlineTrainer:
         """Main stream: fold the tail samples into S', Woodbury-refresh the inverse, adopt S'/c'."""
         h, nf, K, sd = self.history, self.nf, self.K, self._side
         torch.cuda.current_stream().wait_event(side_done)
+        self._mark("fold start")
         nb = B - b1
         ce = uh.element_size()
         _lib.call("ocsc_history_accumulate", _lib.code(uh.dtype), _lib.code(h.S.dtype), K, nf, nb,
                   uh.data_ptr() + b1 * K * nf * ce, K * nf, nf, 1, xh.data_ptr() + b1 * nf * xh.element_size(),
                   nf, 1, _lib.ptr(sd["S"]), _lib.ptr(sd["c"]), _lib.stream())
+        self._mark("tail accumulated")
         if h._inv is None:
             h._inv = torch.empty(h.S.shape, dtype=h.inv_dtype, device=h.S.device)
         _lib.call("ocsc_history_woodbury", _lib.code(uh.dtype), _lib.code(h.inv_dtype), K, nf, nb, _lib.ptr(sd["inv"]),
@@ -311,6 +313,7 @@ class OnlineTrainer:
         h.count += B
         h._inv_count = h.count  # (the hot path's row solves run with check=False, as before)
         self._mark("fold end")
+        # (the rest of the step: J row-solve + projection rounds, den)
 
     def _load(self, X) -> tuple[torch.Tensor, int]:
         P = self.shape.size
@@ -414,6 +417,7 @@ class OnlineTrainer:
         else:
             self._fold(uh, xh, B)
         self._dictionary_update()
+        self._mark("dict end")
         track = self.config.stop_tol > 0
         if track:
             self._track_changes(buf.u[B - 1])
