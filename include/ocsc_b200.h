@@ -125,6 +125,9 @@ int ocsc_debug_fused_profile(void* buf);
 int ocsc_debug_plane_profile(void* buf);   /* debug: clock64 phase stamps of the plane-resident stream kernel */
 /* Development aid: device buffer of 2*B int64 receiving %globaltimer at each sample's start/end. */
 int ocsc_debug_fused_timeline(void* buf);
+/* Development aid: device buffer of 1024 int64: %globaltimer (first 512) and clock64 (last 512)
+ * at the start of each of the first 512 iterations of CTA 0 of the next fused launches. */
+int ocsc_debug_fused_iterations(void* buf);
 int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh,
                     const void* den, double beta, double rho, int max_iters, double rel_tol,
                     void* u, void* t, void* uh, double* obj, double* resid, int32_t* iters,

@@ -47,6 +47,7 @@ SIGNATURES = {
     "ocsc_code_fused_info": [_I, _I, _I, _I, _I, _P],
     "ocsc_debug_fused_profile": [_P],
     "ocsc_debug_plane_profile": [_P],
+    "ocsc_debug_fused_iterations": [_P],
     "ocsc_debug_fused_timeline": [_P],
     "ocsc_code_fused": [_I, _I, _I, _I, _I, _P, _P, _P, _D, _D, _I, _D, _P, _P, _P, _P, _P, _P, _P, _P],
     "ocsc_code_stream_supported": [_I, _I, _I],

@@ -38,6 +38,7 @@ namespace ocsc {
 // optional phase timestamps (development aid): CTA 0, thread 0, iterations 8..15
 __device__ long long* g_fused_prof = nullptr;
 __device__ long long* g_fused_timeline = nullptr;  // [sample][2]: globaltimer at start / end (CTA rank 0)
+__device__ long long* g_fused_iter = nullptr;      // [2][512]: globaltimer / clock64 at each iteration (CTA 0)
 __device__ __forceinline__ long long global_ns() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -318,11 +319,16 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   };
 
   int it = 0, stat = 0;
-  long long* prof = (blockIdx.x == 0 && tid == 0) ? g_fused_prof : nullptr;
+  long long* prof = (blockIdx.x == 0 && a.b0 == 0 && tid == 0) ? g_fused_prof : nullptr;
   long long* tl = (r == 0 && tid == 0) ? g_fused_timeline : nullptr;
   if (tl) tl[2 * b] = global_ns();
+  long long* itl = (blockIdx.x == 0 && a.b0 == 0 && tid == 0) ? g_fused_iter : nullptr;
   for (;;) {
     const int pit = it;
+    if (itl && it < 512) {
+      itl[it] = global_ns();
+      itl[512 + it] = clock64();
+    }
     // ---- A: forward column transforms times D, partial synthesis ------------------------
     OCSC_STAMP(0);
     col_phase(std::integral_constant<int, COL_F>{}, nullptr);
@@ -432,6 +438,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   }
 
   // ---- outputs: U = S(w) (and t), F(U), objective -------------------------------------------
+  if (itl) itl[505] = global_ns();
   double l1 = 0.0;
   if (rvalid) {
     const int64_t rowoff = (((int64_t)b * K + k0 + rj) * N + rq) * N;
@@ -457,10 +464,13 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     row_forward_post<C, N>(z, xrow);
   }
   __syncthreads();
+  if (itl) itl[506] = global_ns();
   col_phase(std::integral_constant<int, COL_FE>{}, a.uh_out + ((int64_t)b * K + k0) * NF);
   __syncthreads();
+  if (itl) itl[507] = global_ns();
   reduce_push();
   cl.sync();
+  if (itl) itl[508] = global_ns();
   double e = 0.0;
   {
     const int f0 = r * slice, f1 = min(NF, f0 + slice);
@@ -479,6 +489,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     dst[1] = ev[1];
   }
   cl.sync();
+  if (itl) itl[509] = global_ns();
   if (r == 0 && tid == 0) {
     double energy = 0.0, l1s = 0.0;
     for (int qq = 0; qq < CS; ++qq) {
@@ -675,6 +686,12 @@ using namespace ocsc;
 extern "C" int ocsc_debug_fused_profile(void* buf) {
   long long* p = reinterpret_cast<long long*>(buf);
   OCSC_CUDA(cudaMemcpyToSymbol(g_fused_prof, &p, sizeof(p)));
+  return OCSC_OK;
+}
+
+extern "C" int ocsc_debug_fused_iterations(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  OCSC_CUDA(cudaMemcpyToSymbol(g_fused_iter, &p, sizeof(p)));
   return OCSC_OK;
 }
 

@@ -8,23 +8,27 @@ c = O.CONFIGS[1]; B = 50
 X = O.synth_images(B, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B, -1)
 tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)), ob.TrainConfig(n_filters=100, rho_dict=1.0, dtype="float32", batch_size=B, stop_tol=0.0))
 tr.partial_fit(X)
-buf = torch.zeros(64, dtype=torch.int64, device="cuda")
-_lib.call("ocsc_debug_fused_profile", buf.data_ptr())
-tr.partial_fit(X); torch.cuda.synchronize()
-_lib.call("ocsc_debug_fused_profile", None)
-t = buf.cpu().numpy().reshape(8, 8)
-names = ["colF", "reduce+cs1", "exchange+decide", "(it++)", "cs2", "colI+row", "norm-push+sync"]
-d = np.diff(t, axis=1)
-print("cycles per phase (median over iters 8..14):")
-for i, n in enumerate(names): print(f"  {n:12s} {int(np.median(d[:7, i]))}")
-print("  iteration  ", int(np.median(np.diff(t[:, 0]))))
-# wall-clock of the fused launch alone (events) to convert cycles -> time
 from paper_1706_06972_b200.transforms import rfft2_dev
 xs = torch.as_tensor(X.reshape(B, 42, 42), dtype=torch.float32).cuda()
 xh = rfft2_dev(xs, tr.shape)
 buf = tr._buf
 obj = torch.empty(B, dtype=torch.float64, device="cuda")
 cc = tr.coding_config
+pbuf = torch.zeros(64, dtype=torch.int64, device="cuda")
+_lib.call("ocsc_debug_fused_profile", pbuf.data_ptr())
+# one direct launch of the whole batch (its own plan: main waves + tail, b0 = 0 for the main)
+_lib.call("ocsc_code_fused", 4, 42, 42, 100, B, xh.data_ptr(), tr.Wh.data_ptr(), tr.den.data_ptr(), cc.beta, cc.rho,
+          cc.max_iters, cc.rel_tol, buf.u.data_ptr(), None, tr._uh.data_ptr(), obj.data_ptr(), None,
+          buf.iters.data_ptr(), buf.status.data_ptr(), _lib.stream())
+torch.cuda.synchronize()
+_lib.call("ocsc_debug_fused_profile", None)
+t = pbuf.cpu().numpy().reshape(8, 8)
+names = ["colF", "reduce+cs1", "exchange+decide", "(it++)", "cs2", "colI+row", "norm-push+sync"]
+d = np.diff(t, axis=1)
+print("cycles per phase (median over iters 8..14):")
+for i, n in enumerate(names): print(f"  {n:12s} {int(np.median(d[:7, i]))}")
+print("  iteration  ", int(np.median(np.diff(t[:, 0]))))
+# wall-clock of the fused launch alone (events) to convert cycles -> time
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for rep in range(3):
     e0.record()
@@ -46,3 +50,24 @@ t = tlb.cpu().numpy().reshape(B, 2).astype(np.float64)
 t -= t[:, 0].min()
 for b in range(B):
     print(f"sample {b:2d}: start {t[b,0]/1e6:7.3f} ms  dur {(t[b,1]-t[b,0])/1e6:6.3f} ms")
+# per-iteration wall time and SM clock rate of CTA 0 (globaltimer vs clock64)
+itb = torch.zeros(1024, dtype=torch.int64, device="cuda")
+_lib.call("ocsc_debug_fused_iterations", itb.data_ptr())
+_lib.call("ocsc_code_fused", 4, 42, 42, 100, B, xh.data_ptr(), tr.Wh.data_ptr(), tr.den.data_ptr(), cc.beta, cc.rho,
+          cc.max_iters, cc.rel_tol, buf.u.data_ptr(), None, tr._uh.data_ptr(), obj.data_ptr(), None,
+          buf.iters.data_ptr(), buf.status.data_ptr(), _lib.stream())
+torch.cuda.synchronize()
+_lib.call("ocsc_debug_fused_iterations", None)
+a = itb.cpu().numpy().astype(np.float64)
+ns, ck = a[:300], a[512:812]
+dns, dck = np.diff(ns), np.diff(ck)
+print(f"iteration ns: median {np.median(dns):.0f} p10 {np.percentile(dns, 10):.0f} p90 {np.percentile(dns, 90):.0f} "
+      f"max {dns.max():.0f}; clock64/ns = {np.sum(dck) / np.sum(dns):.3f} GHz; iters 0-299 span {(ns[-1] - ns[0]) / 1e6:.3f} ms")
+for lo in range(0, 300, 50):
+    print(f"  iters {lo:3d}-{lo + 49:3d}: median {np.median(dns[lo:lo + 49]):.0f} ns, {np.median(dck[lo:lo + 49]):.0f} clk")
+allns = a[:512]
+last = int(np.nonzero(allns)[0].max())
+print(f"iterations recorded: {last + 1}; span all {(allns[last] - allns[0]) / 1e6:.3f} ms; "
+      f"timeline sample 0 dur {(t[0, 1] - t[0, 0]) / 1e6:.3f} ms")
+fin = a[505:510]
+print("final stage (ns after the last iteration start):", [int(x - allns[last]) for x in fin])
