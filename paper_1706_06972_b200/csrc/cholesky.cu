@@ -11,6 +11,8 @@
 // L stays in global memory (full K x K per frequency, lower triangle).  The dictionary row
 // solve then runs two blocked triangular solves per frequency and round:
 //   conj(d) = L^-H L^-1 (c + ridge conj(v - theta)).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "fft_small.cuh"
 #include "transforms.cuh"
@@ -247,6 +249,103 @@ __global__ void __launch_bounds__(128) k_chol_smem(int K, const cx<T>* __restric
     for (int j = tid; j <= i; j += nt) L[(int64_t)i * K + j] = A[i * LD + j];
 }
 
+// Register-resident right-looking Cholesky for K <= 96 (BASELINE config 4's K = 64): the
+// lower triangle is distributed over the CTA as 4 x 4 blocks, one block per thread (thread t ->
+// block (bi, bj), bi >= bj), for the whole factorisation.  Step j: the owners of column j
+// publish it unscaled (with the diagonal) into a double-buffered shared vector, ONE barrier,
+// then every thread scales / updates its own block: L_ij = a_ij / sqrt(d),
+// a_ik -= a_ij conj(a_kj) / d.  Shared traffic is O(K) per step; no global traffic besides
+// reading S and writing L once.
+template <int K>
+constexpr int chol_reg_threads() {
+  return ((K / 4) * (K / 4 + 1) / 2 + 31) / 32 * 32;
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_reg(const cx<T>* __restrict__ S, T ridge,
+                                                                     cx<T>* Lall, int32_t* info) {
+  using C = cx<T>;
+  constexpr int NB = K / 4, NTH = NB * (NB + 1) / 2;
+  __shared__ __align__(16) C col[2][K];
+  const int p = blockIdx.x, t = threadIdx.x;
+  const bool act = t < NTH;
+  int bi = 0, bj = 0;
+  if (act) {
+    bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while (bi * (bi + 1) / 2 > t) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    bj = t - bi * (bi + 1) / 2;
+  }
+  const int i0 = bi * 4, k0 = bj * 4;
+  const int64_t npk = (int64_t)K * (K + 1) / 2;
+  const C* Sp = S + (int64_t)p * npk;
+  C a[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int i = i0 + r, k = k0 + c;
+      C v = mkc<C>(0, 0);
+      if (act && i >= k) {
+        v = Sp[packed_index(i, k)];
+        if (i == k) v = mkc<C>(v.x + ridge, (T)0);
+      }
+      a[r][c] = v;
+    }
+  for (int j = 0; j < K; ++j) {
+    C* cb = col[j & 1];
+    if (act && bj == (j >> 2)) {  // publish the raw column j (rows >= j) of this block
+      static_for<0, 4>([&](auto Cc) {
+        constexpr int c = decltype(Cc)::value;
+        if ((j & 3) == c) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (i0 + r >= j) cb[i0 + r] = a[r][c];
+        }
+      });
+    }
+    __syncthreads();
+    T d = cb[j].x;
+    if (!(d > (T)0)) {
+      if (t == 0) atomicCAS(info, 0, p + 1);
+      d = (T)NAN;
+    }
+    if (!act || k0 + 3 < j) continue;  // this block is final
+    const T ljj = sqrt(d), inv = (T)1 / ljj, invd = (T)1 / d;
+    C ci[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) ci[r] = cb[min(i0 + r, K - 1)];
+    static_for<0, 4>([&](auto Cc) {
+      constexpr int c = decltype(Cc)::value;
+      const int k = k0 + c;
+      if (k == j) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = i0 + r;
+          if (i == j) a[r][c] = mkc<C>(ljj, (T)0);
+          else if (i > j) a[r][c] = cscale(a[r][c], inv);
+        }
+      } else if (k > j) {
+        const C rk = cb[k];
+        const C ck = mkc<C>(rk.x * invd, -rk.y * invd);  // conj(a_kj) / d
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (i0 + r >= k) {
+            a[r][c].x -= ci[r].x * ck.x - ci[r].y * ck.y;
+            a[r][c].y -= ci[r].x * ck.y + ci[r].y * ck.x;
+          }
+      }
+    });
+  }
+  if (!act) return;
+  C* L = Lall + (int64_t)p * K * K;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (i0 + r >= k0 + c) L[(int64_t)(i0 + r) * K + k0 + c] = a[r][c];
+}
+
 // conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)), one CTA (256 threads) per frequency,
 // blocked by 32.  Forward: y_b -= L_b,<b y_<b as a tile GEMV (thread = row r, 4 columns of every
 // tile to the left; all its tile loads issue back to back, 8 threads per row reduce by
@@ -381,6 +480,25 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
   const int nb = K / CT;
   const size_t cs = dtype_hist == OCSC_F64 ? 16 : 8;
   const size_t whole = cs * (size_t)K * (K + 1);
+#define OCSC_CHOL_REG(KK)                                                                                    \
+  if (K == KK) {                                                                                             \
+    if (dtype_hist == OCSC_F32)                                                                              \
+      k_chol_reg<float, KK><<<nfreq, chol_reg_threads<KK>(), 0, s>>>((const float2*)S, (float)ridge,         \
+                                                                     (float2*)L, info);                     \
+    else if (dtype_hist == OCSC_F64)                                                                         \
+      k_chol_reg<double, KK><<<nfreq, chol_reg_threads<KK>(), 0, s>>>((const double2*)S, ridge,              \
+                                                                      (double2*)L, info);                   \
+    else                                                                                                     \
+      return fail(OCSC_EARG, "dtype must be 4 or 8");                                                        \
+    OCSC_LAUNCHED("k_chol_reg");                                                                             \
+    return OCSC_OK;                                                                                          \
+  }
+  if (!getenv("OCSC_CHOL_NOREG")) {  // dev knob: the shared-memory / blocked kernels instead
+    OCSC_CHOL_REG(32)
+    OCSC_CHOL_REG(64)
+    OCSC_CHOL_REG(96)  // (K = 128: one 544-thread CTA per SM, barrier-latency bound: the blocked kernel wins)
+  }
+#undef OCSC_CHOL_REG
   if (K <= 64) {  // small K: the whole matrix in one CTA's shared memory, many CTAs per SM
     const int threads = 64;
     if (dtype_hist == OCSC_F32) {

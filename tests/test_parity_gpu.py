@@ -492,7 +492,7 @@ def _dense_rowsolve(z, x, v, th, t_rho_p):
     return out
 
 
-@pytest.mark.parametrize("K,solver", [(64, "chol"), (64, "gj"), (256, "chol"), (96, "chol")])
+@pytest.mark.parametrize("K,solver", [(64, "chol"), (64, "gj"), (256, "chol"), (96, "chol"), (32, "chol"), (128, "chol")])
 def test_history_solvers_match_dense(K, solver):
     nfreq, B = 5, 12
     h, z, x = _random_history(K, nfreq, B, seed=K, solver=solver)
