@@ -174,10 +174,13 @@ int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfreq, const v
  * K x nb code spectra z element (b,k,p) at z[b*z_sb + k*z_sk + p*z_sp], nb <= 16; out packed as
  * dtype_out.  Lets a trainer invert S plus most of a mini-batch while the rest is still being
  * coded, then fold the remainder in O(K^2 nb) (no reference counterpart; same result as
- * ocsc_history_invert of the full sum).  info as ocsc_history_invert (capacitance matrix). */
+ * ocsc_history_invert of the full sum).  info as ocsc_history_invert (capacitance matrix).
+ * With S, c non-NULL (complex128 history sums) the same nb samples are folded into them in the
+ * same pass (x element (b,p) at x[b*x_sb + p*x_sp], dtype_z), as ocsc_history_accumulate would. */
 int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, const void* inv_in,
                           const void* z, int64_t z_sb, int64_t z_sk, int64_t z_sp, void* out,
-                          int32_t* info, void* stream);
+                          int32_t* info, const void* x, int64_t x_sb, int64_t x_sp, void* S, void* c,
+                          void* stream);
 size_t ocsc_history_woodbury_smem(int K, int nb);
 /* Large K (multiple of 32; BASELINE configs 3-4): blocked right-looking Cholesky of
  * S_p + ridge I per frequency (one CTA per frequency, 32x32 tiles, panel staged in shared

@@ -445,7 +445,8 @@ template <typename Tz, typename To>
 __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const double2* __restrict__ inv_in,
                                                          const typename Cx<Tz>::type* __restrict__ z, int64_t zb,
                                                          int64_t zk, int64_t zp, typename Cx<To>::type* out,
-                                                         int32_t* info) {
+                                                         int32_t* info, const typename Cx<Tz>::type* __restrict__ x,
+                                                         int64_t xb, int64_t xp, double2* S, double2* cvec) {
   using C = double2;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int p = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
@@ -543,6 +544,19 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
     X[e] = acc;
   }
   __syncthreads();
+  if (S) {  // fold the same samples into the history sums: c_p += sum_b conj(x_b) z_b
+    for (int k = tid; k < K; k += nt) {
+      C acc = cvec[(int64_t)p * K + k];
+      for (int m = 0; m < nb; ++m) {
+        const auto xv = x[m * xb + p * xp];
+        const C u = U[k * nb + m];
+        acc.x += (double)xv.x * u.x + (double)xv.y * u.y;
+        acc.y += (double)xv.x * u.y - (double)xv.y * u.x;
+      }
+      cvec[(int64_t)p * K + k] = acc;
+    }
+  }
+  double2* Sp = S ? S + (int64_t)p * npk : nullptr;
   typename Cx<To>::type* o = out + (int64_t)p * npk;
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
   for (int i = warp; i < K; i += nw)
@@ -554,6 +568,15 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
         acc.y -= x.y * w.x - x.x * w.y;
       }
       o[packed_index(i, j)] = ccast<To>(acc);
+      if (Sp) {  // S_p[i][j] += sum_m U[i][m] conj(U[j][m])
+        C sv = Sp[packed_index(i, j)];
+        for (int m = 0; m < nb; ++m) {
+          const C ui = U[i * nb + m], uj = U[j * nb + m];
+          sv.x += ui.x * uj.x + ui.y * uj.y;
+          sv.y += ui.y * uj.x - ui.x * uj.y;
+        }
+        Sp[packed_index(i, j)] = sv;
+      }
     }
 }
 
@@ -563,8 +586,10 @@ extern "C" size_t ocsc_history_woodbury_smem(int K, int nb) {
 
 extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, const void* inv_in,
                                      const void* z, int64_t z_sb, int64_t z_sk, int64_t z_sp, void* out,
-                                     int32_t* info, void* stream) {
+                                     int32_t* info, const void* x, int64_t x_sb, int64_t x_sp, void* S, void* c,
+                                     void* stream) {
   if (K <= 0 || nfreq < 0 || nb < 0 || nb > 16) return fail(OCSC_ESHAPE, "history_woodbury: bad extents (nb <= 16)");
+  if ((S != nullptr) != (c != nullptr) || (S && !x)) return fail(OCSC_EARG, "history_woodbury: S, c and x go together");
   cudaStream_t s = as_stream(stream);
   OCSC_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (nfreq == 0) return OCSC_OK;
@@ -576,7 +601,9 @@ extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfre
                                    (int)sm));                                                                  \
     k_hist_woodbury<TZ, TO><<<nfreq, 512, sm, s>>>(K, nb, (const double2*)inv_in,                               \
                                                    (const typename Cx<TZ>::type*)z, z_sb, z_sk, z_sp,           \
-                                                   (typename Cx<TO>::type*)out, info);                         \
+                                                   (typename Cx<TO>::type*)out, info,                          \
+                                                   (const typename Cx<TZ>::type*)x, x_sb, x_sp, (double2*)S,    \
+                                                   (double2*)c);                                               \
   } while (0)
   if (dtype_z == OCSC_F32 && dtype_out == OCSC_F32) OCSC_WB(float, float);
   else if (dtype_z == OCSC_F32 && dtype_out == OCSC_F64) OCSC_WB(float, double);

@@ -299,14 +299,12 @@ class OnlineTrainer:
         self._mark("fold start")
         nb = B - b1
         ce = uh.element_size()
-        _lib.call("ocsc_history_accumulate", _lib.code(uh.dtype), _lib.code(h.S.dtype), K, nf, nb,
-                  uh.data_ptr() + b1 * K * nf * ce, K * nf, nf, 1, xh.data_ptr() + b1 * nf * xh.element_size(),
-                  nf, 1, _lib.ptr(sd["S"]), _lib.ptr(sd["c"]), _lib.stream())
-        self._mark("tail accumulated")
         if h._inv is None:
             h._inv = torch.empty(h.S.shape, dtype=h.inv_dtype, device=h.S.device)
+        # one pass: Woodbury refresh of the inverse with the tail samples + their fold into S', c'
         _lib.call("ocsc_history_woodbury", _lib.code(uh.dtype), _lib.code(h.inv_dtype), K, nf, nb, _lib.ptr(sd["inv"]),
                   uh.data_ptr() + b1 * K * nf * ce, K * nf, nf, 1, _lib.ptr(h._inv), _lib.ptr(sd["info"][1:]),
+                  xh.data_ptr() + b1 * nf * xh.element_size(), nf, 1, _lib.ptr(sd["S"]), _lib.ptr(sd["c"]),
                   _lib.stream())
         h.S, sd["S"] = sd["S"], h.S
         h.c, sd["c"] = sd["c"], h.c

@@ -13,7 +13,12 @@ inv = torch.randn(nf, npk, dtype=torch.complex128, device="cuda")
 z = torch.randn(nb, K, nf, dtype=torch.complex64, device="cuda")
 out = torch.empty(nf, npk, dtype=torch.complex64, device="cuda")
 info = torch.zeros(1, dtype=torch.int32, device="cuda")
+S = torch.zeros(nf, npk, dtype=torch.complex128, device="cuda")
+c = torch.zeros(nf, K, dtype=torch.complex128, device="cuda")
+x = torch.randn(nb, nf, dtype=torch.complex64, device="cuda")
+fold = len(sys.argv) > 2
 args = (_lib.F32, _lib.F32, K, nf, nb, _lib.ptr(inv), _lib.ptr(z), K * nf, nf, 1, _lib.ptr(out), _lib.ptr(info),
+        _lib.ptr(x) if fold else None, nf, 1, _lib.ptr(S) if fold else None, _lib.ptr(c) if fold else None,
         _lib.stream())
 for _ in range(3):
     _lib.call("ocsc_history_woodbury", *args)

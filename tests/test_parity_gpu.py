@@ -429,7 +429,7 @@ def test_woodbury_refresh_matches_direct_inverse():
     out = torch.empty(nf, K * (K + 1) // 2, dtype=torch.complex128, device="cuda")
     info = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("ocsc_history_woodbury", _lib.F32, _lib.F64, K, nf, nb, _lib.ptr(inv_a), _lib.ptr(z), K * nf, nf, 1,
-              _lib.ptr(out), _lib.ptr(info), _lib.stream())
+              _lib.ptr(out), _lib.ptr(info), None, 0, 0, None, None, _lib.stream())
     U = z.to(torch.complex128).permute(2, 1, 0)  # (p, k, b)
     want = torch.linalg.inv(A + U @ U.conj().transpose(1, 2))[:, ii, jj]
     assert int(info.item()) == 0
