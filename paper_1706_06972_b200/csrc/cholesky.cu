@@ -249,32 +249,37 @@ __global__ void __launch_bounds__(128) k_chol_smem(int K, const cx<T>* __restric
     for (int j = tid; j <= i; j += nt) L[(int64_t)i * K + j] = A[i * LD + j];
 }
 
-// Register-resident right-looking Cholesky for K <= 96 (BASELINE config 4's K = 64): the
-// lower triangle is distributed over the CTA as 4 x 4 blocks, one block per thread (thread t ->
-// block (bi, bj), bi >= bj), for the whole factorisation.  Step j: the owners of column j
-// publish it unscaled (with the diagonal) into a double-buffered shared vector, ONE barrier,
-// then every thread scales / updates its own block: L_ij = a_ij / sqrt(d),
-// a_ik -= a_ij conj(a_kj) / d.  Shared traffic is O(K) per step; no global traffic besides
-// reading S and writing L once.
 template <int K>
 constexpr int chol_reg_threads() {
   return ((K / 4) * (K / 4 + 1) / 2 + 31) / 32 * 32;
 }
 
+// Register-resident BLOCKED right-looking Cholesky (K <= 128): thread t owns the 4 x 4 block
+// (bi, bj), bi >= bj, for the whole factorisation; one step per 4-wide block column kb:
+//   1. the owner of (kb, kb) factors its block in registers and publishes L_kk;      barrier
+//   2. the owners of (bi, kb), bi > kb, solve X L_kk^H = A_{bi,kb} in registers and publish X
+//      into a parity-double-buffered panel;                                          barrier
+//   3. every trailing owner (bj > kb) applies A_{bi,bj} -= X_bi X_bj^H (64 complex FMAs).
+// Two barriers per 4 columns (vs one per column for k_chol_reg) and a rank-4 update per thread.
 template <typename T, int K>
-__global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_reg(const cx<T>* __restrict__ S, T ridge,
-                                                                     cx<T>* Lall, int32_t* info) {
+__global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_rb(const cx<T>* __restrict__ S, T ridge,
+                                                                    cx<T>* Lall, int32_t* info) {
   using C = cx<T>;
   constexpr int NB = K / 4, NTH = NB * (NB + 1) / 2;
-  __shared__ __align__(16) C col[2][K];
+  __shared__ __align__(16) C Lkk[4][4];
+  __shared__ __align__(16) C P[2][4][4][NB];  // element-major: lanes (consecutive blocks) hit consecutive words
   const int p = blockIdx.x, t = threadIdx.x;
   const bool act = t < NTH;
+  // column-major block order: the blocks of early (finished) block columns are contiguous, so
+  // whole warps retire from the trailing updates instead of running partially masked
   int bi = 0, bj = 0;
   if (act) {
-    bi = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-    while (bi * (bi + 1) / 2 > t) --bi;
-    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-    bj = t - bi * (bi + 1) / 2;
+    int off = 0;
+    while (off + (NB - bj) <= t) {
+      off += NB - bj;
+      ++bj;
+    }
+    bi = bj + (t - off);
   }
   const int i0 = bi * 4, k0 = bj * 4;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
@@ -292,51 +297,86 @@ __global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_reg(const cx<T>*
       }
       a[r][c] = v;
     }
-  for (int j = 0; j < K; ++j) {
-    C* cb = col[j & 1];
-    if (act && bj == (j >> 2)) {  // publish the raw column j (rows >= j) of this block
-      static_for<0, 4>([&](auto Cc) {
-        constexpr int c = decltype(Cc)::value;
-        if ((j & 3) == c) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (i0 + r >= j) cb[i0 + r] = a[r][c];
+  bool bad = false;
+  for (int kb = 0; kb < NB; ++kb) {
+    // ---- 1. diagonal block ----
+    if (act && bi == kb && bj == kb) {
+      static_for<0, 4>([&](auto Jc) {
+        constexpr int j = decltype(Jc)::value;
+        T d = a[j][j].x;
+        if (!(d > (T)0)) {
+          bad = true;
+          d = (T)NAN;
         }
+        const T ljj = sqrt(d), inv = (T)1 / ljj;
+        a[j][j] = mkc<C>(ljj, (T)0);
+        static_for<j + 1, 4>([&](auto Rr) { a[decltype(Rr)::value][j] = cscale(a[decltype(Rr)::value][j], inv); });
+        static_for<j + 1, 4>([&](auto Cc) {
+          constexpr int c = decltype(Cc)::value;
+          const C lc = a[c][j];
+          static_for<c, 4>([&](auto Rr) {  // a[r][c] -= L[r][j] conj(L[c][j])
+            constexpr int r = decltype(Rr)::value;
+            a[r][c].x -= a[r][j].x * lc.x + a[r][j].y * lc.y;
+            a[r][c].y -= a[r][j].y * lc.x - a[r][j].x * lc.y;
+          });
+        });
       });
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Lkk[r][c] = a[r][c];
     }
     __syncthreads();
-    T d = cb[j].x;
-    if (!(d > (T)0)) {
-      if (t == 0) atomicCAS(info, 0, p + 1);
-      d = (T)NAN;
-    }
-    if (!act || k0 + 3 < j) continue;  // this block is final
-    const T ljj = sqrt(d), inv = (T)1 / ljj, invd = (T)1 / d;
-    C ci[4];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) ci[r] = cb[min(i0 + r, K - 1)];
-    static_for<0, 4>([&](auto Cc) {
-      constexpr int c = decltype(Cc)::value;
-      const int k = k0 + c;
-      if (k == j) {
+    C (*Pb)[4][NB] = P[kb & 1];
+    // ---- 2. panel: X L_kk^H = A (columns in order) ----
+    if (act && bj == kb && bi > kb) {
+      static_for<0, 4>([&](auto Cc) {
+        constexpr int c = decltype(Cc)::value;
+        const T inv = (T)1 / Lkk[c][c].x;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const int i = i0 + r;
-          if (i == j) a[r][c] = mkc<C>(ljj, (T)0);
-          else if (i > j) a[r][c] = cscale(a[r][c], inv);
+          C x = a[r][c];
+          static_for<0, c>([&](auto Mm) {  // x -= X[r][m] conj(L_kk[c][m])
+            constexpr int m = decltype(Mm)::value;
+            const C l = Lkk[c][m];
+            x.x -= a[r][m].x * l.x + a[r][m].y * l.y;
+            x.y -= a[r][m].y * l.x - a[r][m].x * l.y;
+          });
+          a[r][c] = cscale(x, inv);
         }
-      } else if (k > j) {
-        const C rk = cb[k];
-        const C ck = mkc<C>(rk.x * invd, -rk.y * invd);  // conj(a_kj) / d
+      });
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (i0 + r >= k) {
-            a[r][c].x -= ci[r].x * ck.x - ci[r].y * ck.y;
-            a[r][c].y -= ci[r].x * ck.y + ci[r].y * ck.x;
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Pb[r][c][bi] = a[r][c];
+    }
+    __syncthreads();
+    // ---- 3. trailing: A_{bi,bj} -= X_bi X_bj^H ----
+    if (act && bj > kb) {
+      C xi[4][4], xj[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          xi[r][m] = Pb[r][m][bi];
+          xj[r][m] = Pb[r][m][bj];
+        }
+      // a -= xi conj(xj) as two 2-wide FMAs: a += xi * (-xj.x) + (-xi.y, xi.x) * xj.y
+      // (diagonal blocks also update their upper part: never stored)
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const C xs = mkc<C>(-xi[r][m].y, xi[r][m].x);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            a[r][c] = vfma(xi[r][m], vsplat<C>(-xj[c][m].x), a[r][c]);
+            a[r][c] = vfma(xs, vsplat<C>(xj[c][m].y), a[r][c]);
           }
-      }
-    });
+        }
+    }
   }
+  if (bad) atomicCAS(info, 0, p + 1);
   if (!act) return;
   C* L = Lall + (int64_t)p * K * K;
 #pragma unroll
@@ -483,20 +523,21 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
 #define OCSC_CHOL_REG(KK)                                                                                    \
   if (K == KK) {                                                                                             \
     if (dtype_hist == OCSC_F32)                                                                              \
-      k_chol_reg<float, KK><<<nfreq, chol_reg_threads<KK>(), 0, s>>>((const float2*)S, (float)ridge,         \
-                                                                     (float2*)L, info);                     \
+      k_chol_rb<float, KK><<<nfreq, chol_reg_threads<KK>(), 0, s>>>((const float2*)S, (float)ridge,          \
+                                                                    (float2*)L, info);                      \
     else if (dtype_hist == OCSC_F64)                                                                         \
-      k_chol_reg<double, KK><<<nfreq, chol_reg_threads<KK>(), 0, s>>>((const double2*)S, ridge,              \
-                                                                      (double2*)L, info);                   \
+      k_chol_rb<double, KK><<<nfreq, chol_reg_threads<KK>(), 0, s>>>((const double2*)S, ridge,               \
+                                                                     (double2*)L, info);                    \
     else                                                                                                     \
       return fail(OCSC_EARG, "dtype must be 4 or 8");                                                        \
-    OCSC_LAUNCHED("k_chol_reg");                                                                             \
+    OCSC_LAUNCHED("k_chol_rb");                                                                              \
     return OCSC_OK;                                                                                          \
   }
   if (!getenv("OCSC_CHOL_NOREG")) {  // dev knob: the shared-memory / blocked kernels instead
     OCSC_CHOL_REG(32)
     OCSC_CHOL_REG(64)
-    OCSC_CHOL_REG(96)  // (K = 128: one 544-thread CTA per SM, barrier-latency bound: the blocked kernel wins)
+    OCSC_CHOL_REG(96)
+    OCSC_CHOL_REG(128)
   }
 #undef OCSC_CHOL_REG
   if (K <= 64) {  // small K: the whole matrix in one CTA's shared memory, many CTAs per SM

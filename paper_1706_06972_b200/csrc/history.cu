@@ -424,8 +424,12 @@ __global__ void __launch_bounds__(128) k_rowsolve(int K, int nf, const cx<Ti>* _
   for (int j = threadIdx.x; j < K; j += blockDim.x) {
     C acc = mkc<C>(0, 0);
     const cx<Ti>* row = Ap + packed_index(j, 0);
+    C acc2 = mkc<C>(0, 0);  // second chain: loads of both loops issue 8 ahead
+#pragma unroll 8
     for (int k = 0; k <= j; ++k) cfma(acc, ccast<Th>(row[k]), rhs[k]);
-    for (int k = j + 1; k < K; ++k) cfmac(acc, ccast<Th>(Ap[packed_index(k, j)]), rhs[k]);
+#pragma unroll 8
+    for (int k = j + 1; k < K; ++k) cfmac(acc2, ccast<Th>(Ap[packed_index(k, j)]), rhs[k]);
+    acc = cadd(acc, acc2);
     Dh[(int64_t)j * sk + (int64_t)p * sp] = mkc<cx<Tc>>((Tc)acc.x, (Tc)-acc.y);
   }
 }
