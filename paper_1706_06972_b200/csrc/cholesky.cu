@@ -260,7 +260,7 @@ constexpr int chol_reg_threads() {
 //   2. the owners of (bi, kb), bi > kb, solve X L_kk^H = A_{bi,kb} in registers and publish X
 //      into a parity-double-buffered panel;                                          barrier
 //   3. every trailing owner (bj > kb) applies A_{bi,bj} -= X_bi X_bj^H (64 complex FMAs).
-// Two barriers per 4 columns (vs one per column for k_chol_reg) and a rank-4 update per thread.
+// Two barriers per 4 columns and a rank-4 update per thread.
 template <typename T, int K>
 __global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_rb(const cx<T>* __restrict__ S, T ridge,
                                                                     cx<T>* Lall, int32_t* info) {
