@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_rb(const cx<T>* 
   using C = cx<T>;
   constexpr int NB = K / 4, NTH = NB * (NB + 1) / 2;
   __shared__ __align__(16) C Lkk[4][4];
+  __shared__ T Ldinv[4];  // 1 / L_kk[c][c]
   __shared__ __align__(16) C P[2][4][4][NB];  // element-major: lanes (consecutive blocks) hit consecutive words
   const int p = blockIdx.x, t = threadIdx.x;
   const bool act = t < NTH;
@@ -308,8 +309,17 @@ __global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_rb(const cx<T>* 
           bad = true;
           d = (T)NAN;
         }
-        const T ljj = sqrt(d), inv = (T)1 / ljj;
+        T ljj, inv;
+        if constexpr (sizeof(T) == 4) {  // one MUFU rsqrt + a Newton step (< 1 ulp off IEEE)
+          const T y = rsqrtf(d);
+          inv = y * ((T)1.5 - (T)0.5 * d * y * y);
+          ljj = d * inv;
+        } else {
+          ljj = sqrt(d);
+          inv = (T)1 / ljj;
+        }
         a[j][j] = mkc<C>(ljj, (T)0);
+        Ldinv[j] = inv;
         static_for<j + 1, 4>([&](auto Rr) { a[decltype(Rr)::value][j] = cscale(a[decltype(Rr)::value][j], inv); });
         static_for<j + 1, 4>([&](auto Cc) {
           constexpr int c = decltype(Cc)::value;
@@ -332,7 +342,7 @@ __global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_rb(const cx<T>* 
     if (act && bj == kb && bi > kb) {
       static_for<0, 4>([&](auto Cc) {
         constexpr int c = decltype(Cc)::value;
-        const T inv = (T)1 / Lkk[c][c].x;
+        const T inv = Ldinv[c];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           C x = a[r][c];
