@@ -436,11 +436,11 @@ def test_woodbury_refresh_matches_direct_inverse():
     assert rel(out.cpu().numpy(), want.cpu().numpy()) < 1e-12
 
 
-def test_overlapped_history_inverse_matches_serial_path():
+@pytest.mark.parametrize("B", [50, 47, 16])
+def test_overlapped_history_inverse_matches_serial_path(B):
     """Config-1 shapes: the tail-overlapped inverse (side-stream Gauss-Jordan of the main part +
     Woodbury refresh with the tail) trains like the serial accumulate-then-invert path."""
     c = O.CONFIGS[1]
-    B = 50
     X = O.synth_images(2 * B, c["dims0"], c["grid"], c["K0"], seed=21).reshape(2 * B, -1)
     kw = dict(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0, inner_iters=10)
     shape = ob.SignalShape(c["grid"], (11, 11))
