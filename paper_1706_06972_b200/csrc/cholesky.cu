@@ -89,51 +89,92 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, const cx<T>* __restr
   }
   __syncthreads();
 
+  // ---- diagonal tile kbx: warp 0, lane i holds row i of the tile ----
+  auto diag = [&](int kbx) {
+    C a[CT];
+    const C* row = L + (int64_t)(kbx * CT + lane) * K + kbx * CT;
+#pragma unroll
+    for (int j = 0; j < CT; ++j) a[j] = j <= lane ? row[j] : mkc<C>(0, 0);
+    static_for<0, CT>([&](auto J) {
+      constexpr int j = decltype(J)::value;
+      T d = __shfl_sync(0xffffffffu, a[j].x, j);
+      if (!(d > (T)0)) {
+        if (lane == 0) atomicCAS(info, 0, p + 1);
+        d = (T)NAN;
+      }
+      T ljj, inv;
+      if constexpr (sizeof(T) == 4) {  // one MUFU rsqrt + a Newton step (< 1 ulp off IEEE)
+        const T y = rsqrtf(d);
+        inv = y * ((T)1.5 - (T)0.5 * d * y * y);
+        ljj = d * inv;
+      } else {
+        ljj = sqrt(d);
+        inv = (T)1 / ljj;
+      }
+      if (lane == j) a[j] = mkc<C>(ljj, (T)0);
+      else if (lane > j) a[j] = cscale(a[j], inv);
+      if (lane == 0) dinv[j] = inv;
+      static_for<j + 1, CT>([&](auto Kk) {
+        constexpr int k = decltype(Kk)::value;
+        const T lx = __shfl_sync(0xffffffffu, a[j].x, k), ly = __shfl_sync(0xffffffffu, a[j].y, k);
+        if (lane >= k) {  // a[k] -= L[i][j] conj(L[k][j])
+          a[k].x -= a[j].x * lx + a[j].y * ly;
+          a[k].y -= a[j].y * lx - a[j].x * ly;
+        }
+      });
+    });
+    C* out = L + (int64_t)(kbx * CT + lane) * K + kbx * CT;
+#pragma unroll
+    for (int j = 0; j < CT; ++j) {
+      D[lane * LD + j] = a[j];
+      if (j <= lane) out[j] = a[j];
+    }
+  };
+  // ---- one warp's 8-row x 64-column strip of the trailing update A22 -= P P^H:
+  // 64 x 64 block pair (bi, bj), rows ty * 4.. of the pair with ty = 2 tp + lane / 16 ----
+  auto strip = [&](int r0, int R, int bi, int bj, int tp) {
+    const int ty = 2 * tp + (lane >> 4), tx = lane & 15;
+    const int i0 = bi * 64 + ty * 4, j0 = bj * 64 + tx * 4;  // trailing-local rows / cols
+    C acc[4][4], tgt[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // targets load while the products accumulate from zero
+        const int i = i0 + r, j = j0 + q;
+        tgt[r][q] = (i < R && j <= i) ? L[(int64_t)(r0 + i) * K + r0 + j] : mkc<C>(0, 0);
+        acc[r][q] = mkc<C>(0, 0);
+      }
+    if (i0 < R && j0 <= i0 + 3) {
+#pragma unroll 4
+      for (int k = 0; k < CT; ++k) {
+        // rows past R read panel slack: they only feed outputs that are never stored
+        C zi[4], zs[4], zj[4];
+        load4(PT + k * PR + i0, zi);
+        load4(PT + k * PR + j0, zj);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) zs[r] = mkc<C>(zi[r].y, -zi[r].x);
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cmac_conj2(acc[r][q], zi[r], zs[r], -zj[q].x, -zj[q].y);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = i0 + r, j = j0 + q;
+        if (i < R && j <= i) L[(int64_t)(r0 + i) * K + r0 + j] = cadd(tgt[r][q], acc[r][q]);
+      }
+  };
+  constexpr int NW = NT / 32;
+  __shared__ int ctr;
+
+  if (warp == 0) diag(0);
+  __syncthreads();
   for (int kb = 0; kb < nb; ++kb) {
     const int r0 = (kb + 1) * CT;  // first trailing row
     const int R = K - r0;          // trailing rows
-    // ---- diagonal tile: warp 0, lane i holds row i of the tile ----
-    if (warp == 0) {
-      C a[CT];
-      const C* row = L + (int64_t)(kb * CT + lane) * K + kb * CT;
-#pragma unroll
-      for (int j = 0; j < CT; ++j) a[j] = j <= lane ? row[j] : mkc<C>(0, 0);
-      static_for<0, CT>([&](auto J) {
-        constexpr int j = decltype(J)::value;
-        T d = __shfl_sync(0xffffffffu, a[j].x, j);
-        if (!(d > (T)0)) {
-          if (lane == 0) atomicCAS(info, 0, p + 1);
-          d = (T)NAN;
-        }
-        T ljj, inv;
-        if constexpr (sizeof(T) == 4) {  // one MUFU rsqrt + a Newton step (< 1 ulp off IEEE)
-          const T y = rsqrtf(d);
-          inv = y * ((T)1.5 - (T)0.5 * d * y * y);
-          ljj = d * inv;
-        } else {
-          ljj = sqrt(d);
-          inv = (T)1 / ljj;
-        }
-        if (lane == j) a[j] = mkc<C>(ljj, (T)0);
-        else if (lane > j) a[j] = cscale(a[j], inv);
-        if (lane == 0) dinv[j] = inv;
-        static_for<j + 1, CT>([&](auto Kk) {
-          constexpr int k = decltype(Kk)::value;
-          const T lx = __shfl_sync(0xffffffffu, a[j].x, k), ly = __shfl_sync(0xffffffffu, a[j].y, k);
-          if (lane >= k) {  // a[k] -= L[i][j] conj(L[k][j])
-            a[k].x -= a[j].x * lx + a[j].y * ly;
-            a[k].y -= a[j].y * lx - a[j].x * ly;
-          }
-        });
-      });
-      C* out = L + (int64_t)(kb * CT + lane) * K + kb * CT;
-#pragma unroll
-      for (int j = 0; j < CT; ++j) {
-        D[lane * LD + j] = a[j];
-        if (j <= lane) out[j] = a[j];
-      }
-    }
-    __syncthreads();
     if (R == 0) break;
     // ---- panel: x L_kk^H = a for every trailing row (thread per row) ----
     for (int rr = tid; rr < R; rr += NT) {
@@ -158,47 +199,26 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, const cx<T>* __restr
         PT[j * PR + rr] = x[j];
       }
     }
+    if (tid == 0) ctr = 0;
     __syncthreads();
-    // ---- trailing update A22 -= P P^H, 64 x 64 block pairs (bi >= bj) ----
+    // ---- lookahead: A. the first 64 trailing columns (next diagonal tile + next panel) ----
     const int nb64 = (R + 63) / 64;
-    const int half = tid >> 8, ty = (tid & 255) >> 4, tx = tid & 15;
-    for (int pr = half; pr < nb64 * (nb64 + 1) / 2; pr += NT / 256) {
-      int bi = (int)((sqrtf(8.0f * pr + 1.0f) - 1.0f) * 0.5f);
-      while (bi * (bi + 1) / 2 > pr) --bi;
-      while ((bi + 1) * (bi + 2) / 2 <= pr) ++bi;
-      const int bj = pr - bi * (bi + 1) / 2;
-      const int i0 = bi * 64 + ty * 4, j0 = bj * 64 + tx * 4;  // trailing-local rows / cols
-      C acc[4][4], tgt[4][4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {  // targets load while the products accumulate from zero
-          const int i = i0 + r, j = j0 + q;
-          tgt[r][q] = (i < R && j <= i) ? L[(int64_t)(r0 + i) * K + r0 + j] : mkc<C>(0, 0);
-          acc[r][q] = mkc<C>(0, 0);
-        }
-      if (i0 < R && j0 <= i0 + 3) {
-#pragma unroll 4
-        for (int k = 0; k < CT; ++k) {
-          // rows past R read panel slack: they only feed outputs that are never stored
-          C zi[4], zs[4], zj[4];
-          load4(PT + k * PR + i0, zi);
-          load4(PT + k * PR + j0, zj);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) zs[r] = mkc<C>(zi[r].y, -zi[r].x);
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cmac_conj2(acc[r][q], zi[r], zs[r], -zj[q].x, -zj[q].y);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int i = i0 + r, j = j0 + q;
-          if (i < R && j <= i) L[(int64_t)(r0 + i) * K + r0 + j] = cadd(tgt[r][q], acc[r][q]);
-        }
+    for (int sidx = warp; sidx < nb64 * 8; sidx += NW) strip(r0, R, sidx >> 3, 0, sidx & 7);
+    __syncthreads();
+    // ---- B. warp 0 factors the next diagonal tile while the other warps take the rest of the
+    // trailing update (64 x 64 block pairs with bj >= 1, 8 strips each, dynamic); warp 0 joins ----
+    if (warp == 0) diag(kb + 1);
+    const int nB = 8 * (nb64 * (nb64 - 1) / 2);
+    for (;;) {
+      int sidx = 0;
+      if (lane == 0) sidx = atomicAdd(&ctr, 1);
+      sidx = __shfl_sync(0xffffffffu, sidx, 0);
+      if (sidx >= nB) break;
+      const int q = sidx >> 3;
+      int b = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+      while (b * (b + 1) / 2 > q) --b;
+      while ((b + 1) * (b + 2) / 2 <= q) ++b;
+      strip(r0, R, b + 1, q - b * (b + 1) / 2 + 1, sidx & 7);
     }
     __syncthreads();
   }
