@@ -77,6 +77,7 @@ __host__ __device__ inline double seeded_uniform(uint64_t seed, double lo, doubl
 // ----------------------------------------------------------------------------- geometry --
 __host__ __device__ __forceinline__ int reflect_index(int i, int n) {
   // scipy.ndimage mode="reflect": period 2n, mirror about -0.5 and n-0.5
+  if (i >= -n && i < 2 * n) return i < 0 ? -1 - i : (i >= n ? 2 * n - 1 - i : i);  // one mirror at most
   const int p = 2 * n;
   int m = i % p;
   if (m < 0) m += p;
@@ -118,24 +119,23 @@ struct PrepArgs {
   uint64_t seed0;
   double sig_lo, sig_hi;  // PreprocessSpec.taper_sigma_range
   int flags;              // bit 0: LCN, bit 1: taper
+  const double* kg;       // Gaussian tables from k_prep_weights: LCN [s1], then taper [N][s2]
 };
 
 constexpr int T = 32;         // output tile edge
 constexpr int NT = 256;       // threads per CTA
 constexpr int MAXS = 64;      // largest kernel held in the shared weight table
 
-__device__ void gaussian_weights(double* k, int size, double sigma) {
+__device__ void gaussian_table(double* k, int size, double sigma) {
   // preprocessing.py:46-50: exp(-0.5 ((x - (size-1)/2) / sigma)^2) / sum
-  if (threadIdx.x == 0) {
-    const double half = (size - 1) / 2.0;
-    double sum = 0.0;
-    for (int t = 0; t < size; ++t) {
-      const double z = (t - half) / sigma;
-      k[t] = exp(-0.5 * (z * z));
-      sum += k[t];
-    }
-    for (int t = 0; t < size; ++t) k[t] /= sum;
+  const double half = (size - 1) / 2.0;
+  double sum = 0.0;
+  for (int t = 0; t < size; ++t) {
+    const double z = (t - half) / sigma;
+    k[t] = exp(-0.5 * (z * z));
+    sum += k[t];
   }
+  for (int t = 0; t < size; ++t) k[t] /= sum;
 }
 
 // acc[o] = sum_t k[t] * v[o + t], o < RB, over a strip whose values come from `load(u)`, u < RB+S-1
@@ -222,6 +222,19 @@ __host__ __device__ inline Plan make_plan(int H, int W, int s1, int s2, int flag
 inline size_t smem_bytes(const Plan& p) { return (size_t)p.nD * sizeof(double) + (size_t)p.nI * sizeof(int); }
 
 // S1/S2 > 0: compile-time kernel sizes (register-blocked strips); 0: runtime sizes.
+// Per-launch Gaussian tables (preprocessing.py:46-50): thread N builds the LCN kernel, thread
+// i < N the taper kernel of image i (its width from taper_sigmas or default_rng(seed0 + i)).
+__global__ void k_prep_weights(PrepArgs a, double* kg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool lcn = a.flags & 1, taper = a.flags & 2;
+  if (i == a.N && lcn) {
+    gaussian_table(kg, a.s1, a.sigma1);
+  } else if (i < a.N && taper) {
+    const double sg = a.sigma2 ? a.sigma2[i] : seeded_uniform(a.seed0 + (uint64_t)i, a.sig_lo, a.sig_hi);
+    gaussian_table(kg + a.s1 + (int64_t)i * a.s2, a.s2, sg);
+  }
+}
+
 template <typename Tin, typename Tout, int S1, int S2>
 __global__ void __launch_bounds__(NT) k_preprocess(const Tin* __restrict__ in, Tout* __restrict__ out, PrepArgs a) {
   extern __shared__ double sm[];
@@ -253,19 +266,9 @@ __global__ void __launch_bounds__(NT) k_preprocess(const Tin* __restrict__ in, T
   double* OT = MV + T * NP;  // Th x OP   blended output tile
 
   const int tid = threadIdx.x;
-  if (lcn) gaussian_weights(K1, s1, a.sigma1);
-  if (taper && tid == 32) {
-    const double sg = a.sigma2 ? a.sigma2[img] : seeded_uniform(a.seed0 + (uint64_t)img, a.sig_lo, a.sig_hi);
-    // weights built by one lane of warp 1 while warp 0 builds the LCN kernel
-    const double half = (s2 - 1) / 2.0;
-    double sum = 0.0;
-    for (int t = 0; t < s2; ++t) {
-      const double z = (t - half) / sg;
-      K2[t] = exp(-0.5 * (z * z));
-      sum += K2[t];
-    }
-    for (int t = 0; t < s2; ++t) K2[t] /= sum;
-  }
+  // Gaussian tables (built once per launch by k_prep_weights, not per tile)
+  if (lcn && tid < s1) K1[tid] = a.kg[tid];
+  if (taper && tid >= 32 && tid < 32 + s2) K2[tid - 32] = a.kg[s1 + (int64_t)img * s2 + (tid - 32)];
   for (int u = tid; u < L.Xh; u += NT) rowx[u] = reflect_index(L.Rlo - h1lo + u, H);
   for (int u = tid; u < L.Xw; u += NT) colx[u] = reflect_index(L.Clo - h1lo + u, W);
   if (taper) {
@@ -422,12 +425,18 @@ __global__ void __launch_bounds__(NT) k_preprocess(const Tin* __restrict__ in, T
 }
 
 template <typename Tin, typename Tout, int S1, int S2>
-int launch_k(const void* in, void* out, const PrepArgs& a, size_t bytes, cudaStream_t st) {
+int launch_k(const void* in, void* out, PrepArgs a, size_t bytes, cudaStream_t st) {
   auto kern = k_preprocess<Tin, Tout, S1, S2>;
   OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  double* kg = nullptr;  // stream-ordered scratch for the Gaussian tables
+  OCSC_CUDA(cudaMallocAsync((void**)&kg, sizeof(double) * ((size_t)a.s1 + (size_t)a.N * a.s2 + 1), st));
+  k_prep_weights<<<(a.N + 1 + 127) / 128, 128, 0, st>>>(a, kg);
+  OCSC_LAUNCHED("k_prep_weights");
+  a.kg = kg;
   dim3 grid((a.W + T - 1) / T, (a.H + T - 1) / T, a.N);
   kern<<<grid, NT, bytes, st>>>(static_cast<const Tin*>(in), static_cast<Tout*>(out), a);
   OCSC_LAUNCHED("k_preprocess");
+  OCSC_CUDA(cudaFreeAsync(kg, st));
   return OCSC_OK;
 }
 
