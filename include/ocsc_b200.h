@@ -138,6 +138,9 @@ int ocsc_code_fused(int dtype, int H, int W, int K, int B, const void* xh, const
  * 0, 2, 3).  On return u holds the codes U = S(w); iters/status as ocsc_code_admm.  `work`
  * holds ocsc_code_stream_workspace_bytes() bytes. */
 int ocsc_code_stream_supported(int dtype, int H, int W);
+/* CTAs (one per SM) one code iteration of the plane-resident streaming kernel occupies for this
+ * batch (float32 100 x 100), 0 when another path runs; the rest of the SMs are free for overlap. */
+int ocsc_code_stream_plane_ctas(int dtype, int H, int W, int K, int B);
 size_t ocsc_code_stream_workspace_bytes(int dtype, int H, int W, int K, int B);
 int ocsc_code_stream(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh, const void* den,
                      double beta, double rho, int max_iters, double rel_tol, void* u, void* work,
@@ -169,6 +172,12 @@ int ocsc_history_accumulate(int dtype_in, int dtype_hist, int K, int nfreq, int 
  * info (device int32): 0, or 1 + a frequency whose matrix was not positive definite. */
 int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfreq, const void* S, double ridge,
                         double scale, void* inv, int32_t* info, void* stream);
+/* Persistent form of ocsc_history_invert (32 < K <= 100): `ctas` CTAs claim frequencies from the
+ * device counter *ctr (zeroed by the caller) until none are left, so a few CTAs can run beside
+ * another kernel and a later full-grid launch sharing the counter finishes the rest.  info is
+ * not reset. */
+int ocsc_history_invert_claim(int dtype_hist, int dtype_inv, int K, int nfreq, const void* S, double ridge,
+                              double scale, void* inv, int32_t* info, int32_t* ctr, int ctas, void* stream);
 /* Low-rank refresh of a packed inverse (Woodbury): out_p = (A_p + U_p U_p^H)^-1 from
  * inv_in_p = A_p^-1 (packed complex128, e.g. ocsc_history_invert with dtype_inv = f64), U_p the
  * K x nb code spectra z element (b,k,p) at z[b*z_sb + k*z_sk + p*z_sp], nb <= 16; out packed as

@@ -57,6 +57,8 @@ SIGNATURES = {
     "ocsc_synthesize": [_I, _I, _I, _I, _P, _P, _P, _P],
     "ocsc_history_accumulate": [_I, _I, _I, _I, _I, _P, _I64, _I64, _I64, _P, _I64, _I64, _P, _P, _P],
     "ocsc_history_invert": [_I, _I, _I, _I, _P, _D, _D, _P, _P, _P],
+    "ocsc_code_stream_plane_ctas": [_I, _I, _I, _I, _I],
+    "ocsc_history_invert_claim": [_I, _I, _I, _I, _P, _D, _D, _P, _P, _P, _I, _P],
     "ocsc_history_woodbury": [_I, _I, _I, _I, _I, _P, _P, _I64, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P],
     "ocsc_history_woodbury_smem": [_I, _I],
     "ocsc_packed_to_full": [_I, _I, _I, _P, _D, _P, _P],

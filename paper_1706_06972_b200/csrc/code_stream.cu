@@ -920,6 +920,12 @@ extern "C" int ocsc_code_stream_supported(int dtype, int H, int W) {
   return 0;
 }
 
+extern "C" int ocsc_code_stream_plane_ctas(int dtype, int H, int W, int K, int B) {
+  // CTAs one iteration of the plane-resident kernel occupies (one per SM; 0: not that path)
+  if (dtype != OCSC_F32 || H != 100 || W != 100 || K <= 0 || B <= 0) return 0;
+  return plane_groups(K, B) * B;
+}
+
 extern "C" size_t ocsc_code_stream_workspace_bytes(int dtype, int H, int W, int K, int B) {
   const int WH = W / 2 + 1;
   const int L = H == 266 ? SGeo<float, 266, 266>::L : SGeo<float, 100, 100>::L;

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(512) k_hist_invert(int K, const cx<Th>* __rest
 // column k travel through shared memory, so shared traffic is O(K) instead of O(K^2).
 template <typename Th, typename Ti, int BI, int BJ>
 __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>* __restrict__ S, Th ridge, Th scale,
-                                                            cx<Ti>* inv, int32_t* info) {
+                                                            cx<Ti>* inv, int32_t* info, int nfreq, int* ctr) {
   using C = cx<Th>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // row k / column k / 1 / pivot, double-buffered by step parity: the owners of step k + 1
@@ -285,98 +285,113 @@ __global__ void __launch_bounds__(512, 1) k_hist_invert_reg(int K, const cx<Th>*
   C* rowb = reinterpret_cast<C*>(smem_raw);  // [2][K]
   C* colb = rowb + 2 * K;                    // [2][K]
   __shared__ Th piv_b[2];
-  const int p = blockIdx.x;
-  const int64_t npk = (int64_t)K * (K + 1) / 2;
-  const C* Sp = S + (int64_t)p * npk;
-  const int tjn = (K + BJ - 1) / BJ, tin = (K + BI - 1) / BI;
-  const int t = threadIdx.x;
-  const bool active = t < tin * tjn;
-  const int i0 = active ? (t / tjn) * BI : K, j0 = active ? (t % tjn) * BJ : K;
-  C a[BI][BJ];
-#pragma unroll
-  for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-    for (int jj = 0; jj < BJ; ++jj) {
-      const int i = i0 + ii, j = j0 + jj;
-      C v = mkc<C>(0, 0);
-      if (i < K && j < K) {
-        v = i >= j ? Sp[packed_index(i, j)] : cconj(Sp[packed_index(j, i)]);
-        if (i == j) v = mkc<C>(v.x + ridge, (Th)0);
-      }
-      a[ii][jj] = v;
+  // ctr == null: one frequency per CTA (p = blockIdx.x); otherwise a persistent grid that claims
+  // frequencies from *ctr (a few CTAs can run beside another kernel and a later full grid finishes)
+  __shared__ int pclaim;
+  for (int it = 0;; ++it) {
+    int p;
+    if (ctr) {
+      if (threadIdx.x == 0) pclaim = atomicAdd(ctr, 1);
+      __syncthreads();
+      p = pclaim;
+      __syncthreads();
+      if (p >= nfreq) break;
+    } else {
+      if (it > 0) break;
+      p = blockIdx.x;
     }
-  for (int k = 0; k < K; ++k) {
-    C* rowk = rowb + (k & 1) * K;
-    C* colk = colb + (k & 1) * K;
-    const bool own_row = k >= i0 && k < i0 + BI, own_col = k >= j0 && k < j0 + BJ;
-    // publish row k and column k (only their owners)
-    if (own_row) {
-#pragma unroll
-      for (int ii = 0; ii < BI; ++ii)
-        if (i0 + ii == k)
-#pragma unroll
-          for (int jj = 0; jj < BJ; ++jj) {
-            if (j0 + jj < K) rowk[j0 + jj] = a[ii][jj];
-            if (j0 + jj == k) {  // pivot owner: one reciprocal per step for the whole CTA
-              const Th d = a[ii][jj].x;
-              piv_b[k & 1] = (Th)1 / d;
-              if (!(d > (Th)0)) atomicCAS(info, 0, p + 1);
-            }
-          }
-    }
-    if (own_col) {
-#pragma unroll
-      for (int jj = 0; jj < BJ; ++jj)
-        if (j0 + jj == k)
-#pragma unroll
-          for (int ii = 0; ii < BI; ++ii)
-            if (i0 + ii < K) colk[i0 + ii] = a[ii][jj];
-    }
-    __syncthreads();
-    const Th pinv = piv_b[k & 1];
-    // generic rank-1 update with row/column k masked out (ci = 0 on row k, rs = 0 on column k)
-    C rs[BJ];
-#pragma unroll
-    for (int jj = 0; jj < BJ; ++jj) {
-      const int j = j0 + jj;
-      rs[jj] = (j < K && j != k) ? cscale(rowk[j], pinv) : mkc<C>(0, 0);
-    }
-#pragma unroll
-    for (int ii = 0; ii < BI; ++ii) {
-      const int i = i0 + ii;
-      const C ci = (i < K && i != k) ? colk[i] : mkc<C>(0, 0);
-#pragma unroll
+    const int64_t npk = (int64_t)K * (K + 1) / 2;
+    const C* Sp = S + (int64_t)p * npk;
+    const int tjn = (K + BJ - 1) / BJ, tin = (K + BI - 1) / BI;
+    const int t = threadIdx.x;
+    const bool active = t < tin * tjn;
+    const int i0 = active ? (t / tjn) * BI : K, j0 = active ? (t % tjn) * BJ : K;
+    C a[BI][BJ];
+  #pragma unroll
+    for (int ii = 0; ii < BI; ++ii)
+  #pragma unroll
       for (int jj = 0; jj < BJ; ++jj) {
-        C& v = a[ii][jj];
-        v.x = fma(-ci.x, rs[jj].x, fma(ci.y, rs[jj].y, v.x));
-        v.y = fma(-ci.x, rs[jj].y, fma(-ci.y, rs[jj].x, v.y));
+        const int i = i0 + ii, j = j0 + jj;
+        C v = mkc<C>(0, 0);
+        if (i < K && j < K) {
+          v = i >= j ? Sp[packed_index(i, j)] : cconj(Sp[packed_index(j, i)]);
+          if (i == j) v = mkc<C>(v.x + ridge, (Th)0);
+        }
+        a[ii][jj] = v;
+      }
+    for (int k = 0; k < K; ++k) {
+      C* rowk = rowb + (k & 1) * K;
+      C* colk = colb + (k & 1) * K;
+      const bool own_row = k >= i0 && k < i0 + BI, own_col = k >= j0 && k < j0 + BJ;
+      // publish row k and column k (only their owners)
+      if (own_row) {
+  #pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+          if (i0 + ii == k)
+  #pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) {
+              if (j0 + jj < K) rowk[j0 + jj] = a[ii][jj];
+              if (j0 + jj == k) {  // pivot owner: one reciprocal per step for the whole CTA
+                const Th d = a[ii][jj].x;
+                piv_b[k & 1] = (Th)1 / d;
+                if (!(d > (Th)0)) atomicCAS(info, 0, p + 1);
+              }
+            }
+      }
+      if (own_col) {
+  #pragma unroll
+        for (int jj = 0; jj < BJ; ++jj)
+          if (j0 + jj == k)
+  #pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+              if (i0 + ii < K) colk[i0 + ii] = a[ii][jj];
+      }
+      __syncthreads();
+      const Th pinv = piv_b[k & 1];
+      // generic rank-1 update with row/column k masked out (ci = 0 on row k, rs = 0 on column k)
+      C rs[BJ];
+  #pragma unroll
+      for (int jj = 0; jj < BJ; ++jj) {
+        const int j = j0 + jj;
+        rs[jj] = (j < K && j != k) ? cscale(rowk[j], pinv) : mkc<C>(0, 0);
+      }
+  #pragma unroll
+      for (int ii = 0; ii < BI; ++ii) {
+        const int i = i0 + ii;
+        const C ci = (i < K && i != k) ? colk[i] : mkc<C>(0, 0);
+  #pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+          C& v = a[ii][jj];
+          v.x = fma(-ci.x, rs[jj].x, fma(ci.y, rs[jj].y, v.x));
+          v.y = fma(-ci.x, rs[jj].y, fma(-ci.y, rs[jj].x, v.y));
+        }
+      }
+      // row k -> scaled row, column k -> -scaled column, pivot -> 1/pivot (owners only)
+      if (own_row) {
+  #pragma unroll
+        for (int ii = 0; ii < BI; ++ii)
+          if (i0 + ii == k)
+  #pragma unroll
+            for (int jj = 0; jj < BJ; ++jj) a[ii][jj] = (j0 + jj == k) ? mkc<C>(pinv, (Th)0) : rs[jj];
+      }
+      if (own_col) {
+  #pragma unroll
+        for (int jj = 0; jj < BJ; ++jj)
+          if (j0 + jj == k)
+  #pragma unroll
+            for (int ii = 0; ii < BI; ++ii)
+              if (i0 + ii != k && i0 + ii < K) a[ii][jj] = cscale(colk[i0 + ii], -pinv);
       }
     }
-    // row k -> scaled row, column k -> -scaled column, pivot -> 1/pivot (owners only)
-    if (own_row) {
-#pragma unroll
-      for (int ii = 0; ii < BI; ++ii)
-        if (i0 + ii == k)
-#pragma unroll
-          for (int jj = 0; jj < BJ; ++jj) a[ii][jj] = (j0 + jj == k) ? mkc<C>(pinv, (Th)0) : rs[jj];
-    }
-    if (own_col) {
-#pragma unroll
-      for (int jj = 0; jj < BJ; ++jj)
-        if (j0 + jj == k)
-#pragma unroll
-          for (int ii = 0; ii < BI; ++ii)
-            if (i0 + ii != k && i0 + ii < K) a[ii][jj] = cscale(colk[i0 + ii], -pinv);
-    }
+    cx<Ti>* out = inv + (int64_t)p * npk;
+  #pragma unroll
+    for (int ii = 0; ii < BI; ++ii)
+  #pragma unroll
+      for (int jj = 0; jj < BJ; ++jj) {
+        const int i = i0 + ii, j = j0 + jj;
+        if (i < K && j <= i) out[packed_index(i, j)] = ccast<Ti>(cscale(a[ii][jj], scale));
+      }
   }
-  cx<Ti>* out = inv + (int64_t)p * npk;
-#pragma unroll
-  for (int ii = 0; ii < BI; ++ii)
-#pragma unroll
-    for (int jj = 0; jj < BJ; ++jj) {
-      const int i = i0 + ii, j = j0 + jj;
-      if (i < K && j <= i) out[packed_index(i, j)] = ccast<Ti>(cscale(a[ii][jj], scale));
-    }
 }
 
 template <typename T>
@@ -672,7 +687,7 @@ static int launch_invert(int K, int nfreq, const void* S, double ridge, double s
     const int threads = ((((K + 3) / 4) * ((K + 4) / 5)) + 31) / 32 * 32;
     const size_t sm = sizeof(cx<Th>) * 4 * (size_t)K;
     k_hist_invert_reg<Th, Ti, 4, 5><<<nfreq, threads, sm, s>>>(K, (const cx<Th>*)S, (Th)ridge, (Th)scale,
-                                                              (cx<Ti>*)inv, info);
+                                                              (cx<Ti>*)inv, info, nfreq, nullptr);
     OCSC_LAUNCHED("k_hist_invert_reg");
     return OCSC_OK;
   }
@@ -696,6 +711,30 @@ extern "C" int ocsc_history_invert(int dtype_hist, int dtype_inv, int K, int nfr
   if (dtype_hist == OCSC_F64 && dtype_inv == OCSC_F32) return launch_invert<double, float>(K, nfreq, S, ridge, scale, inv, info, s);
   if (dtype_hist == OCSC_F32 && dtype_inv == OCSC_F32) return launch_invert<float, float>(K, nfreq, S, ridge, scale, inv, info, s);
   return fail(OCSC_EARG, "history_invert: unsupported dtype pair");
+}
+
+// Persistent variant of the register-blocked inverse (32 < K <= 100): `ctas` CTAs claim
+// frequencies from the device counter *ctr (zeroed by the caller before the first launch) until
+// none are left.  Two launches sharing the counter split the work: e.g. a few CTAs beside the
+// streaming code kernel, then a full grid after it.  info is not reset here.
+extern "C" int ocsc_history_invert_claim(int dtype_hist, int dtype_inv, int K, int nfreq, const void* S,
+                                         double ridge, double scale, void* inv, int32_t* info, int32_t* ctr,
+                                         int ctas, void* stream) {
+  if (K <= 32 || K > 100 || nfreq < 0 || ctas <= 0) return fail(OCSC_ESHAPE, "history_invert_claim: 32 < K <= 100");
+  cudaStream_t s = as_stream(stream);
+  if (nfreq == 0) return OCSC_OK;
+  const int threads = ((((K + 3) / 4) * ((K + 4) / 5)) + 31) / 32 * 32;
+  const size_t sm = csize(dtype_hist) * 4 * (size_t)K;
+#define OCSC_GJC(TH, TI)                                                                                        \
+  k_hist_invert_reg<TH, TI, 4, 5><<<ctas, threads, sm, s>>>(K, (const cx<TH>*)S, (TH)ridge, (TH)scale,         \
+                                                            (cx<TI>*)inv, info, nfreq, (int*)ctr)
+  if (dtype_hist == OCSC_F64 && dtype_inv == OCSC_F64) OCSC_GJC(double, double);
+  else if (dtype_hist == OCSC_F64 && dtype_inv == OCSC_F32) OCSC_GJC(double, float);
+  else if (dtype_hist == OCSC_F32 && dtype_inv == OCSC_F32) OCSC_GJC(float, float);
+  else return fail(OCSC_EARG, "history_invert_claim: unsupported dtype pair");
+#undef OCSC_GJC
+  OCSC_LAUNCHED("k_hist_invert_reg");
+  return OCSC_OK;
 }
 
 extern "C" int ocsc_packed_to_full(int dtype, int K, int nfreq, const void* packed, double scale, void* full,

@@ -313,6 +313,67 @@ class OnlineTrainer:
         self._mark("fold end")
         # (the rest of the step: J row-solve + projection rounds, den)
 
+    def _invert_beside_plan(self, B: int) -> int:
+        """CTAs for the history inverse beside the plane-resident stream kernel (0: no overlap).
+
+        The plane kernel occupies one CTA per SM for a fixed set of (sample, filter group) CTAs;
+        the remaining SMs run a persistent Gauss-Jordan of S + t_final rho P I during coding, a
+        full grid finishes it, and a Woodbury refresh folds the batch in."""
+        key = ("beside", B)
+        if key not in self._fused_ok:
+            lib = _lib.load()
+            h = self.history
+            ctas = lib.ocsc_code_stream_plane_ctas(_lib.code(self.dtype), self.H, self.W, self.K, B)
+            sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+            ok = (self.config.overlap and ctas > 0 and sms - ctas >= 4 and B <= 16 and 32 < self.K <= 100
+                  and type(self)._fold is OnlineTrainer._fold and h.solver == "gj"
+                  and h.S.dtype == torch.complex128
+                  and lib.ocsc_history_woodbury_smem(self.K, B) <= 227 * 1024)
+            self._fused_ok[key] = sms - ctas if ok else 0
+        return self._fused_ok[key]
+
+    def _invert_beside_coding(self, B: int, ctas: int):
+        """Side stream: zero the claim counter, launch `ctas` persistent inverse CTAs on S."""
+        h = self.history
+        sd = self._side_state()
+        if "ctr" not in sd:
+            sd["ctr"] = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        ready = torch.cuda.Event()
+        ready.record()
+        with torch.cuda.stream(sd["stream"]):
+            sd["stream"].wait_event(ready)
+            sd["ctr"].zero_()
+            zeroed = torch.cuda.Event()
+            zeroed.record()
+            sd["info"].zero_()
+            _lib.call("ocsc_history_invert_claim", _lib.code(h.S.dtype), _lib.code(h.S.dtype), self.K, self.nf,
+                      _lib.ptr(h.S), (h.count + B) * h.ridge, 1.0, _lib.ptr(sd["inv"]), _lib.ptr(sd["info"]),
+                      _lib.ptr(sd["ctr"]), int(ctas), _lib.stream())
+            self._mark("side inverse end")
+            done = torch.cuda.Event()
+            done.record()
+        return zeroed, done
+
+    def _finish_inverse(self, B: int, zeroed: torch.cuda.Event) -> None:
+        """Main stream, after coding: a full grid claims the frequencies the side CTAs have not."""
+        h, sd = self.history, self._side
+        torch.cuda.current_stream().wait_event(zeroed)
+        _lib.call("ocsc_history_invert_claim", _lib.code(h.S.dtype), _lib.code(h.S.dtype), self.K, self.nf,
+                  _lib.ptr(h.S), (h.count + B) * h.ridge, 1.0, _lib.ptr(sd["inv"]), _lib.ptr(sd["info"]),
+                  _lib.ptr(sd["ctr"]), int(min(self.nf, 4 * 148)), _lib.stream())
+
+    def _fold_woodbury(self, uh, xh, B: int, side_done: torch.cuda.Event) -> None:
+        """Main stream: Woodbury refresh of the inverse with the whole batch + its fold into S, c."""
+        h, nf, K, sd = self.history, self.nf, self.K, self._side
+        torch.cuda.current_stream().wait_event(side_done)
+        if h._inv is None:
+            h._inv = torch.empty(h.S.shape, dtype=h.inv_dtype, device=h.S.device)
+        _lib.call("ocsc_history_woodbury", _lib.code(uh.dtype), _lib.code(h.inv_dtype), K, nf, B, _lib.ptr(sd["inv"]),
+                  _lib.ptr(uh), K * nf, nf, 1, _lib.ptr(h._inv), _lib.ptr(sd["info"][1:]), _lib.ptr(xh), nf, 1,
+                  _lib.ptr(h.S), _lib.ptr(h.c), _lib.stream())
+        h.count += B
+        h._inv_count = h.count
+
     def _load(self, X) -> tuple[torch.Tensor, int]:
         P = self.shape.size
         if isinstance(X, torch.Tensor):
@@ -400,18 +461,31 @@ class OnlineTrainer:
             else:
                 self._code_fused(xh, buf, uh, obj, 0, B)
         elif stream:
+            pre = self._invert_beside_plan(B)
+            if pre:  # the history inverse of S (+ this batch's ridge) runs on the SMs coding leaves idle
+                inv_zeroed, side_done = self._invert_beside_coding(B, pre)
             infer_codes_stream(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
         else:
             infer_codes(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
+        pre = self._invert_beside_plan(B) if stream else 0
+        if pre:  # finish the inverse on the full grid (the side CTAs keep claiming frequencies)
+            self._mark("coded")
+            self._finish_inverse(B, inv_zeroed)
+            self._mark("inverse finished")
         if check:
             status = buf.status[:B].cpu()
             if bool((status == 2).any()):
+                if pre:
+                    side_done.synchronize()
                 it = int(buf.iters[:B][status.to(buf.iters.device) == 2].min().cpu())
                 raise DivergenceError(f"code solver diverged at iteration {it}")
         if not fused:
             obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
         if split:
             self._fold_overlapped(uh, xh, split, B, side_done)
+        elif pre:
+            self._fold_woodbury(uh, xh, B, side_done)
+            self._mark("woodbury")
         else:
             self._fold(uh, xh, B)
         self._dictionary_update()

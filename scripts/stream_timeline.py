@@ -1,0 +1,28 @@
+"""Event timeline of one config-2 mini-batch with the inverse beside the stream kernel (dev aid)."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1706_06972_b200 as ob  # noqa: E402
+from oracle import ocsc_oracle as O  # noqa: E402
+
+B = 10
+X = O.synth_images(4 * B, (100, 100), (100, 100), 20, seed=1).reshape(4 * B, -1)
+for overlap in (True, False):
+    tr = ob.OnlineTrainer(ob.SignalShape((100, 100), (11, 11)),
+                          ob.TrainConfig(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0,
+                                         overlap=overlap))
+    for m in range(3):
+        tr.partial_fit(X[m * B:(m + 1) * B])
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tr._tl = []
+    e0.record()
+    tr.partial_fit(X[3 * B:4 * B])
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"overlap={overlap}: beside={tr._invert_beside_plan(B)} step {e0.elapsed_time(e1):.2f} ms")
+    for label, ev in tr._tl:
+        print(f"   {label:18s} {e0.elapsed_time(ev):8.3f} ms")

@@ -455,6 +455,27 @@ def test_overlapped_history_inverse_matches_serial_path(B):
     assert rel(a.final_filters(), b.final_filters()) < 1e-5
 
 
+def test_inverse_beside_stream_coding_matches_serial_path():
+    """Config-2 shapes (plane-resident stream kernel): the history inverse claimed by persistent
+    CTAs on the SMs coding leaves idle + a full-grid finish + a Woodbury refresh with the batch
+    trains like the serial accumulate-then-invert path."""
+    c = O.CONFIGS[0]
+    B = 10
+    X = O.synth_images(2 * B, (100, 100), (100, 100), 20, seed=23).reshape(2 * B, -1)
+    kw = dict(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0, inner_iters=10,
+              code_max_iters=60)
+    shape = ob.SignalShape((100, 100), (11, 11))
+    a = ob.OnlineTrainer(shape, ob.TrainConfig(overlap=True, **kw))
+    b = ob.OnlineTrainer(shape, ob.TrainConfig(overlap=False, **kw))
+    assert a._invert_beside_plan(B) > 0 and b._invert_beside_plan(B) == 0
+    for m in range(2):
+        ra, rb = a.partial_fit(X[m * B:(m + 1) * B]), b.partial_fit(X[m * B:(m + 1) * B])
+        assert np.max(np.abs(ra.objectives - rb.objectives) / np.abs(rb.objectives)) < 1e-5
+    assert a.history.count == b.history.count == 2 * B
+    assert rel(a.history.inverse().cpu().numpy(), b.history.inverse().cpu().numpy()) < 1e-5
+    assert rel(a.final_filters(), b.final_filters()) < 1e-5
+
+
 def test_fused_divergence_raises():
     shape = ob.SignalShape((14, 14), (3, 3))
     tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=4, batch_size=2))
