@@ -7,7 +7,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1706_06972_b200 import _lib  # noqa: E402
 
-K, nf, nb = 100, 924, int(sys.argv[1]) if len(sys.argv) > 1 else 5
+K, nb = 100, int(sys.argv[1]) if len(sys.argv) > 1 else 5
+nf = int(os.environ.get("WB_NF", "924"))
 npk = K * (K + 1) // 2
 inv = torch.randn(nf, npk, dtype=torch.complex128, device="cuda")
 z = torch.randn(nb, K, nf, dtype=torch.complex64, device="cuda")
