@@ -470,17 +470,18 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
   extern __shared__ __align__(16) unsigned char smraw[];
   const int p = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
+  const int nbp = nb | 1;  // odd row pitch (complex): lanes along K hit distinct bank groups
   C* A = reinterpret_cast<C*>(smraw);  // packed A^-1
-  C* U = A + npk;                      // [K][nb]
-  C* Wm = U + K * nb;                  // [K][nb]  W = A^-1 U
-  C* X = Wm + K * nb;                  // [K][nb]  X = W Cinv
-  C* Cm = X + K * nb;                  // [nb][nb] capacitance, inverted in place
+  C* U = A + npk;                      // [K][nbp]
+  C* Wm = U + K * nbp;                 // [K][nbp]  W = A^-1 U
+  C* X = Wm + K * nbp;                 // [K][nbp]  X = W Cinv
+  C* Cm = X + K * nbp;                 // [nb][nb] capacitance, inverted in place
   const double2* Ap = inv_in + (int64_t)p * npk;
   for (int64_t e = tid; e < npk; e += nt) A[e] = Ap[e];
   for (int e = tid; e < K * nb; e += nt) {
     const int k = e / nb, j = e - k * nb;
     const auto v = z[j * zb + k * zk + p * zp];
-    U[e] = make_double2((double)v.x, (double)v.y);
+    U[k * nbp + j] = make_double2((double)v.x, (double)v.y);
   }
   __syncthreads();
   // W[t][j] = sum_{k<=t} A[t][k] U[k][j] + sum_{i>t} conj(A[i][t]) U[i][j]: the packed row of t,
@@ -491,20 +492,20 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
     const C* row = A + packed_index(t, 0);
     int k = 0;
     for (; k + 1 <= t; k += 2) {
-      cfma(a0, row[k], U[k * nb + j]);
-      cfma(a1, row[k + 1], U[(k + 1) * nb + j]);
+      cfma(a0, row[k], U[k * nbp + j]);
+      cfma(a1, row[k + 1], U[(k + 1) * nbp + j]);
     }
-    if (k <= t) cfma(a0, row[k], U[k * nb + j]);
+    if (k <= t) cfma(a0, row[k], U[k * nbp + j]);
     int i = t + 1;
     int64_t q = packed_index(i, t);  // packed (i, t): advances by i + 1 per row
     for (; i + 1 < K; i += 2) {
-      cfma(a0, cconj(A[q]), U[i * nb + j]);
+      cfma(a0, cconj(A[q]), U[i * nbp + j]);
       q += i + 1;
-      cfma(a1, cconj(A[q]), U[(i + 1) * nb + j]);
+      cfma(a1, cconj(A[q]), U[(i + 1) * nbp + j]);
       q += i + 2;
     }
-    if (i < K) cfma(a0, cconj(A[q]), U[i * nb + j]);
-    Wm[e] = make_double2(a0.x + a1.x, a0.y + a1.y);
+    if (i < K) cfma(a0, cconj(A[q]), U[i * nbp + j]);
+    Wm[t * nbp + j] = make_double2(a0.x + a1.x, a0.y + a1.y);
   }
   __syncthreads();
   {  // C = I + U^H W: one warp per entry, lanes split the K-sum, shuffle reduction
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
       const int a = e / nb, b = e - a * nb;
       double ax = 0, ay = 0;
       for (int k = lane; k < K; k += 32) {
-        const C u = U[k * nb + a], w = Wm[k * nb + b];
+        const C u = U[k * nbp + a], w = Wm[k * nbp + b];
         ax += u.x * w.x + u.y * w.y;  // conj(u) w
         ay += u.x * w.y - u.y * w.x;
       }
@@ -559,8 +560,8 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
   for (int e = tid; e < K * nb; e += nt) {  // X = W Cinv
     const int i = e / nb, j = e - i * nb;
     C acc = make_double2(0, 0);
-    for (int m = 0; m < nb; ++m) cfma(acc, Wm[i * nb + m], Cm[m * nb + j]);
-    X[e] = acc;
+    for (int m = 0; m < nb; ++m) cfma(acc, Wm[i * nbp + m], Cm[m * nb + j]);
+    X[i * nbp + j] = acc;
   }
   __syncthreads();
   if (S) {  // fold the same samples into the history sums: c_p += sum_b conj(x_b) z_b
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
       C acc = cvec[(int64_t)p * K + k];
       for (int m = 0; m < nb; ++m) {
         const auto xv = x[m * xb + p * xp];
-        const C u = U[k * nb + m];
+        const C u = U[k * nbp + m];
         acc.x += (double)xv.x * u.x + (double)xv.y * u.y;
         acc.y += (double)xv.x * u.y - (double)xv.y * u.x;
       }
@@ -582,7 +583,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
     for (int j = lane; j <= i; j += 32) {  // out[i][j] = A^-1[i][j] - sum_m X[i][m] conj(W[j][m])
       C acc = A[packed_index(i, j)];
       for (int m = 0; m < nb; ++m) {
-        const C x = X[i * nb + m], w = Wm[j * nb + m];
+        const C x = X[i * nbp + m], w = Wm[j * nbp + m];
         acc.x -= x.x * w.x + x.y * w.y;
         acc.y -= x.y * w.x - x.x * w.y;
       }
@@ -590,7 +591,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
       if (Sp) {  // S_p[i][j] += sum_m U[i][m] conj(U[j][m])
         C sv = Sp[packed_index(i, j)];
         for (int m = 0; m < nb; ++m) {
-          const C ui = U[i * nb + m], uj = U[j * nb + m];
+          const C ui = U[i * nbp + m], uj = U[j * nbp + m];
           sv.x += ui.x * uj.x + ui.y * uj.y;
           sv.y += ui.y * uj.x - ui.x * uj.y;
         }
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
 }
 
 extern "C" size_t ocsc_history_woodbury_smem(int K, int nb) {
-  return sizeof(double2) * ((size_t)K * (K + 1) / 2 + 3 * (size_t)K * nb + (size_t)nb * nb);
+  return sizeof(double2) * ((size_t)K * (K + 1) / 2 + 3 * (size_t)K * (nb | 1) + (size_t)nb * nb);
 }
 
 extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, const void* inv_in,
