@@ -477,12 +477,14 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
   C* X = Wm + K * nbp;                 // [K][nbp]  X = W Cinv
   C* Cm = X + K * nbp;                 // [nb][nb] capacitance, inverted in place
   const double2* Ap = inv_in + (int64_t)p * npk;
-  for (int64_t e = tid; e < npk; e += nt) A[e] = Ap[e];
+  for (int64_t e = tid; e < npk; e += nt) cp_async<16>(A + e, Ap + e);  // all in flight at once
+  cp_async_commit();
   for (int e = tid; e < K * nb; e += nt) {
     const int k = e / nb, j = e - k * nb;
     const auto v = z[j * zb + k * zk + p * zp];
     U[k * nbp + j] = make_double2((double)v.x, (double)v.y);
   }
+  cp_async_wait<0>();
   __syncthreads();
   // W[t][j] = sum_{k<=t} A[t][k] U[k][j] + sum_{i>t} conj(A[i][t]) U[i][j]: the packed row of t,
   // then its packed column (K terms for every t, branch-free), two interleaved accumulators
