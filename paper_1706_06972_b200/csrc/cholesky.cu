@@ -77,14 +77,23 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, const cx<T>* __restr
   C* L = Lall + (int64_t)p * K * K;
   const int PR = K - CT + 64;  // panel row stride: K - CT rows + slack for the last 64-block
 
-  // expand the packed lower triangle (+ ridge) into the lower half of the full layout
+  // expand the packed lower triangle (+ ridge) into the lower half of the full layout; each
+  // lane issues up to 8 loads of its row before storing (the copy is latency-bound otherwise)
   for (int i = warp; i < K; i += NT / 32) {
     const C* src = Sp + packed_index(i, 0);
     C* dst = L + (int64_t)i * K;
-    for (int j = lane; j <= i; j += 32) {
-      C v = src[j];
-      if (j == i) v = mkc<C>(v.x + ridge, (T)0);
-      dst[j] = v;
+    for (int j0 = lane; j0 <= i; j0 += 8 * 32) {
+      C v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + 32 * u;
+        v[u] = j <= i ? src[j] : mkc<C>(0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + 32 * u;
+        if (j <= i) dst[j] = j == i ? mkc<C>(v[u].x + ridge, (T)0) : v[u];
+      }
     }
   }
   __syncthreads();
