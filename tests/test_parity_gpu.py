@@ -455,6 +455,25 @@ def test_overlapped_history_inverse_matches_serial_path(B):
     assert rel(a.final_filters(), b.final_filters()) < 1e-5
 
 
+def test_overlapped_inverse_does_not_drift():
+    """Twelve config-1 mini-batches (600 samples): the Woodbury-refreshed inverse path stays on
+    the serial path's objective trace and filters (no accumulation of refresh error)."""
+    c = O.CONFIGS[1]
+    B, steps = 50, 12
+    X = O.synth_images(B * steps, c["dims0"], c["grid"], c["K0"], seed=31).reshape(B * steps, -1)
+    kw = dict(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0, inner_iters=10,
+              code_max_iters=100)
+    shape = ob.SignalShape(c["grid"], (11, 11))
+    a = ob.OnlineTrainer(shape, ob.TrainConfig(overlap=True, **kw))
+    b = ob.OnlineTrainer(shape, ob.TrainConfig(overlap=False, **kw))
+    worst = 0.0
+    for m in range(steps):
+        ra, rb = a.partial_fit(X[m * B:(m + 1) * B]), b.partial_fit(X[m * B:(m + 1) * B])
+        worst = max(worst, float(np.max(np.abs(ra.objectives - rb.objectives) / np.abs(rb.objectives))))
+    assert worst < 1e-4
+    assert rel(a.final_filters(), b.final_filters()) < 1e-4
+
+
 def test_inverse_beside_stream_coding_matches_serial_path():
     """Config-2 shapes (plane-resident stream kernel): the history inverse claimed by persistent
     CTAs on the SMs coding leaves idle + a full-grid finish + a Woodbury refresh with the batch
