@@ -352,7 +352,7 @@ def run_b200(args, rank, world, local_rank):
                    "sample": "n/a (memory): the reference's inv_gram for config 3 alone is 74 GB of complex128 "
                              "(dictionary.py:30-54), plus >= 3 same-size temporaries in update_history"}
         else:
-            n = int(os.environ.get("OCSC_CPU_SAMPLE_IMAGES", "2" if args.config == 1 else "1"))
+            n = int(os.environ.get("OCSC_CPU_SAMPLE_IMAGES", "3" if args.config == 1 else "1"))  # ~12 s of CPU work
             rate, done, dt = cpu_oracle_rate(n)
             cpu = {"value": rate, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
                    "sample": f"{done} image(s) of config {args.config} through oracle/ocsc_oracle.py (reference "
