@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0,
   C* twW = twH + H;                         // e^{+2 pi i n / W}
   C* Y = twW + W;                           // [M0][Wh], reused as Q
   T* al = reinterpret_cast<T*>(Y + (int64_t)M0 * Wh);
+  C* Xs = reinterpret_cast<C*>(smem_raw) + H + W + (int64_t)M0 * Wh + (M + 1) / 2 + 1;  // [nf] D + Theta
   __shared__ double scratch[32];
   __shared__ double norm_s;
   const int k = blockIdx.x;
@@ -52,14 +53,16 @@ __global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0,
   __syncthreads();
 
   if (mode != SUPPORT_RFFT) {
+    // stage D + Theta (coalesced, every load of the plane in flight at once)
+    for (int o = threadIdx.x; o < nf; o += blockDim.x) Xs[o] = Tk ? cadd(Dk[o], Tk[o]) : Dk[o];
+    __syncthreads();
     // pruned inverse along u
     for (int o = threadIdx.x; o < M0 * Wh; o += blockDim.x) {
       const int m0 = o / Wh, v = o % Wh;
       C acc = mkc<C>(0, 0);
       int idx = (int)(((int64_t)u0 * m0) % H);
       for (int u = u0; u < u1; ++u) {
-        C x = Dk[(int64_t)(u - u0) * Wh + v];
-        if (Tk) x = cadd(x, Tk[(int64_t)(u - u0) * Wh + v]);
+        const C x = Xs[(u - u0) * Wh + v];
         cfma(acc, x, twH[idx]);
         idx += m0;
         if (idx >= H) idx -= H;
@@ -197,7 +200,8 @@ template <typename T>
 static int launch_project(int mode, int H, int W, int M0, int M1, int K, int u0, int u1, const void* Dh, void* Th,
                           void* Vh, void* alpha, double* apart, cudaStream_t s) {
   const int Wh = W / 2 + 1;
-  const size_t smem = sizeof(cx<T>) * ((size_t)H + W + (size_t)M0 * Wh) + sizeof(T) * (size_t)M0 * M1 + 16;
+  const int M = M0 * M1;
+  const size_t smem = sizeof(cx<T>) * ((size_t)H + W + (size_t)M0 * Wh + (M + 1) / 2 + 1 + (size_t)(u1 - u0) * Wh);
   if (smem > 227 * 1024) return fail(OCSC_EARG, "dict_project: grid too large for the fused projection");
   OCSC_CUDA(cudaFuncSetAttribute(k_project<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_project<T><<<K, 256, smem, s>>>(mode, H, W, M0, M1, u0, u1, (const cx<T>*)Dh, (cx<T>*)Th, (cx<T>*)Vh,
