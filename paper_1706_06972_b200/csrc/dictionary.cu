@@ -23,7 +23,7 @@ namespace ocsc {
 enum ProjMode { PROJECT = 0, CROP_ONLY = 1, SUPPORT_RFFT = 2, CROP_PARTIAL = 3 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0, int M1, int u0, int u1,
+__global__ void __launch_bounds__(256) k_project(int mode, int staged, int H, int W, int M0, int M1, int u0, int u1,
                                                  const cx<T>* __restrict__ Dh, cx<T>* Th, cx<T>* Vh, T* alpha,
                                                  double* apart) {
   using C = cx<T>;
@@ -53,16 +53,19 @@ __global__ void __launch_bounds__(256) k_project(int mode, int H, int W, int M0,
   __syncthreads();
 
   if (mode != SUPPORT_RFFT) {
-    // stage D + Theta (coalesced, every load of the plane in flight at once)
-    for (int o = threadIdx.x; o < nf; o += blockDim.x) Xs[o] = Tk ? cadd(Dk[o], Tk[o]) : Dk[o];
-    __syncthreads();
+    // stage D + Theta (coalesced, every load of the plane in flight at once) when it fits
+    if (staged) {
+      for (int o = threadIdx.x; o < nf; o += blockDim.x) Xs[o] = Tk ? cadd(Dk[o], Tk[o]) : Dk[o];
+      __syncthreads();
+    }
     // pruned inverse along u
     for (int o = threadIdx.x; o < M0 * Wh; o += blockDim.x) {
       const int m0 = o / Wh, v = o % Wh;
       C acc = mkc<C>(0, 0);
       int idx = (int)(((int64_t)u0 * m0) % H);
       for (int u = u0; u < u1; ++u) {
-        const C x = Xs[(u - u0) * Wh + v];
+        const int64_t q = (int64_t)(u - u0) * Wh + v;
+        const C x = staged ? Xs[q] : (Tk ? cadd(Dk[q], Tk[q]) : Dk[q]);
         cfma(acc, x, twH[idx]);
         idx += m0;
         if (idx >= H) idx -= H;
@@ -201,10 +204,13 @@ static int launch_project(int mode, int H, int W, int M0, int M1, int K, int u0,
                           void* Vh, void* alpha, double* apart, cudaStream_t s) {
   const int Wh = W / 2 + 1;
   const int M = M0 * M1;
-  const size_t smem = sizeof(cx<T>) * ((size_t)H + W + (size_t)M0 * Wh + (M + 1) / 2 + 1 + (size_t)(u1 - u0) * Wh);
+  const size_t base = sizeof(cx<T>) * ((size_t)H + W + (size_t)M0 * Wh + (M + 1) / 2 + 1);
+  const size_t with_plane = base + sizeof(cx<T>) * (size_t)(u1 - u0) * Wh;  // + staged D + Theta
+  const int staged = with_plane <= 100 * 1024;  // small grids (config 1: 7 KB); large ones read L2
+  const size_t smem = staged ? with_plane : base;
   if (smem > 227 * 1024) return fail(OCSC_EARG, "dict_project: grid too large for the fused projection");
   OCSC_CUDA(cudaFuncSetAttribute(k_project<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_project<T><<<K, 256, smem, s>>>(mode, H, W, M0, M1, u0, u1, (const cx<T>*)Dh, (cx<T>*)Th, (cx<T>*)Vh,
+  k_project<T><<<K, 256, smem, s>>>(mode, staged, H, W, M0, M1, u0, u1, (const cx<T>*)Dh, (cx<T>*)Th, (cx<T>*)Vh,
                                     (T*)alpha, apart);
   OCSC_LAUNCHED("k_project");
   return OCSC_OK;
