@@ -436,7 +436,7 @@ def test_woodbury_refresh_matches_direct_inverse():
     assert rel(out.cpu().numpy(), want.cpu().numpy()) < 1e-12
 
 
-@pytest.mark.parametrize("B", [50, 47, 16])
+@pytest.mark.parametrize("B", [50, 47, 46, 16])
 def test_overlapped_history_inverse_matches_serial_path(B):
     """Config-1 shapes: the tail-overlapped inverse (side-stream Gauss-Jordan of the main part +
     Woodbury refresh with the tail) trains like the serial accumulate-then-invert path."""
