@@ -431,12 +431,18 @@ int launch_k(const void* in, void* out, PrepArgs a, size_t bytes, cudaStream_t s
   double* kg = nullptr;  // stream-ordered scratch for the Gaussian tables
   OCSC_CUDA(cudaMallocAsync((void**)&kg, sizeof(double) * ((size_t)a.s1 + (size_t)a.N * a.s2 + 1), st));
   k_prep_weights<<<(a.N + 1 + 127) / 128, 128, 0, st>>>(a, kg);
-  OCSC_LAUNCHED("k_prep_weights");
-  a.kg = kg;
-  dim3 grid((a.W + T - 1) / T, (a.H + T - 1) / T, a.N);
-  kern<<<grid, NT, bytes, st>>>(static_cast<const Tin*>(in), static_cast<Tout*>(out), a);
-  OCSC_LAUNCHED("k_preprocess");
-  OCSC_CUDA(cudaFreeAsync(kg, st));
+  count_launches(1);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    a.kg = kg;
+    dim3 grid((a.W + T - 1) / T, (a.H + T - 1) / T, a.N);
+    kern<<<grid, NT, bytes, st>>>(static_cast<const Tin*>(in), static_cast<Tout*>(out), a);
+    count_launches(1);
+    e = cudaGetLastError();
+  }
+  const cudaError_t ef = cudaFreeAsync(kg, st);  // freed on every path (no leak on a launch error)
+  if (e != cudaSuccess) return cuda_fail(e, "k_preprocess");
+  if (ef != cudaSuccess) return cuda_fail(ef, "cudaFreeAsync");
   return OCSC_OK;
 }
 
