@@ -455,6 +455,26 @@ def test_overlapped_history_inverse_matches_serial_path(B):
     assert rel(a.final_filters(), b.final_filters()) < 1e-5
 
 
+def test_new_entry_points_fail_loudly():
+    """Argument errors of the overlap entry points surface as the reference exception classes."""
+    from paper_1706_06972_b200 import _lib
+    K, nf = 40, 3
+    inv = torch.zeros(nf, K * (K + 1) // 2, dtype=torch.complex128, device="cuda")
+    z = torch.zeros(17, K, nf, dtype=torch.complex64, device="cuda")
+    info = torch.zeros(2, dtype=torch.int32, device="cuda")
+    with pytest.raises(ob.ShapeMismatchError, match="nb <= 16"):
+        _lib.call("ocsc_history_woodbury", _lib.F32, _lib.F64, K, nf, 17, _lib.ptr(inv), _lib.ptr(z), K * nf, nf, 1,
+                  _lib.ptr(inv), _lib.ptr(info), None, 0, 0, None, None, _lib.stream())
+    with pytest.raises(ValueError, match="go together"):
+        _lib.call("ocsc_history_woodbury", _lib.F32, _lib.F64, K, nf, 2, _lib.ptr(inv), _lib.ptr(z), K * nf, nf, 1,
+                  _lib.ptr(inv), _lib.ptr(info), None, 0, 0, _lib.ptr(inv), None, _lib.stream())
+    with pytest.raises(ob.ShapeMismatchError, match="32 < K <= 100"):
+        _lib.call("ocsc_history_invert_claim", _lib.F64, _lib.F64, 120, nf, _lib.ptr(inv), 1.0, 1.0, _lib.ptr(inv),
+                  _lib.ptr(info), _lib.ptr(info), 4, _lib.stream())
+    assert _lib.load().ocsc_code_stream_plane_ctas(_lib.F64, 100, 100, 100, 10) == 0   # float64: row/column kernels
+    assert _lib.load().ocsc_code_stream_plane_ctas(_lib.F32, 100, 100, 100, 10) > 0
+
+
 def test_overlapped_inverse_does_not_drift():
     """Twelve config-1 mini-batches (600 samples): the Woodbury-refreshed inverse path stays on
     the serial path's objective trace and filters (no accumulation of refresh error)."""
