@@ -216,3 +216,49 @@ def test_gloo_world2_frequency_exchange():
         p.join(timeout=60)
     assert [r[1] for r in res] == [True, True]
     assert [r[2] for r in res] == [3.0, 3.0]
+
+
+def test_overlap_entry_points_validate_on_the_host():
+    """The overlap helpers reject bad extents before any device work and size their plans on the host."""
+    from paper_1706_06972_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.ocsc_history_woodbury(4, 8, 40, 3, 17, None, None, 0, 0, 0, None, None, None, 0, 0, None, None,
+                                     None) == -1                       # nb <= 16
+    assert lib.ocsc_history_invert_claim(8, 8, 120, 3, None, 1.0, 1.0, None, None, None, 4, None) == -1
+    assert lib.ocsc_history_woodbury_smem(100, 5) == 16 * (5050 + 3 * 100 * 5 + 25)
+    assert lib.ocsc_history_woodbury_smem(100, 10) == 16 * (5050 + 3 * 100 * 11 + 100)   # odd pitch
+    # plane-resident stream kernel: one CTA per (sample, filter group), at most one wave of 148 SMs
+    ctas = lib.ocsc_code_stream_plane_ctas(4, 100, 100, 100, 10)
+    assert 0 < ctas <= 148 and ctas % 10 == 0
+    assert lib.ocsc_code_stream_plane_ctas(8, 100, 100, 100, 10) == 0
+    assert lib.ocsc_code_stream_plane_ctas(4, 266, 266, 256, 32) == 0
+
+
+def test_committed_launch_list_and_traffic_table_agree():
+    """profiles/traffic.json is what scripts/traffic_from_launches.py derives from the committed
+    launch list (the bench's roofline.traffic comes from it)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "traffic_from_launches.py"),
+                          os.path.join(root, "profiles", "r1_bench_launches.csv")], capture_output=True, text=True,
+                         check=True).stdout
+    assert "k_code_fused" in out
+    t = json.load(open(os.path.join(root, "profiles", "traffic.json")))
+    fused_us = sum(k["us"] for k in t["kernels"] if "k_code_fused" in k["kernel"])
+    assert fused_us / t["step_us_serialised"] > 0.8
+    assert abs(t["fused_bytes_per_batch_iter"] - t["fused_dram_bytes_per_step"] / 300.0) < 1.0
+
+
+def test_bench_fp32_peak_uses_the_measured_fma_rate():
+    import importlib.util
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    peak, src = bench.fp32_peak_tflops(148, 1965.0)
+    assert 60.0 < peak < 74.5 and "measured" in src
