@@ -390,7 +390,6 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     // ---- C: row IFFT -> c -> update w (registers) -> t -> row FFT --------------------------
     // (even, odd) pixel pairs run as 2-wide FP32x2 arithmetic
     C s0 = mkc<C>(0, 0), s1 = mkc<C>(0, 0), s2 = mkc<C>(0, 0), s3 = mkc<C>(0, 0);
-    bool bad = false;
     if (rvalid) {
       C z[M];
       row_inverse_pre<C, N>(xrow, z);
