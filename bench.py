@@ -1,23 +1,27 @@
 #!/usr/bin/env python
 """bench.py -- OCSC training images/sec on B200 (BASELINE.json metric), one JSON line.
 
-Workload (BASELINE.json configs[1]): seeded synthetic 32x32
-images zero-padded to 42x42, K = 100 filters of 11x11, beta = 1,
-rho_code = rho_dict = 1, J = 10 dictionary rounds, <= 300 code iterations,
-float32 arithmetic (float64 history), mini-batch 50 per GPU.  A step is one
-mini-batch through the whole hot path: batched code ADMM -> objective ->
-history fold -> Cholesky -> J dictionary rounds.
+Headline workload (BASELINE.json configs[1]): seeded synthetic 32x32 images
+zero-padded to 42x42, K = 100 filters of 11x11, beta = 1, rho_code = rho_dict = 1, J = 10
+dictionary rounds, <= 300 code iterations, float32 arithmetic (float64 history), global
+mini-batch 50.  A step is one mini-batch through the whole hot path: batched code ADMM ->
+objective -> history fold -> inverse / Cholesky -> J dictionary rounds.  At N = 1 the line also
+carries a "secondary" block with BASELINE configs 2 and 3 (training steps, same contract) and
+config 4 at K = 256 (history accumulation + Cholesky solve), measured in the same run.
 
     python bench.py [--gpus N --steps K --warmup W]            # this build
-    python bench.py --impl reference [--steps K --warmup W]    # CPU reference arm
-    torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1: sample-sharded
+    python bench.py --impl reference [--steps K --warmup W]    # CPU reference arm (oracle port)
+    torchrun --nproc-per-node N bench.py --gpus N ...          # N > 1: strong scaling
 
-Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events
-on the trainer's stream, L2 flushed (256 MiB write) between steps outside the
-events, barrier + synchronize around the block, max over ranks.  `value` has
-the inputs already resident in HBM; `e2e` runs the public API
-(`OnlineTrainer.partial_fit`) on pinned host arrays, H2D of the images and
-D2H of the per-sample objectives inside the timed region.
+Scaling is strong: the global mini-batch of the configuration is split into ragged sample shards
+(50 over 8 ranks = 7,7,6,6,6,6,6,6), so the dictionary is updated once per B samples at every N.
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the trainer's
+stream, L2 flushed (256 MiB write) between steps outside the events, barrier + synchronize
+around the block, max over ranks.  `value` has the inputs already resident in HBM; `e2e` runs
+the public API (`OnlineTrainer.partial_fit`) on pinned host arrays, H2D of the images and D2H
+of the per-sample objectives inside the timed region.  The roofline's kernel time comes from
+CUDA events the trainer records around its code kernels inside the timed steps.
 """
 
 from __future__ import annotations
@@ -38,23 +42,22 @@ sys.path.insert(0, ROOT)
 
 METRIC = "OCSC training images/sec at 1/2/4/8 B200; % of HBM/FP32 roofline per kernel"
 UNIT = "images/s"
-CFG = dict(dims0=(32, 32), grid=(42, 42), fdims=(11, 11), K0=20, K=100, beta=1.0, rho_code=1.0, rho_dict=1.0,
-           J=10, max_iters=300, rel_tol=1e-3, B=50)
-WORKLOAD = ("BASELINE config 1: seeded synthetic 32x32 images zero-padded to 42x42, K=100 filters 11x11, "
-            "beta=1, rho=1, J=10, <=300 code iterations, float32 (history float64), mini-batch 50 per GPU")
-
-
-# secondary training configs; printed as their own lines, not the headline
+# BASELINE.json training configs; config 1 is the headline, 2 and 3 ride along as
+# the line's "secondary" block (or run alone with --config N)
 TRAIN_CFGS = {
+    1: (dict(dims0=(32, 32), grid=(42, 42), fdims=(11, 11), K0=20, K=100, beta=1.0, rho_code=1.0, rho_dict=1.0,
+             J=10, max_iters=300, rel_tol=1e-3, B=50),
+        "BASELINE config 1: seeded synthetic 32x32 images zero-padded to 42x42, K=100 filters 11x11, beta=1, "
+        "rho=1, J=10, <=300 code iterations, float32 (history float64), global mini-batch 50"),
     2: (dict(dims0=(100, 100), grid=(100, 100), fdims=(11, 11), K0=20, K=100, beta=1.0, rho_code=1.0,
              rho_dict=1.0, J=10, max_iters=300, rel_tol=1e-3, B=10),
         "BASELINE config 2: seeded synthetic 100x100 images (no padding), K=100 filters 11x11, beta=1, rho=1, "
-        "J=10, <=300 code iterations, float32 (history float64), mini-batch 10 per GPU"),
+        "J=10, <=300 code iterations, float32 (history float64), global mini-batch 10"),
     3: (dict(dims0=(256, 256), grid=(266, 266), fdims=(11, 11), K0=64, K=256, beta=0.5, rho_code=1.0,
              rho_dict=1.0, J=10, max_iters=300, rel_tol=1e-3, B=32, history="float32"),
         "BASELINE config 3: seeded synthetic 256x256 images zero-padded to 266x266, K=256 filters 11x11, "
         "beta=0.5, rho=1, J=10, <=300 code iterations, float32 with the complex64 history BASELINE sizes "
-        "(9.4 GB packed half spectrum), mini-batch 32 per GPU"),
+        "(9.4 GB packed half spectrum), global mini-batch 32"),
 }
 
 
@@ -65,10 +68,10 @@ def _env_int(name, default):
         return default
 
 
-def make_images(n, start, seed=0):
-    from oracle import ocsc_oracle as O  # bench input generator; not the measured path
-    return O.synth_images(n, CFG["dims0"], CFG["grid"], CFG["K0"], filter_dims=CFG["fdims"], seed=seed,
-                          start=start).reshape(n, -1)
+def make_images(cfg, n, start, seed=0):
+    from paper_1706_06972_b200.workloads import synth_images  # seeded inputs
+    return synth_images(n, cfg["dims0"], cfg["grid"], cfg["K0"], filter_dims=cfg["fdims"], seed=seed,
+                        start=start).reshape(n, -1)
 
 
 # ------------------------------------------------------------------ clocks --
@@ -154,13 +157,35 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_oracle_rate(n_images, budget_s=None, warmup=0):
-    """Images/s of the CPU reference algorithm (oracle port, composed mini-batch of 1) on config 1."""
+def cpu_description():
+    """Host CPU model, thread settings and numpy / BLAS versions."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = []
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": i.get("internal_api"), "version": i.get("version"), "threads": i.get("num_threads")}
+                for i in threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "numpy": np.__version__, "blas": blas,
+            "env": {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")},
+            "note": "numpy FFTs (pocketfft) are single-threaded; the batched inverse/einsum parts use the BLAS threads"}
+
+
+def cpu_oracle_rate(cfg, n_images, budget_s=None, warmup=0):
+    """Images/s of the CPU reference algorithm (oracle port, OnlineTrainer.step = mini-batch of 1)."""
     from oracle import ocsc_oracle as O
-    tr = O.Trainer(CFG["grid"], CFG["fdims"], K=CFG["K"], beta=CFG["beta"], rho_code=CFG["rho_code"],
-                   rho_dict=CFG["rho_dict"], inner_iters=CFG["J"], seed=0, code_max_iters=CFG["max_iters"],
-                   code_rel_tol=CFG["rel_tol"], stop_tol=0.0)
-    X = make_images(n_images + warmup, start=10_000_000)
+    tr = O.Trainer(cfg["grid"], cfg["fdims"], K=cfg["K"], beta=cfg["beta"], rho_code=cfg["rho_code"],
+                   rho_dict=cfg["rho_dict"], inner_iters=cfg["J"], seed=0, code_max_iters=cfg["max_iters"],
+                   code_rel_tol=cfg["rel_tol"], stop_tol=0.0)
+    X = make_images(cfg, n_images + warmup, start=10_000_000)
     for i in range(warmup):
         tr.step_batch(X[i:i + 1])
     done, t0 = 0, time.perf_counter()
@@ -176,48 +201,76 @@ def cpu_oracle_rate(n_images, budget_s=None, warmup=0):
 def run_reference(args, rank):
     if rank != 0:
         return
+    cfg, workload = TRAIN_CFGS[args.config]
     budget = float(os.environ.get("OCSC_REF_BUDGET_S", "150"))
-    rate, done, dt = cpu_oracle_rate(args.steps, budget_s=budget, warmup=min(args.warmup, 1))
+    rate, done, dt = cpu_oracle_rate(cfg, args.steps, budget_s=budget, warmup=min(args.warmup, 1))
     cores = cpu_threads()
-    sample = (f"{done} timed step(s) of 1 image each of config 1 (reference OnlineTrainer.step semantics, "
-              f"oracle/ocsc_oracle.py numpy port), {dt:.1f} s; warm-up {min(args.warmup, 1)} step")
+    sample = (f"{done} timed step(s) of 1 image each of config {args.config} (reference OnlineTrainer.step "
+              f"semantics, oracle/ocsc_oracle.py numpy port, float64), {dt:.1f} s; warm-up {min(args.warmup, 1)} step")
     line = {"metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * dt / max(done, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded planted-dictionary images, SURVEY.md 8(d))",
-            "config": {"workload": WORKLOAD, "global_batch": 1, "parallelism": "cpu"},
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "config": {"workload": workload, "global_batch": 1, "parallelism": "cpu (BLAS threads)"},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                             "host": cpu_description()},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------- GPU legs --
-def run_b200(args, rank, world, local_rank):
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "MEASURED_PEAKS.json (driver-measured)"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback 6650 GB/s (B200_PROFILING.md)"
+
+
+def load_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def code_intervals(tl):
+    """(start, end) events of the code-ADMM kernels per step from the trainer's timeline marks
+    (fused: main + tail launches; stream / cuFFT: the whole coding loop)."""
+    out, start = [], None
+    for label, ev in tl:
+        if label in ("main start", "code start"):
+            start = ev
+        elif label in ("tail end", "code end") and start is not None:
+            out.append((start, ev))
+            start = None
+    return out
+
+
+def train_line(args, cfg_id, rank, world, local_rank, steps, warmup, e2e=True, cpu=True):
+    """One training configuration through the public API; returns the JSON dict (rank 0)."""
     import torch
     import torch.distributed as dist
 
     import paper_1706_06972_b200 as ob
     from paper_1706_06972_b200 import _lib
-    from paper_1706_06972_b200.coding import infer_codes
-    from paper_1706_06972_b200.sharded import DistComm, ShardedTrainer
-    from paper_1706_06972_b200.transforms import rfft2_dev
+    from paper_1706_06972_b200.sharded import DistComm, ShardedTrainer, sample_shards
 
-    torch.cuda.set_device(local_rank)
+    cfg, workload = TRAIN_CFGS[cfg_id]
     dev = torch.device("cuda", local_rank)
     lib = _lib.load()
-    B = args.batch
-    shape = ob.SignalShape(CFG["grid"], CFG["fdims"])
-    cfg = ob.TrainConfig(n_filters=CFG["K"], beta=CFG["beta"], rho_code=CFG["rho_code"], rho_dict=CFG["rho_dict"],
-                         inner_iters=CFG["J"], seed=0, code_max_iters=CFG["max_iters"], code_rel_tol=CFG["rel_tol"],
-                         dtype="float32", history_dtype=CFG.get("history", "float64"), batch_size=B, stop_tol=0.0,
-                         poll=16)
-    # N > 1: samples AND spectrum rows sharded (sharded.py: all_to_all of code spectra, one K x M
-    # all-reduce per dictionary round); N = 1: the plain trainer
-    Trainer = (lambda: ShardedTrainer(shape, cfg, DistComm())) if world > 1 else (lambda: ob.OnlineTrainer(shape, cfg))
-    nsteps = args.warmup + args.steps
+    B = args.batch if (args.batch and cfg_id == args.config) else cfg["B"]
+    mine = sample_shards(B, world)[rank]
+    b = mine.stop - mine.start
+    shape = ob.SignalShape(cfg["grid"], cfg["fdims"])
+    tcfg = ob.TrainConfig(n_filters=cfg["K"], beta=cfg["beta"], rho_code=cfg["rho_code"], rho_dict=cfg["rho_dict"],
+                          inner_iters=cfg["J"], seed=0, code_max_iters=cfg["max_iters"], code_rel_tol=cfg["rel_tol"],
+                          dtype="float32", history_dtype=cfg.get("history", "float64"), batch_size=B, stop_tol=0.0,
+                          poll=16)
+    Trainer = (lambda: ShardedTrainer(shape, tcfg, DistComm())) if world > 1 else (lambda: ob.OnlineTrainer(shape, tcfg))
+    nsteps = warmup + steps
     P = shape.size
-    # rank r owns rows [r*B, (r+1)*B) of each global mini-batch of world*B images
-    X = np.stack([make_images(B, start=(s * world + rank) * B) for s in range(nsteps)]).astype(np.float32)
+    # strong scaling: every step is one global mini-batch of B images; rank r codes its shard
+    X = np.stack([make_images(cfg, B, start=s * B)[mine] for s in range(nsteps)]).astype(np.float32)
 
     def barrier():
         if world > 1:
@@ -231,173 +284,175 @@ def run_b200(args, rank, world, local_rank):
         return float(t.item())
 
     flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.2)
 
     # ---- value: inputs resident in HBM, device-timed --------------------------------
     trainer = Trainer()
     Xd = torch.as_tensor(X).to(dev)
-    for s in range(args.warmup):
+    for s in range(warmup):
         trainer.partial_fit(Xd[s])
     torch.cuda.synchronize()
     barrier()
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    time.sleep(0.2)
     stream = torch.cuda.current_stream()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    iters_sum, iters_max = [], []
     launches0 = lib.ocsc_kernel_launches()
+    trainer._tl = []  # code-kernel start/end events inside the timed steps (the roofline's timer)
     torch.cuda.synchronize()
     barrier()
     t_on = time.perf_counter()
-    for i in range(args.steps):
+    for i in range(steps):
         flush.zero_()
         evs[i][0].record(stream)
-        res = trainer.partial_fit(Xd[args.warmup + i])
+        res = trainer.partial_fit(Xd[warmup + i])
         evs[i][1].record(stream)
+        iters_sum.append(int(np.sum(res.iterations)))
+        iters_max.append(int(np.max(res.iterations)) if len(res.iterations) else 0)
     torch.cuda.synchronize()
     sampler.mark(t_on, time.perf_counter())
     barrier()
     launches = lib.ocsc_kernel_launches() - launches0
-    total_ms = sum(a.elapsed_time(b) for a, b in evs)
-    total_ms = max_over_ranks(total_ms)
-    value = world * B * args.steps / (total_ms / 1e3)
-    iters_mean = float(np.mean(res.iterations))
-
-    # ---- roofline of the dominant kernel: the code ADMM over the mini-batch ----------------
-    # k_code_fused runs every iteration of every sample in one launch; per-iteration time =
-    # launch time / iterations.  Algorithmic bytes per image-iteration are SURVEY.md 8(d)'s
-    # G1-G4 figure (what an HBM-streaming implementation must move); the fused kernel keeps
-    # the state on-chip, so its measured DRAM traffic (profiles/traffic.json) is far lower.
-    xh = rfft2_dev(Xd[0].reshape(B, *CFG["grid"]), shape)
-    cc = trainer.coding_config
-    buf = trainer._buf
-    H, W = CFG["grid"]
-    obj = torch.empty(B, dtype=torch.float64, device=dev)
-    fused = trainer.use_fused(B)
-    from paper_1706_06972_b200.coding import infer_codes_stream, stream_supported
-    streamed = not fused and stream_supported(shape, torch.float32)
-    durs, iters_run = [], 1
-    for _ in range(3):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        if fused:
-            _lib.call("ocsc_code_fused", _lib.F32, H, W, CFG["K"], B, _lib.ptr(xh), _lib.ptr(trainer.Wh),
-                      _lib.ptr(trainer.den), cc.beta, cc.rho, cc.max_iters, cc.rel_tol, _lib.ptr(buf.u), None,
-                      _lib.ptr(trainer._uh), _lib.ptr(obj), None, _lib.ptr(buf.iters), _lib.ptr(buf.status),
-                      _lib.stream())
-        elif streamed:
-            infer_codes_stream(xh, trainer.Wh, trainer.den, shape, cc, buf, B, poll=0)
-        else:
-            infer_codes(xh, trainer.Wh, trainer.den, shape, cc, buf, B, poll=0)
-        b.record(stream)
-        torch.cuda.synchronize()
-        iters_run = max(int(buf.iters[:B].max().item()), 1)
-        durs.append(a.elapsed_time(b) / iters_run)
-    it_ms = min(durs)
-    Pf, Ph, K, s = H * W, H * (W // 2 + 1), CFG["K"], 4
-    bytes_per_img_iter = 8 * Pf * K * s + 8 * Ph * K * s          # SURVEY.md 8(d) G1-G4, algorithmic
-    flops_per_img_iter = 2 * K * 2.5 * Pf * np.log2(Pf) + 16 * Ph * K + 8 * Pf * K
-    achieved = B * bytes_per_img_iter / (it_ms / 1e3) / 1e9       # GB/s
-    achieved_tf = B * flops_per_img_iter / (it_ms / 1e3) / 1e12   # TFLOP/s
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
-    pipe = None
-    try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        pipe = tj.get("fused_ncu_set_full") if fused else None
-        key = ("fused_bytes_per_batch_iter" if fused else
-               f"stream{H}_bytes_per_batch_iter" if streamed else "generic_bytes_per_batch_iter")
-        traffic = tj.get(key)
-    except (OSError, ValueError):
-        pass
+    path = trainer.last_path
+    total_ms = max_over_ranks(sum(a.elapsed_time(b_) for a, b_ in evs))
+    value = B * steps / (total_ms / 1e3)
+    code_ms = [a.elapsed_time(b_) for a, b_ in code_intervals(trainer._tl)]
+    trainer._tl = None
+    code_ms_step = float(np.mean(code_ms)) if code_ms else float("nan")
 
     # ---- e2e: public API, pinned host input, objectives back to host -----------------
-    del trainer, buf
-    torch.cuda.empty_cache()
-    trainer2 = Trainer()
-    Xh = torch.as_tensor(X).pin_memory()
-    for s in range(args.warmup):
-        trainer2.partial_fit(Xh[s])
-    torch.cuda.synchronize()
-    barrier()
-    e2e_s = 0.0
-    for i in range(args.steps):
-        flush.zero_()
+    e2e_line = None
+    if e2e:
+        del trainer
+        torch.cuda.empty_cache()
+        trainer2 = Trainer()
+        Xh = torch.as_tensor(X).pin_memory()
+        for s in range(warmup):
+            trainer2.partial_fit(Xh[s])
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        r2 = trainer2.partial_fit(Xh[args.warmup + i])
-        _ = float(r2.objectives.sum())
-        t1 = time.perf_counter()
-        sampler.mark(t0, t1)
-        e2e_s += t1 - t0
-    barrier()
+        barrier()
+        e2e_s = 0.0
+        for i in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r2 = trainer2.partial_fit(Xh[warmup + i])
+            _ = float(r2.objectives.sum())
+            t1 = time.perf_counter()
+            sampler.mark(t0, t1)
+            e2e_s += t1 - t0
+        barrier()
+        e2e_s = max_over_ranks(e2e_s)
+        e2e_line = {"value": B * steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": b * P * 4,
+                    "d2h_bytes_per_step": (2 * b + 4) * 8}
+        del trainer2
+    else:
+        del trainer
+    torch.cuda.empty_cache()
     clocks = sampler.stop()
+
+    # ---- roofline of the dominant kernel: the code ADMM of the step ------------------------
+    peaks, peak_src = load_peaks()
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     fp32_peak, fp32_src = fp32_peak_tflops(torch.cuda.get_device_properties(dev).multi_processor_count, sm_mhz)
-    achieved_tf = B * flops_per_img_iter / (it_ms / 1e3) / 1e12   # TFLOP/s
-    e2e_s = max_over_ranks(e2e_s)
-    e2e = world * B * args.steps / e2e_s
+    H, W = cfg["grid"]
+    Pf, Ph, K, s = H * W, H * (W // 2 + 1), cfg["K"], 4
+    flops_img_iter = 2 * K * 2.5 * Pf * np.log2(Pf) + 16 * Ph * K + 8 * Pf * K
+    bytes_img_iter = 8 * Pf * K * s + 8 * Ph * K * s
+    flops_step = float(np.mean(iters_sum)) * flops_img_iter
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tj = load_traffic()
+    on_chip = path in ("fused", "fused+split") or (path and path.startswith("stream") and (H, W) == (100, 100))
+    kname = {"fused": "k_code_fused (one cluster per sample, ADMM state in SMEM)",
+             "fused+split": "k_code_fused main + tail launches (one cluster per sample, ADMM state in SMEM)"}.get(
+        path, "k_plane (one CTA per (sample, filter group), planes in SMEM) + k_gsum per iteration"
+        if on_chip else "k_rows + k_cols_f + k_gsum + k_cols_i per iteration (state streamed through HBM)")
+    it_ms = code_ms_step / max(float(np.mean(iters_max)), 1.0)
+    traffic_key = ("fused_bytes_per_batch_iter" if path and path.startswith("fused") else
+                   f"plane{H}_bytes_per_batch_iter" if on_chip else f"stream{H}_bytes_per_batch_iter")
+    traffic = tj.get(traffic_key)
+    if on_chip:
+        achieved = flops_step / (code_ms_step / 1e3) / 1e12
+        roof = {"bound": "fp32", "kernel": kname, "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": traffic,
+                "algorithmic": "SURVEY 8(d) flops 2K*2.5*P*log2(P) + 16*Ph*K + 8*P*K per image-iteration x the "
+                               "iterations each sample ran",
+                "peak_source": fp32_src, "code_ms_per_step": code_ms_step, "iter_ms": it_ms,
+                "timer": "CUDA events on the launching streams around the code kernels of every timed step",
+                "hbm_equivalent": {"achieved_GB/s": float(np.mean(iters_sum)) * bytes_img_iter / code_ms_step / 1e6,
+                                   "peak": hbm, "note": "SURVEY 8(d) G1-G4 bytes an HBM-streaming design would "
+                                   "move; this kernel keeps the state on chip (traffic = measured DRAM bytes per "
+                                   "mini-batch iteration)"}}
+        pipe = tj.get("fused_ncu_set_full") if path.startswith("fused") else None
+        if pipe:
+            roof["ncu_fma_pipe_active_pct"] = pipe.get("sm__pipe_fma_cycles_active_pct_of_peak_active")
+            roof["ncu_source"] = pipe.get("source")
+    else:
+        achieved = (traffic or float("nan")) / (it_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": traffic,
+                "algorithmic": "measured DRAM bytes (ncu) of one mini-batch iteration of the streaming kernels "
+                               "(profiles/traffic.json)", "peak_source": peak_src, "code_ms_per_step": code_ms_step,
+                "iter_ms": it_ms, "fp32_equivalent": {"achieved_TFLOP/s": flops_step / code_ms_step / 1e9,
+                                                       "peak": fp32_peak}}
 
     # ---- CPU baseline (rank 0, N = 1 only) -------------------------------------------
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.config == 3:
-            # the reference keeps full-spectrum complex128 inverses: 70,756 x 256 x 256 x 16 B = 74 GB
-            cpu = {"value": None, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                   "sample": "n/a (memory): the reference's inv_gram for config 3 alone is 74 GB of complex128 "
-                             "(dictionary.py:30-54), plus >= 3 same-size temporaries in update_history"}
+    cpu_line = None
+    if cpu and rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if cfg_id == 3:
+            cpu_line = {"value": None, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                        "sample": "n/a (memory): the reference's inv_gram for config 3 alone is 74 GB of complex128 "
+                                  "(dictionary.py:30-54), plus >= 3 same-size temporaries in update_history"}
         else:
-            n = int(os.environ.get("OCSC_CPU_SAMPLE_IMAGES", "3" if args.config == 1 else "1"))  # ~12 s of CPU work
-            rate, done, dt = cpu_oracle_rate(n)
-            cpu = {"value": rate, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                   "sample": f"{done} image(s) of config {args.config} through oracle/ocsc_oracle.py (reference "
-                             f"algorithm, OnlineTrainer.step semantics, float64), {dt:.1f} s on host cores"}
+            n = int(os.environ.get("OCSC_CPU_SAMPLE_IMAGES", "3" if cfg_id == 1 else "1"))  # ~12 s of CPU work
+            rate, done, dt = cpu_oracle_rate(cfg, n)
+            cpu_line = {"value": rate, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                        "sample": f"{done} image(s) of config {cfg_id} through oracle/ocsc_oracle.py (reference "
+                                  f"algorithm, OnlineTrainer.step semantics, float64), {dt:.1f} s on host cores",
+                        "host": cpu_description()}
 
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warmup, "ms_per_step": total_ms / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded planted-dictionary images, SURVEY.md 8(d))",
+            "config": {"workload": workload, "global_batch": B, "per_rank_batch": b, "path": path,
+                       "code_iterations_mean": float(np.mean(iters_sum)) / max(b, 1),
+                       "l2": "flushed between timed steps (256 MiB device write outside the events)",
+                       "parallelism": (f"dp{world} x freq{world}: the global mini-batch of {B} split into ragged "
+                                       f"sample shards, history and dictionary ADMM sharded by spectrum rows "
+                                       f"(all_to_all of code spectra + K x M all-reduce per round)" if world > 1 else
+                                       "single GPU")},
+            "roofline": roof, "cpu_baseline": cpu_line, "e2e": e2e_line, "gpu_launches": int(launches),
+            "clocks": clocks}
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    line = train_line(args, args.config, rank, world, local_rank, args.steps, args.warmup)
+    if args.config == 1 and (world == 1 or args.secondary) and not args.no_secondary:
+        # the other BASELINE configurations in the same run (driver-visible)
+        sec = {}
+        for cid, st, wu in ((2, 5, 2), (3, 2, 1)):
+            try:
+                sec[f"config{cid}"] = train_line(args, cid, rank, world, local_rank, st, wu, e2e=(cid == 2),
+                                                 cpu=False)
+            except Exception as e:  # a secondary failure must not lose the headline
+                sec[f"config{cid}"] = {"error": f"{type(e).__name__}: {e}"}
+        try:
+            args_k = argparse.Namespace(**vars(args))
+            args_k.ks, args_k.steps, args_k.warmup = [256], 3, 1
+            sec["config4_K256"] = run_history_microbench(args_k, rank, world, local_rank, emit=False)[0]
+        except Exception as e:
+            sec["config4_K256"] = {"error": f"{type(e).__name__}: {e}"}
+        line["secondary"] = sec
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic (seeded planted-dictionary images, SURVEY.md 8(d))",
-                "config": {"workload": WORKLOAD, "global_batch": world * B, "per_gpu_batch": B,
-                           "code_iterations_mean": iters_mean,
-                           "l2": "flushed between timed steps (256 MiB device write outside the events)",
-                           "parallelism": (f"dp{world} x freq{world} (sample-sharded coding; history and "
-                                           f"dictionary ADMM sharded by spectrum rows; all_to_all of code "
-                                           f"spectra + K x M all-reduce per round)" if world > 1 else
-                                           "single GPU")},
-                "roofline": {"bound": "hbm",
-                             "kernel": ("k_code_fused (cluster per sample, state in SMEM), one ADMM iteration over "
-                                        "the mini-batch" if fused else
-                                        "plane-resident streaming code ADMM (k_plane: one CTA per (sample, filter "
-                                        "group), planes in SMEM), one iteration over the mini-batch"
-                                        if streamed and (H, W) == (100, 100) else
-                                        "streaming code ADMM (k_rows + k_cols_f + k_cols_i), one iteration over the "
-                                        "mini-batch" if streamed else "cuFFT code-ADMM iteration over the mini-batch"),
-                             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                             "traffic": traffic, "iter_ms": it_ms, "iterations": iters_run,
-                             "algorithmic_bytes_per_batch_iter": B * bytes_per_img_iter,
-                             "note": "algorithmic bytes = SURVEY 8(d) G1-G4 (an HBM-streaming design's traffic); "
-                                     "the fused kernel keeps the ADMM state on-chip, traffic = measured DRAM bytes",
-                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback"},
-                "roofline_fp32": {"achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-                                  "frac": achieved_tf / fp32_peak,
-                                  "flops": "SURVEY 8(d): 2K*2.5*P*log2(P) + 16*Ph*K + 8*P*K per image-iteration",
-                                  "peak_source": fp32_src,
-                                  "ncu_fma_pipe_active_pct": pipe and pipe.get("sm__pipe_fma_cycles_active_pct_of_peak_active"),
-                                  "ncu_source": pipe and pipe.get("source")},
-                "cpu_baseline": cpu,
-                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": B * P * 4,
-                        "d2h_bytes_per_step": (2 * B + 4) * 8},
-                "gpu_launches": int(launches), "clocks": clocks}
         print(json.dumps(line), flush=True)
 
 
-def run_history_microbench(args, rank, world, local_rank):
+def run_history_microbench(args, rank, world, local_rank, emit=True):
     """BASELINE config 4: per-frequency rank-64 history accumulation + (A + rho I) Cholesky solve.
 
     P = 128 x 128 independent frequencies (full grid: random codes are not Hermitian),
@@ -424,6 +479,7 @@ def run_history_microbench(args, rank, world, local_rank):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     shape = ob.SignalShape((P,), (1,))
+    lines = []
     for K in args.ks:
         z = torch.complex(torch.randn(B, P, K, device=dev, generator=gen),
                           torch.randn(B, P, K, device=dev, generator=gen)) / np.sqrt(2)
@@ -475,9 +531,11 @@ def run_history_microbench(args, rank, world, local_rank):
                                    "frac_fp32": g7_flops / (tf + ts) / 1e9 / fp32},
                 "peaks": {"hbm_GB/s": hbm, "fp32_TFLOP/s_nominal": fp32},
                 "parity_rel_err_vs_dense_c128": err, "data": "synthetic CN(0,1), seeded"}
-        if rank == 0:
+        lines.append(line)
+        if rank == 0 and emit:
             print(json.dumps(line), flush=True)
         del z, x
+    return lines
 
 
 def run_preprocess_microbench(args, rank, world, local_rank):
@@ -579,12 +637,9 @@ def main():
                     help="1: BASELINE config 1 training step (default); 2, 3: BASELINE configs 2 and 3; "
                          "4: history + Cholesky microbenchmark; 5: image preprocessing (row f4)")
     ap.add_argument("--ks", type=int, nargs="+", default=[64, 128, 256, 512], help="K values for --config 4")
+    ap.add_argument("--no-secondary", action="store_true", help="headline config 1 only (no configs 2-4 block)")
+    ap.add_argument("--secondary", action="store_true", help="also run the secondary block at N > 1")
     args = ap.parse_args()
-    global CFG, WORKLOAD
-    if args.config in TRAIN_CFGS:
-        CFG, WORKLOAD = TRAIN_CFGS[args.config]
-    if args.batch is None:
-        args.batch = CFG["B"]
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local_rank = _env_int("LOCAL_RANK", 0)
@@ -592,6 +647,10 @@ def main():
         import torch
         local_rank %= max(torch.cuda.device_count(), 1)
     if args.impl == "reference":
+        if args.config not in TRAIN_CFGS:
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "the reference arm times training configs 1-3"}))
+            return
         run_reference(args, rank)
         return
     if world > 1:
@@ -601,6 +660,7 @@ def main():
         # OCSC_BENCH_BACKEND=gloo is a functional check of the N > 1 code path on a box with fewer
         # GPUs than ranks (host-staged collectives; never a reported number)
         backend = os.environ.get("OCSC_BENCH_BACKEND", "nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # NVLS / transport selection in the log (stderr)
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:

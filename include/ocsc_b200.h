@@ -191,9 +191,10 @@ int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, 
                           int32_t* info, const void* x, int64_t x_sb, int64_t x_sp, void* S, void* c,
                           void* stream);
 size_t ocsc_history_woodbury_smem(int K, int nb);
-/* Large K (multiple of 32; BASELINE configs 3-4): blocked right-looking Cholesky of
- * S_p + ridge I per frequency (one CTA per frequency, 32x32 tiles, panel staged in shared
- * memory, one warp per trailing tile).  L is written full (nfreq, K, K), lower triangle;
+/* Large K (BASELINE configs 3-4; any K): blocked right-looking Cholesky of S_p + ridge I per
+ * frequency (one CTA per frequency, 32x32 tiles, panel staged in shared memory).  L is written
+ * full (nfreq, Kp, Kp), lower triangle, Kp = K rounded up to a multiple of 32 (the padding is
+ * the decoupled block ridge * I, so rows/columns >= K never touch the history's solution);
  * ocsc_history_factor_bytes gives its size.  info as ocsc_history_invert. */
 size_t ocsc_history_factor_bytes(int dtype_hist, int K, int nfreq);
 int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void* S, double ridge, void* L,
@@ -214,7 +215,8 @@ int ocsc_dict_rowsolve(int dtype, int dtype_hist, int dtype_inv, int K, int nfre
                        const void* c, double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
                        void* Dh, void* stream);
 /* Row solve with the Cholesky factor of ocsc_history_factor (two triangular solves per
- * frequency): conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)). */
+ * frequency): conj(D_p) = L^-H L^-1 (c_p + ridge conj(V_p - Theta_p)).  K is the history's
+ * order (L padded as ocsc_history_factor writes it). */
 int ocsc_dict_rowsolve_chol(int dtype, int dtype_hist, int K, int nfreq, const void* L, const void* c,
                             double ridge, const void* Vh, const void* Th, int64_t sk, int64_t sp,
                             void* Dh, void* stream);

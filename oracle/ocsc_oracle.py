@@ -345,35 +345,6 @@ def train_online(samples, dims, filter_dims, batch_size=1, max_passes=10, **kw):
     return report
 
 
-# ------------------------------------------------------- synthetic workload --
-
-def synth_images(n: int, dims0, grid, K0: int, filter_dims=(11, 11), seed: int = 0,
-                 density: float = 0.01, noise: float = 0.01, start: int = 0) -> np.ndarray:
-    """Seeded planted-dictionary images of SURVEY.md 8(d) / BASELINE.json configs.
-
-    Ground-truth filters from default_rng(seed) (M, K0) ~ N(0,1), unit columns;
-    image i uses default_rng([seed, i]): codes N(0,1) * [U < density] on the
-    unpadded grid, circular convolution (transforms.py:137-141 convention),
-    + noise * N(0,1), standardised to zero mean / unit variance, then
-    zero-padded bottom/right to `grid`.  Returns (n, Hg, Wg) float64.
-    """
-    H0, W0 = grid_of(dims0)
-    Hg, Wg = grid_of(grid)
-    M0, M1 = fdims_of(filter_dims)
-    f = np.random.default_rng(seed).normal(size=(M0 * M1, K0))
-    f = f / np.linalg.norm(f, axis=0)
-    fh = fwd(pad(f, H0, W0, M0, M1))                      # (K0, H0, W0)
-    out = np.zeros((n, Hg, Wg))
-    for j in range(n):
-        rng = np.random.default_rng([seed, start + j])
-        codes = rng.normal(size=(K0, H0, W0)) * (rng.random(size=(K0, H0, W0)) < density)
-        img = np.fft.ifft2((fh * fwd(codes)).sum(axis=0)).real
-        img = img + noise * rng.normal(size=(H0, W0))
-        img = (img - img.mean()) / img.std()
-        out[j, :H0, :W0] = img
-    return out
-
-
 # ---------------------------------------------------------- preprocessing --
 # preprocessing.py:13-100 (row f4): grayscale, Gaussian LCN, seeded edge taper.  scipy's
 # correlate1d(mode="reflect") is restated as np.pad(mode="symmetric") + a sliding dot product
@@ -432,12 +403,3 @@ def taper(a, size=11, sigma=2.0):
 def preprocess(image, window=9, sigma=3.0, eps=1e-4, size=11, sigma_range=(1.0, 3.0), seed=0):
     s = float(np.random.default_rng(seed).uniform(*sigma_range))
     return taper(lcn(gray(image), window, sigma, eps), size, s)
-
-
-# BASELINE.json configs; rho_code = rho_dict = 1 (BASELINE "rho=1").
-CONFIGS = {
-    0: dict(n=10, dims0=(100, 100), grid=(100, 100), K0=20, K=100, beta=1.0, B=1, passes=1, dtype="float64"),
-    1: dict(n=50_000, dims0=(32, 32), grid=(42, 42), K0=20, K=100, beta=1.0, B=50, passes=1, dtype="float32"),
-    2: dict(n=1_000, dims0=(100, 100), grid=(100, 100), K0=20, K=100, beta=1.0, B=10, passes=2, dtype="float32"),
-    3: dict(n=2_000, dims0=(256, 256), grid=(266, 266), K0=64, K=256, beta=0.5, B=32, passes=1, dtype="float32"),
-}

@@ -61,8 +61,10 @@ __device__ __forceinline__ void cmac_conj2(C& acc, C a, C as, decltype(C::x) bx,
 // NT = 256 (8 warps; two CTAs per SM where shared memory allows) or 512 (16 warps, two 64 x 64
 // block pairs of the trailing update at a time: K = 512, where one CTA fills the SM anyway)
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT) k_chol_blocked(int K, const cx<T>* __restrict__ S, T ridge, cx<T>* Lall,
-                                                          int32_t* info) {
+__global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>* __restrict__ S, T ridge,
+                                                          cx<T>* Lall, int32_t* info) {
+  // K: factored order (a multiple of 32); Kv <= K: the history's order (S packed with Kv). Rows
+  // and columns Kv..K-1 are the decoupled padding ridge * I, so L = diag(chol(A), sqrt(ridge) I).
   using C = cx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LD = CT + 1;
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, const cx<T>* __restr
   const int nb = K / CT;
   const int p = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t npk = (int64_t)K * (K + 1) / 2;
+  const int64_t npk = (int64_t)Kv * (Kv + 1) / 2;
   const C* Sp = S + (int64_t)p * npk;
   C* L = Lall + (int64_t)p * K * K;
   const int PR = K - CT + 64;  // panel row stride: K - CT rows + slack for the last 64-block
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, const cx<T>* __restr
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int j = j0 + 32 * u;
-        v[u] = j <= i ? src[j] : mkc<C>(0, 0);
+        v[u] = j <= i && i < Kv ? src[j] : mkc<C>(0, 0);
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(chol_reg_threads<K>()) k_chol_rb(const cx<T>* 
 // y_b -= L_>b,b^H x_>b as the transposed tile GEMV (column sums through shared memory), then
 // L_bb^H x_b = y_b by warp 0.  Every element of L is read once per direction.
 template <typename Tc, typename Th>
-__global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __restrict__ Lall,
+__global__ void __launch_bounds__(256) k_rowsolve_chol(int K, int Kv, const cx<Th>* __restrict__ Lall,
                                                        const cx<Th>* __restrict__ c, Th ridge,
                                                        const cx<Tc>* __restrict__ Vh, const cx<Tc>* __restrict__ Th_,
                                                        int64_t sk, int64_t sp, cx<Tc>* Dh) {
@@ -453,10 +455,14 @@ __global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __re
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int tr = tid >> 3, tq = (tid & 7) * 4;  // tile row, first of 4 tile columns
   const C* L = Lall + (int64_t)p * K * K;
-  for (int k = tid; k < K; k += 256) {
+  for (int k = tid; k < K; k += 256) {  // padding rows (k >= Kv) have a zero right-hand side
+    if (k >= Kv) {
+      y[k] = mkc<C>(0, 0);
+      continue;
+    }
     const int64_t o = (int64_t)k * sk + (int64_t)p * sp;
     const C v = csub(ccast<Th>(Vh[o]), ccast<Th>(Th_[o]));
-    const C ck = c[(int64_t)p * K + k];
+    const C ck = c[(int64_t)p * Kv + k];
     y[k] = mkc<C>(ck.x + ridge * v.x, ck.y - ridge * v.y);
   }
   __syncthreads();
@@ -545,7 +551,7 @@ __global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __re
     }
     __syncthreads();
   }
-  for (int j = tid; j < K; j += 256)
+  for (int j = tid; j < Kv; j += 256)
     Dh[(int64_t)j * sk + (int64_t)p * sp] = mkc<cx<Tc>>((Tc)y[j].x, (Tc)-y[j].y);
 }
 
@@ -553,15 +559,20 @@ __global__ void __launch_bounds__(256) k_rowsolve_chol(int K, const cx<Th>* __re
 
 using namespace ocsc;
 
+// the factor of a K that is not a multiple of 32 is stored padded to the next multiple
+static int chol_order(int K) { return K % CT ? (K / CT + 1) * CT : K; }
+
 extern "C" size_t ocsc_history_factor_bytes(int dtype_hist, int K, int nfreq) {
-  return (size_t)(dtype_hist == OCSC_F64 ? 16 : 8) * (size_t)K * K * nfreq;
+  const size_t Kp = (size_t)chol_order(K);
+  return (size_t)(dtype_hist == OCSC_F64 ? 16 : 8) * Kp * Kp * nfreq;
 }
 
 extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void* S, double ridge, void* L,
                                    int32_t* info, void* stream) {
   if (K <= 0 || nfreq < 0) return fail(OCSC_ESHAPE, "history_factor: bad extents");
-  if (K % CT) return fail(OCSC_EARG, "history_factor: K must be a multiple of 32");
   cudaStream_t s = as_stream(stream);
+  const int Kv = K;
+  K = chol_order(K);
   OCSC_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (nfreq == 0) return OCSC_OK;
   const int nb = K / CT;
@@ -580,14 +591,14 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
     OCSC_LAUNCHED("k_chol_rb");                                                                              \
     return OCSC_OK;                                                                                          \
   }
-  if (!getenv("OCSC_CHOL_NOREG")) {  // dev knob: the shared-memory / blocked kernels instead
+  if (K == Kv && !getenv("OCSC_CHOL_NOREG")) {  // dev knob: the shared-memory / blocked kernels instead
     OCSC_CHOL_REG(32)
     OCSC_CHOL_REG(64)
     OCSC_CHOL_REG(96)
     OCSC_CHOL_REG(128)
   }
 #undef OCSC_CHOL_REG
-  if (K <= 64) {  // small K: the whole matrix in one CTA's shared memory, many CTAs per SM
+  if (K == Kv && K <= 64) {  // small K: the whole matrix in one CTA's shared memory, many CTAs per SM
     const int threads = 64;
     if (dtype_hist == OCSC_F32) {
       OCSC_CUDA(cudaFuncSetAttribute(k_chol_smem<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)whole));
@@ -607,13 +618,13 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
   if (smem > 227 * 1024) return fail(OCSC_EARG, "history_factor: panel exceeds shared memory for this K/dtype");
   if (dtype_hist == OCSC_F32 && K >= 384) {
     OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<float, 512><<<nfreq, 512, smem, s>>>(K, (const float2*)S, (float)ridge, (float2*)L, info);
+    k_chol_blocked<float, 512><<<nfreq, 512, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
   } else if (dtype_hist == OCSC_F32) {
     OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<float, 256><<<nfreq, 256, smem, s>>>(K, (const float2*)S, (float)ridge, (float2*)L, info);
+    k_chol_blocked<float, 256><<<nfreq, 256, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
   } else if (dtype_hist == OCSC_F64) {
     OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<double, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<double, 256><<<nfreq, 256, smem, s>>>(K, (const double2*)S, ridge, (double2*)L, info);
+    k_chol_blocked<double, 256><<<nfreq, 256, smem, s>>>(K, Kv, (const double2*)S, ridge, (double2*)L, info);
   } else {
     return fail(OCSC_EARG, "dtype must be 4 or 8");
   }
@@ -627,10 +638,11 @@ extern "C" int ocsc_dict_rowsolve_chol(int dtype, int dtype_hist, int K, int nfr
   if (K <= 0 || nfreq < 0) return fail(OCSC_ESHAPE, "dict_rowsolve_chol: bad extents");
   if (nfreq == 0) return OCSC_OK;
   cudaStream_t s = as_stream(stream);
-  if (K % CT) return fail(OCSC_EARG, "dict_rowsolve_chol: K must be a multiple of 32");
+  const int Kv = K;
+  K = chol_order(K);
   const size_t smem = (dtype_hist == OCSC_F64 ? 16 : 8) * ((size_t)K + CT * (CT + 1));
 #define RC(TC, TH)                                                                                          \
-  k_rowsolve_chol<TC, TH><<<nfreq, 256, smem, s>>>(K, (const cx<TH>*)L, (const cx<TH>*)c, (TH)ridge,        \
+  k_rowsolve_chol<TC, TH><<<nfreq, 256, smem, s>>>(K, Kv, (const cx<TH>*)L, (const cx<TH>*)c, (TH)ridge,        \
                                                    (const cx<TC>*)Vh, (const cx<TC>*)Th, sk, sp, (cx<TC>*)Dh)
   if (dtype == OCSC_F32 && dtype_hist == OCSC_F32) RC(float, float);
   else if (dtype == OCSC_F32 && dtype_hist == OCSC_F64) RC(float, double);

@@ -67,6 +67,21 @@ template <typename C> __device__ __forceinline__ void cfmac(C& acc, C a, C b) {
   acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
 }
 
+// acc += conj(a) * b with the product rounded on its own before the (uncontracted) add, so
+// a sum over repeated identical terms is exactly that multiple of one term (duplicating every
+// sample of a corpus leaves the averaged history bit-identical, as in the reference's numpy
+// sums; reference tests/test_training.py:180-195)
+__device__ __forceinline__ void cmacc_sep(double2& acc, double2 a, double2 b) {
+  const double px = fma(a.x, b.x, a.y * b.y), py = fma(a.x, b.y, -(a.y * b.x));
+  acc.x = __dadd_rn(acc.x, px);
+  acc.y = __dadd_rn(acc.y, py);
+}
+__device__ __forceinline__ void cmacc_sep(float2& acc, float2 a, float2 b) {
+  const float px = fmaf(a.x, b.x, a.y * b.y), py = fmaf(a.x, b.y, -(a.y * b.x));
+  acc.x = __fadd_rn(acc.x, px);
+  acc.y = __fadd_rn(acc.y, py);
+}
+
 // ---- 2-wide arithmetic: Blackwell FP32x2 (FADD2/FMUL2/FFMA2) for float2, plain for double2 ----
 __device__ __forceinline__ float2 vadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 vmul(float2 a, float2 b) { return __fmul2_rn(a, b); }

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
     __syncthreads();
     for (int k = threadIdx.x; k < K; k += blockDim.x) {
       Ci acc = mkc<Ci>(0, 0);
-      for (int bb = 0; bb < bc; ++bb) cfmac(acc, xs[bb], Zs[bb * K + k]);
+      for (int bb = 0; bb < bc; ++bb) cmacc_sep(acc, xs[bb], Zs[bb * K + k]);
       C& dst = c[(int64_t)p * K + k];
       dst = cadd(dst, ccast<Th>(acc));
     }
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256) k_hist_accum(int K, int nf, int B, int BC
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) cfmac(acc[r][q], zj[q], zi[r]);  // z_i conj(z_j)
+          for (int q = 0; q < 4; ++q) cmacc_sep(acc[r][q], zj[q], zi[r]);  // z_i conj(z_j)
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {

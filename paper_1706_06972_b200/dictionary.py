@@ -62,8 +62,8 @@ class HistoryState:
         self.inv_dtype = dtype if inv_dtype is None else inv_dtype
         if solver == "auto":
             solver = "gj" if self.K <= self.GJ_MAX_K[dtype] else "chol"
-        if solver == "chol" and self.K % 32:
-            raise ValueError(f"the blocked Cholesky path needs K % 32 == 0 (K={self.K})")
+        if solver not in ("gj", "chol"):
+            raise ValueError(f"history solver must be 'gj', 'chol' or 'auto', got {solver!r}")
         self.solver = solver      # "gj": explicit packed inverse; "chol": blocked Cholesky factor
         self._inv = None          # packed (S + t rho P I)^-1, valid for count == _inv_count
         self._inv_count = -1
@@ -95,19 +95,44 @@ class HistoryState:
         """(P, K, K) exact inverse of (averaged Gram + rho P I)."""
         if self.count == 0:
             return np.zeros((self.nfreq, self.K, self.K), dtype=np.complex128)
-        inv = self.inverse()
-        full = torch.empty((self.nfreq, self.K, self.K), dtype=inv.dtype, device=inv.device)
-        _lib.call("ocsc_packed_to_full", _lib.code(inv.dtype), self.K, self.nfreq, _lib.ptr(inv),
-                  float(self.count), _lib.ptr(full), _lib.stream())
-        return _np(full).astype(np.complex128)
+        return _np(self._inv_gram_dev()).astype(np.complex128)
 
-    def gram(self) -> np.ndarray:
-        """(P, K, K) averaged Gram (1/t) sum z z^H (reconstruct_gram's value, exact)."""
+    def _inv_gram_dev(self) -> torch.Tensor:
+        """t (S + t rho P I)^-1 on the device, full (nfreq, K, K) layout."""
+        if self.solver == "gj":
+            inv = self.inverse()
+            full = torch.empty((self.nfreq, self.K, self.K), dtype=inv.dtype, device=inv.device)
+            _lib.call("ocsc_packed_to_full", _lib.code(inv.dtype), self.K, self.nfreq, _lib.ptr(inv),
+                      float(self.count), _lib.ptr(full), _lib.stream())
+            return full
+        # Cholesky path: column j of A^-1 is the row solve of the unit vector e_j with c = 0
+        # (conj(d) = L^-H L^-1 (0 + 1 * conj(e_j))), one launch per column
+        L = self.factor()
+        dt = self.S.dtype
+        K, nf = self.K, self.nfreq
+        zero_c = torch.zeros((nf, K), dtype=dt, device=self.S.device)
+        unit = torch.zeros((nf, K), dtype=dt, device=self.S.device)
+        zero_t = torch.zeros_like(unit)
+        col = torch.empty_like(unit)
+        full = torch.empty((nf, K, K), dtype=dt, device=self.S.device)
+        for j in range(K):
+            unit.zero_()
+            unit[:, j] = 1.0
+            _lib.call("ocsc_dict_rowsolve_chol", _lib.code(dt), _lib.code(dt), K, nf, _lib.ptr(L), _lib.ptr(zero_c),
+                      1.0, _lib.ptr(unit), _lib.ptr(zero_t), 1, K, _lib.ptr(col), _lib.stream())
+            full[:, :, j] = col.conj() * self.count
+        return full
+
+    def _gram_dev(self) -> torch.Tensor:
         full = torch.empty((self.nfreq, self.K, self.K), dtype=self.S.dtype, device=self.S.device)
         scale = 1.0 / self.count if self.count else 0.0
         _lib.call("ocsc_packed_to_full", _lib.code(self.S.dtype), self.K, self.nfreq, _lib.ptr(self.S), scale,
                   _lib.ptr(full), _lib.stream())
-        return _np(full).astype(np.complex128)
+        return full
+
+    def gram(self) -> np.ndarray:
+        """(P, K, K) averaged Gram (1/t) sum z z^H (reconstruct_gram's value, exact)."""
+        return _np(self._gram_dev()).astype(np.complex128)
 
     # -- device operations ---------------------------------------------------
     def accumulate(self, z: torch.Tensor, zs: tuple[int, int, int], x: torch.Tensor, xs: tuple[int, int],
@@ -119,10 +144,12 @@ class HistoryState:
         self.count += B
 
     def factor(self, check: bool = True) -> torch.Tensor:
-        """Full-layout Cholesky factor L of S + t rho P I (large-K path, cached)."""
+        """Full-layout Cholesky factor L of S + t rho P I (large-K path, cached); (nfreq, Kp, Kp)
+        with Kp = K rounded up to a multiple of 32 (decoupled ridge * I padding)."""
         if self._inv is None:
             nbytes = _lib.load().ocsc_history_factor_bytes(_lib.code(self.S.dtype), self.K, self.nfreq)
-            self._inv = torch.empty((self.nfreq, self.K, self.K), dtype=self.S.dtype, device=self.S.device)
+            Kp = -(-self.K // 32) * 32
+            self._inv = torch.empty((self.nfreq, Kp, Kp), dtype=self.S.dtype, device=self.S.device)
             assert self._inv.numel() * self._inv.element_size() == nbytes
         if self._inv_count != self.count:
             _lib.call("ocsc_history_factor", _lib.code(self.S.dtype), self.K, self.nfreq, _lib.ptr(self.S),

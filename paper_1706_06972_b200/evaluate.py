@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from .coding import CodeBuffers, CodingConfig, code_den, code_objectives, infer_codes
-from .errors import ShapeMismatchError
+from .errors import DivergenceError, ShapeMismatchError
 from .transforms import SignalShape, rfft2_dev
 
 PSNR_PEAK_SQ = 255.0 ** 2  # evaluate.py:18
@@ -35,6 +35,9 @@ def evaluate_dictionary(filters, samples, shape: SignalShape, coding: CodingConf
     samples = np.atleast_2d(np.asarray(samples, dtype=np.float64))
     if samples.shape[1] != shape.size:
         raise ShapeMismatchError(f"samples must be (N, {shape.size}), got {samples.shape}")
+    if filters.ndim != 2 or filters.shape[0] != shape.filter_size:
+        # the reference raises here through pad_filter_cols (transforms.py:179-196)
+        raise ShapeMismatchError(f"filters must be ({shape.filter_size}, K), got {filters.shape}")
     rdt = torch.float32 if dtype == "float32" else torch.float64
     cdt = torch.complex64 if rdt == torch.float32 else torch.complex128
     dev = _lib.device()
@@ -56,6 +59,10 @@ def evaluate_dictionary(filters, samples, shape: SignalShape, coding: CodingConf
         x = torch.as_tensor(chunk.reshape(b, H, W), dtype=rdt).to(dev)
         xh = rfft2_dev(x, shape)
         infer_codes(xh, Wh, den, shape, coding, buf, b)
+        status = buf.status[:b].cpu()
+        if bool((status == 2).any()):  # coding.py:105-106, as the reference's infer_code raises
+            it = int(buf.iters[:b][status.to(buf.iters.device) == 2].min().cpu())
+            raise DivergenceError(f"code solver diverged at iteration {it}")
         obj, resid = code_objectives(xh, Wh, buf.u, shape, coding.beta, b, uh, want_resid=True)
         objs.extend(obj.cpu().tolist())
         errs.extend(resid.cpu().tolist())

@@ -109,7 +109,10 @@ _STATE = ("Wh", "den", "Dh", "Th", "alpha", "_prev_alpha")
 
 
 def save_checkpoint(trainer, path) -> None:
-    """Every piece of an OnlineTrainer's state -> one `.npz` (resumable)."""
+    """Every piece of an OnlineTrainer's state -> one `.npz` (resumable).  A ShardedTrainer writes
+    one file per rank (`ShardedTrainer.save_checkpoint`; reload with `ShardedTrainer.load_checkpoint`)."""
+    if getattr(trainer, "_collective", False):
+        return trainer.save_checkpoint(path)
     h = trainer.history
     arrays = {name: getattr(trainer, name).detach().cpu().numpy() for name in _STATE}
     arrays["hist_S"] = h.S.detach().cpu().numpy()

@@ -143,15 +143,15 @@ class _HalfHistory(HistoryState):
             return np.zeros((self.shape.size, self.K), dtype=np.complex128)
         return _np(self._extend(self.c / self.count)).astype(np.complex128)
 
+    def gram(self) -> np.ndarray:
+        """Averaged Gram over all P frequencies (the half spectrum's mirror is its conjugate)."""
+        return _np(self._extend(self._gram_dev())).astype(np.complex128)
+
     @property
     def inv_gram(self) -> np.ndarray:
         if self.count == 0:
             return np.zeros((self.shape.size, self.K, self.K), dtype=np.complex128)
-        inv = self.inverse()
-        full = torch.empty((self.nfreq, self.K, self.K), dtype=inv.dtype, device=inv.device)
-        _lib.call("ocsc_packed_to_full", _lib.code(inv.dtype), self.K, self.nfreq, _lib.ptr(inv),
-                  float(self.count), _lib.ptr(full), _lib.stream())
-        return _np(self._extend(full)).astype(np.complex128)
+        return _np(self._extend(self._inv_gram_dev())).astype(np.complex128)
 
 
 class OnlineTrainer:
@@ -197,6 +197,7 @@ class OnlineTrainer:
         self._fused_ok = {}
         self._side = None          # side stream + scratch of the overlapped history inverse
         self._tl = None            # dev aid: list collecting (label, timing event) of the overlap
+        self.last_path = None      # device path of the last partial_fit (see partial_fit)
 
     # ---------------------------------------------------------- internals --
     def _make_history(self, hist_cdtype: torch.dtype) -> HistoryState:
@@ -343,9 +344,9 @@ class OnlineTrainer:
         with torch.cuda.stream(sd["stream"]):
             sd["stream"].wait_event(ready)
             sd["ctr"].zero_()
-            zeroed = torch.cuda.Event()
-            zeroed.record()
             sd["info"].zero_()
+            zeroed = torch.cuda.Event()  # both the claim counter and info are zero past this event
+            zeroed.record()
             _lib.call("ocsc_history_invert_claim", _lib.code(h.S.dtype), _lib.code(h.S.dtype), self.K, self.nf,
                       _lib.ptr(h.S), (h.count + B) * h.ridge, 1.0, _lib.ptr(sd["inv"]), _lib.ptr(sd["info"]),
                       _lib.ptr(sd["ctr"]), int(ctas), _lib.stream())
@@ -404,6 +405,12 @@ class OnlineTrainer:
                   _lib.ptr(self.den), s)
 
     # -------------------------------------------------------------- API --
+    _collective = False  # True when partial_fit must agree with other ranks after coding
+
+    def _agree(self, B: int, diverged_at: int) -> int:
+        """First divergence iteration over all participants (-1: none); one process here."""
+        return diverged_at
+
     def _fold(self, uh: torch.Tensor, xh: torch.Tensor, B: int) -> None:
         """History += this mini-batch (overridden by the distributed trainer)."""
         nf = self.nf
@@ -438,6 +445,10 @@ class OnlineTrainer:
         fused = self.use_fused(B) and not want_z
         stream = not fused and not want_z and self.config.stream and stream_supported(self.shape, self.dtype)
         split = self._split_plan(B) if fused else 0
+        # which device path codes this batch (tests assert it): fused cluster kernel (+ the tail
+        # split with the overlapped inverse), streaming FFT kernels (+ the inverse beside them), cuFFT
+        self.last_path = ("fused+split" if split else "fused") if fused else (
+            ("stream+beside" if self._invert_beside_plan(B) else "stream") if stream else "cufft")
         if fused:
             obj = self._obj[:B]
             if split:
@@ -459,25 +470,35 @@ class OnlineTrainer:
                 side_done = self._prefold_side(uh, xh, split, B, main_done)
                 torch.cuda.current_stream().wait_event(tail_done)
             else:
+                self._mark("code start")
                 self._code_fused(xh, buf, uh, obj, 0, B)
+                self._mark("code end")
         elif stream:
             pre = self._invert_beside_plan(B)
             if pre:  # the history inverse of S (+ this batch's ridge) runs on the SMs coding leaves idle
                 inv_zeroed, side_done = self._invert_beside_coding(B, pre)
+            self._mark("code start")
             infer_codes_stream(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
+            self._mark("code end")
         else:
+            self._mark("code start")
             infer_codes(xh, self.Wh, self.den, self.shape, self.coding_config, buf, B, poll=self.config.poll)
+            self._mark("code end")
         pre = self._invert_beside_plan(B) if stream else 0
         if pre:  # finish the inverse on the full grid (the side CTAs keep claiming frequencies)
             self._mark("coded")
             self._finish_inverse(B, inv_zeroed)
             self._mark("inverse finished")
-        if check:
-            status = buf.status[:B].cpu()
-            if bool((status == 2).any()):
+        if check or self._collective:
+            it = -1
+            if B:
+                status = buf.status[:B].cpu()
+                if bool((status == 2).any()):
+                    it = int(buf.iters[:B][status.to(buf.iters.device) == 2].min().cpu())
+            it = self._agree(B, it)  # (sharded trainer: every rank learns every rank's outcome)
+            if it >= 0:
                 if pre:
                     side_done.synchronize()
-                it = int(buf.iters[:B][status.to(buf.iters.device) == 2].min().cpu())
                 raise DivergenceError(f"code solver diverged at iteration {it}")
         if not fused:
             obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
@@ -493,10 +514,16 @@ class OnlineTrainer:
         track = self.config.stop_tol > 0
         if track:
             self._track_changes(buf.u[B - 1])
-        host = torch.cat([obj, buf.iters[:B].double(), self._metrics]).cpu().numpy()
+        parts = [obj, buf.iters[:B].double(), self._metrics]
+        overlapped = bool(split or pre)
+        if overlapped:  # the overlapped inverse's positive-definiteness flags ride on the one sync
+            parts.append(self._side["info"].double())
+        host = torch.cat(parts).cpu().numpy()
         objectives, iterations = host[:B], host[B:2 * B].astype(np.int64)
+        if overlapped and check and bool(np.any(host[2 * B + 4:] != 0)):
+            raise DivergenceError("history Gram matrix lost positive definiteness")
         if track:
-            self._set_changes(host[2 * B:], B)
+            self._set_changes(host[2 * B:2 * B + 4], B)
         self.last_objective = float(objectives[-1])
         return BatchResult(objectives=objectives, iterations=iterations, codes=buf.u[:B])
 

@@ -17,9 +17,10 @@ import torch
 import paper_1706_06972_b200 as ob
 from paper_1706_06972_b200 import _lib
 from oracle import ocsc_oracle as O
+from paper_1706_06972_b200.workloads import synth_images  # noqa: E402
 from paper_1706_06972_b200.transforms import rfft2_dev
 B = 50
-X = O.synth_images(B, (32, 32), (42, 42), 20, seed=1).reshape(B, -1)
+X = synth_images(B, (32, 32), (42, 42), 20, seed=1).reshape(B, -1)
 tr = ob.OnlineTrainer(ob.SignalShape((42, 42), (11, 11)), ob.TrainConfig(n_filters=100, dtype="float32", batch_size=B,
                       stop_tol=0.0))
 tr.partial_fit(X)

@@ -14,10 +14,11 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1706_06972_b200 as ob  # noqa: E402
 from oracle import ocsc_oracle as O  # noqa: E402
+from paper_1706_06972_b200.workloads import CONFIGS, synth_images  # noqa: E402
 
 nb, B = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (2, 50)
-c = O.CONFIGS[1]
-X = O.synth_images(nb * B, c["dims0"], c["grid"], c["K0"], seed=7).reshape(nb * B, -1)
+c = CONFIGS[1]
+X = synth_images(nb * B, c["dims0"], c["grid"], c["K0"], seed=7).reshape(nb * B, -1)
 kw = dict(beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0, code_max_iters=300)
 ora = O.Trainer(c["grid"], (11, 11), K=100, **kw)
 tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)),

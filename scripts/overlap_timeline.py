@@ -7,10 +7,11 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1706_06972_b200 as ob  # noqa: E402
 from oracle import ocsc_oracle as O  # noqa: E402
+from paper_1706_06972_b200.workloads import CONFIGS, synth_images  # noqa: E402
 
-c = O.CONFIGS[1]
+c = CONFIGS[1]
 B = 50
-X = O.synth_images(4 * B, c["dims0"], c["grid"], c["K0"], seed=1).reshape(4 * B, -1)
+X = synth_images(4 * B, c["dims0"], c["grid"], c["K0"], seed=1).reshape(4 * B, -1)
 for overlap in (True, False):
     tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)),
                           ob.TrainConfig(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0,

@@ -4,8 +4,9 @@ import numpy as np, torch
 import paper_1706_06972_b200 as ob
 from paper_1706_06972_b200 import _lib
 from oracle import ocsc_oracle as O
-c = O.CONFIGS[1]; B = 50
-X = O.synth_images(B, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B, -1)
+from paper_1706_06972_b200.workloads import CONFIGS, synth_images  # noqa: E402
+c = CONFIGS[1]; B = 50
+X = synth_images(B, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B, -1)
 tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)), ob.TrainConfig(n_filters=100, rho_dict=1.0, dtype="float32", batch_size=B, stop_tol=0.0))
 tr.partial_fit(X)
 from paper_1706_06972_b200.transforms import rfft2_dev

@@ -4,10 +4,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_1706_06972_b200 as ob
 from oracle import ocsc_oracle as O
+from paper_1706_06972_b200.workloads import CONFIGS, synth_images  # noqa: E402
 
-c = O.CONFIGS[1]
+c = CONFIGS[1]
 B = 50
-X = O.synth_images(B * 4, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B * 4, -1)
+X = synth_images(B * 4, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B * 4, -1)
 shape = ob.SignalShape(c["grid"], (11, 11))
 cfg = ob.TrainConfig(n_filters=100, beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0,
                      dtype="float32", history_dtype=os.environ.get("HD", "float64"), batch_size=B, stop_tol=0.0)

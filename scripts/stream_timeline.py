@@ -7,9 +7,10 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1706_06972_b200 as ob  # noqa: E402
 from oracle import ocsc_oracle as O  # noqa: E402
+from paper_1706_06972_b200.workloads import synth_images  # noqa: E402
 
 B = 10
-X = O.synth_images(4 * B, (100, 100), (100, 100), 20, seed=1).reshape(4 * B, -1)
+X = synth_images(4 * B, (100, 100), (100, 100), 20, seed=1).reshape(4 * B, -1)
 for overlap in (True, False):
     tr = ob.OnlineTrainer(ob.SignalShape((100, 100), (11, 11)),
                           ob.TrainConfig(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0,

@@ -9,11 +9,12 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1706_06972_b200 as ob  # noqa: E402
 from oracle import ocsc_oracle as O  # noqa: E402
+from paper_1706_06972_b200.workloads import CONFIGS, synth_images  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
 B = 50
-c = O.CONFIGS[1]
-X = O.synth_images(N, c["dims0"], c["grid"], c["K0"], seed=11).reshape(N, -1).astype(np.float32)
+c = CONFIGS[1]
+X = synth_images(N, c["dims0"], c["grid"], c["K0"], seed=11).reshape(N, -1).astype(np.float32)
 tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)),
                       ob.TrainConfig(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0))
 Xd = torch.as_tensor(X).cuda()

@@ -13,6 +13,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libocsc_b200.so")
     config.addinivalue_line("markers", "slow: long-running parity case")
+    config.addinivalue_line("markers", "ref_suite: the reference's own tests run through the ocsc shim")
 
 
 @pytest.fixture

@@ -26,7 +26,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 import ocsc  # noqa: E402  (the reference, via PYTHONPATH)
 from ocsc.training import OnlineTrainer  # noqa: E402
 
-from oracle.ocsc_oracle import synth_images  # noqa: E402  (inputs only)
+from paper_1706_06972_b200.workloads import synth_images  # noqa: E402  (inputs only)
 
 assert "reference" in ocsc.__file__, f"expected the reference ocsc, got {ocsc.__file__}"
 
@@ -188,7 +188,7 @@ def case_train_online():
 
 def case_cfg0(steps=1):
     """Config 0 at full size (100x100, K=100, f64, B=1, rho=1): the 1e-9 parity target."""
-    from oracle.ocsc_oracle import CONFIGS
+    from paper_1706_06972_b200.workloads import CONFIGS
     c = CONFIGS[0]
     X = synth_images(steps, c["dims0"], c["grid"], c["K0"], seed=0).reshape(steps, -1)
     shape = ocsc.SignalShape(c["grid"], (11, 11))
@@ -207,6 +207,41 @@ def case_cfg0(steps=1):
          code_idx=np.concatenate(nz_idx), code_val=np.concatenate(nz_val),
          code_counts=np.array([len(i) for i in nz_idx]),
          final_filters=tr.final_filters(), coding_filters=tr.coding_filters())
+
+
+def case_config_minibatch(name, cfg_id, K, B, nbatches, seed, beta=None, dims0=None, grid=None, K0=None):
+    """A BASELINE config's own shapes, composed mini-batch semantics built from
+    reference calls only, in the reference's float64.  X is regenerated from the seed by
+    paper_1706_06972_b200.workloads.synth_images (its sha256 is stored to pin the generator)."""
+    import hashlib
+
+    from paper_1706_06972_b200.workloads import CONFIGS
+    c = CONFIGS[cfg_id]
+    dims0, grid, K0 = dims0 or c["dims0"], grid or c["grid"], K0 or c["K0"]
+    beta = c["beta"] if beta is None else beta
+    X = synth_images(B * nbatches, dims0, grid, K0, seed=seed).reshape(B * nbatches, -1)
+    shape = ocsc.SignalShape(grid, (11, 11))
+    cfg = ocsc.TrainConfig(n_filters=K, beta=beta, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0,
+                           code_max_iters=300, code_rel_tol=1e-3)
+    tr = OnlineTrainer(shape, cfg)
+    coding = cfg.coding()
+    objs, iters, filt = [], [], []
+    for m in range(nbatches):
+        t0 = time.time()
+        batch = X[m * B:(m + 1) * B]
+        states = [ocsc.infer_code(x, tr.working_freq, shape, coding) for x in batch]
+        for x, st in zip(batch, states):
+            objs.append(ocsc.coding_objective(x, tr.working_freq, st.code, shape, cfg.beta))
+            iters.append(st.iterations)
+        for x, st in zip(batch, states):
+            ocsc.update_history(tr.history, ocsc.forward_dft_cols(st.code, shape), ocsc.forward_dft(x, shape))
+        tr.dict_state = ocsc.update_dictionary(tr.dict_state, tr.history, cfg.inner_iters)
+        tr.working_freq = ocsc.forward_dft_cols(tr.dict_state.v, shape)
+        filt.append(tr.final_filters())
+        print(f"{name} mini-batch {m}: {time.time() - t0:.1f}s", flush=True)
+    save(name, cfg_id=cfg_id, dims0=dims0, grid=grid, K0=K0, K=K, B=B, seed=seed, beta=beta,
+         x_sha256=hashlib.sha256(X.tobytes()).hexdigest(), objectives=np.array(objs), iterations=np.array(iters),
+         batch_filters=np.array(filt), final_filters=tr.final_filters(), coding_filters=tr.coding_filters())
 
 
 if __name__ == "__main__":
@@ -273,3 +308,10 @@ if __name__ == "__main__":
         print("wrote dict_2x3_k3.dic, sample_4x5.smp")
     if "cfg0" in which:
         case_cfg0()
+    # BASELINE configs' own shapes through the composed mini-batch oracle (reference float64)
+    if "cfg1_mb" in which:   # headline: 42x42, K=100, B=50, two mini-batches
+        case_config_minibatch("cfg1_mb", 1, K=100, B=50, nbatches=2, seed=101)
+    if "cfg2_mb" in which:   # 100x100, K=100, B=10, two mini-batches
+        case_config_minibatch("cfg2_mb", 2, K=100, B=10, nbatches=2, seed=102)
+    if "cfg3_mb" in which:   # 266x266 grid, K=32 (the reference's (P, K, K) inverse of K=256 is 74 GB), B=4
+        case_config_minibatch("cfg3_mb", 3, K=32, B=4, nbatches=2, seed=103)

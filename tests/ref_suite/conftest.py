@@ -1,0 +1,81 @@
+"""Run the reference's own hot-path tests against the B200 build through the `ocsc` shim.
+
+Collected only when the staged copies exist (tests/ref_suite/fetch.py, run by build())
+and a CUDA device is present -- every item is marked `gpu` (and `ref_suite`), so the CPU
+suite (`-m "not gpu"`) never collects them.  Tests of components the build leaves out of
+scope are marked xfail with the reason; the documented behavioural
+differences are listed in DESIGN.md section 5.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+SHIM = os.path.join(HERE, "shim")
+STAGED = os.path.join(HERE, "_ref")
+
+
+def _cuda() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
+
+
+collect_ignore = ["shim", "fetch.py"]
+if not os.path.isdir(STAGED) or not _cuda():
+    collect_ignore.append("_ref")
+else:
+    for p in (SHIM, ROOT):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    # acceptance 5 runs children with `python -c "from ocsc import ..."`
+    os.environ["PYTHONPATH"] = os.pathsep.join([SHIM, ROOT] + [p for p in os.environ.get("PYTHONPATH", "").split(os.pathsep) if p])
+
+# out-of-scope components: the FISTA training mode
+OUT_OF_SCOPE = {
+    "test_training.py::TestFistaMode::test_smoke_produces_feasible_filters":
+        "train_fista_dict (FISTA baseline mode) is outside the B200 hot path",
+    "test_training.py::TestEmptyStream::test_all_modes_return_init_and_empty_records":
+        "iterates over train_fista_dict, outside the B200 hot path",
+    "test_training.py::TestDispatcher::test_modes_route_to_matching_runner":
+        "routes 'fista-dict' to train_fista_dict, outside the B200 hot path",
+}
+
+
+# criteria the REFERENCE itself fails (pkg/test_output.txt: acceptance 8 FAIL with "psnr gain 1.01 dB
+# (target >= 3), pass-3 obj 5054.9270 vs pass-1 5072.0876" -- this build prints the same digits)
+REFERENCE_FAILS = {
+    "test_acceptance.py::test_online_recovery_on_consistent_synthetic_data":
+        "fails identically in the reference (pkg/test_output.txt: 1.01 dB gain < 3 dB on dense-code data)",
+}
+
+
+@pytest.hookimpl(tryfirst=True)
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        if STAGED not in str(item.fspath):
+            continue
+        item.add_marker(pytest.mark.gpu)
+        item.add_marker(pytest.mark.ref_suite)
+        key = f"{os.path.basename(str(item.fspath))}::{'::'.join(item.nodeid.split('::')[1:])}"
+        if key in OUT_OF_SCOPE:
+            item.add_marker(pytest.mark.xfail(reason=OUT_OF_SCOPE[key], raises=NotImplementedError, strict=True))
+        if key in REFERENCE_FAILS:
+            item.add_marker(pytest.mark.xfail(reason=REFERENCE_FAILS[key], raises=AssertionError, strict=False))
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    for module in list(sys.modules.values()):
+        lines = getattr(module, "__dict__", {}).get("_ACCEPTANCE_LINES")
+        if isinstance(lines, list) and lines:
+            terminalreporter.section("reference acceptance criteria (B200 build)")
+            for line in lines:
+                terminalreporter.write_line(line)
+            break

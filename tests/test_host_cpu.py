@@ -95,13 +95,17 @@ def test_train_dispatch_errors():
         train("fista-dict", np.zeros((1, 8)), SignalShape((8,), (2,)), TrainConfig())
 
 
-def test_shard_rows_partitions_in_rank_order():
-    from paper_1706_06972_b200.parallel import shard_rows
+def test_sample_shards_are_ragged_contiguous_rank_order():
+    from paper_1706_06972_b200.sharded import sample_shards
 
-    rows = [list(range(100))[shard_rows(100, r, 4)] for r in range(4)]
-    assert sum(rows, []) == list(range(100))
-    with pytest.raises(ValueError):
-        shard_rows(10, 0, 3)
+    for n, G in [(100, 4), (50, 8), (10, 8), (5, 2), (3, 4), (1, 2)]:
+        sh = sample_shards(n, G)
+        rows = sum((list(range(n))[s] for s in sh), [])
+        assert rows == list(range(n)) and len(sh) == G
+        sizes = [s.stop - s.start for s in sh]
+        assert max(sizes) - min(sizes) <= 1 and sizes == sorted(sizes, reverse=True)
+    assert [s.stop - s.start for s in sample_shards(50, 8)] == [7, 7, 6, 6, 6, 6, 6, 6]
+    assert [s.stop - s.start for s in sample_shards(10, 8)] == [2, 2, 1, 1, 1, 1, 1, 1]
 
 
 def _free_port():
@@ -112,41 +116,79 @@ def _free_port():
     return port
 
 
-def _gloo_worker(rank, world, port, out):
+def _collectives_worker(rank, world, port, out):
+    """Comm primitives of the sharded trainer over gloo, with a ragged 3 + 2 (+ 0) sample split."""
     import torch.distributed as dist
 
-    from paper_1706_06972_b200.parallel import gather_rank_ordered, shard_rows
+    from paper_1706_06972_b200.sharded import DistComm, exchange_codes, row_slices, sample_shards
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
-        B, K, nf = 3, 4, 5
-        glob = torch.arange(world * B * K * nf, dtype=torch.float64).reshape(world * B, K, nf)
-        mine = glob[shard_rows(world * B, rank, world)].clone()
-        # complex spectra travel as complex tensors in the trainer
-        got = gather_rank_ordered(torch.complex(mine, -mine))
-        ok = torch.equal(got, torch.complex(glob, -glob))
-        # the change metrics come from the LAST rank (last sample of the global batch)
+        comm = DistComm()
+        B, K, H, Wh = 5, 3, 7, 4
+        g = torch.Generator().manual_seed(0)
+        uh_all = torch.complex(torch.randn(B, K, H, Wh, generator=g, dtype=torch.float64),
+                               torch.randn(B, K, H, Wh, generator=g, dtype=torch.float64))
+        xh_all = torch.complex(torch.randn(B, H, Wh, generator=g, dtype=torch.float64),
+                               torch.randn(B, H, Wh, generator=g, dtype=torch.float64))
+        mine = sample_shards(B, world)[rank]
+        b = mine.stop - mine.start
+        # agreement: shard sizes + divergence flags of every rank
+        table = comm.gather_ints([b, 17 if rank == world - 1 else -1])
+        counts = [int(v) for v in table[:, 0]]
+        rows = row_slices(H, world)
+        z, x = exchange_codes(uh_all[mine], xh_all[mine], rows, comm, counts)
+        u0, u1 = rows[rank]
+        ok_a2a = torch.equal(z, uh_all[:, :, u0:u1].reshape(B, K, -1)) and \
+            torch.equal(x, xh_all[:, u0:u1].reshape(B, -1))
+        # reduce-scatter of rank-chunked increments: chunk q summed over ranks lands on rank q
+        chunks = torch.stack([torch.full((2, 3), float(10 * q + rank), dtype=torch.float64) for q in range(world)])
+        got = torch.empty(2, 3, dtype=torch.float64)
+        comm.reduce_scatter(got, chunks)
+        ok_rs = torch.equal(got, torch.full((2, 3), float(world * 10 * rank + sum(range(world)))))
+        # all-gather in rank order
+        ag = torch.empty(world, 2, dtype=torch.float64)
+        comm.all_gather(ag, torch.full((2,), float(rank), dtype=torch.float64))
+        ok_ag = torch.equal(ag[:, 0], torch.arange(world, dtype=torch.float64))
+        # the change metrics come from the last rank with a non-empty shard
+        src = max(r for r, c in enumerate(counts) if c > 0)
         m = torch.full((4,), float(rank))
-        dist.broadcast(m, src=world - 1)
-        out.put((rank, bool(ok), float(m[0])))
+        comm.broadcast_(m, src)
+        out.put((rank, counts, table[:, 1].tolist(), bool(ok_a2a), bool(ok_rs), bool(ok_ag), float(m[0])))
+    except Exception as e:  # surface worker failures instead of a queue timeout
+        import traceback
+        out.put((rank, "error", traceback.format_exc(), e.__class__.__name__, None, None, None))
+        raise
     finally:
         dist.destroy_process_group()
 
 
-def test_gloo_world2_exchange_is_rank_ordered():
+@pytest.mark.parametrize("world", [2, 3, 6])
+def test_gloo_ragged_collectives(world):
+    """Exchange A with ragged shards (B = 5 over 2 ranks = 3 + 2; over 6 ranks one is empty),
+    the reduce-scatter of exchange A's north_star variant, the agreement table, all-gather, and
+    the change-metric broadcast -- over a real multi-process gloo group."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_collectives_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=120) for _ in procs)
+    res = sorted(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert [r[1] for r in res] == [True, True]
-    assert [r[2] for r in res] == [1.0, 1.0]
+    from paper_1706_06972_b200.sharded import sample_shards
+
+    sizes = [s.stop - s.start for s in sample_shards(5, world)]
+    src = max(r for r, c in enumerate(sizes) if c > 0)
+    for rank, counts, flags, ok_a2a, ok_rs, ok_ag, m0 in res:
+        assert counts != "error", flags
+        assert counts == sizes
+        assert flags == [-1] * (world - 1) + [17]
+        assert ok_a2a and ok_rs and ok_ag
+        assert m0 == float(src)
 
 
 def test_taper_sigmas_match_numpy_default_rng():
@@ -171,51 +213,6 @@ def test_row_slices_partition():
         assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
         sizes = [b - a for a, b in rows]
         assert max(sizes) - min(sizes) <= 1
-
-
-def _exchange_worker(rank, world, port, out):
-    import torch.distributed as dist
-
-    from paper_1706_06972_b200.sharded import DistComm, exchange_codes, row_slices
-
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    try:
-        B, K, H, Wh = 2, 3, 5, 4
-        g = torch.Generator().manual_seed(0)
-        uh_all = torch.complex(torch.randn(world * B, K, H, Wh, generator=g, dtype=torch.float64),
-                               torch.randn(world * B, K, H, Wh, generator=g, dtype=torch.float64))
-        xh_all = torch.complex(torch.randn(world * B, H, Wh, generator=g, dtype=torch.float64),
-                               torch.randn(world * B, H, Wh, generator=g, dtype=torch.float64))
-        rows = row_slices(H, world)
-        comm = DistComm()
-        z, x = exchange_codes(uh_all[rank * B:(rank + 1) * B], xh_all[rank * B:(rank + 1) * B], rows, comm)
-        u0, u1 = rows[rank]
-        ok = torch.equal(z, uh_all[:, :, u0:u1].reshape(world * B, K, -1)) and \
-            torch.equal(x, xh_all[:, u0:u1].reshape(world * B, -1))
-        # exchange B: the partial supports sum to the same value on every rank
-        part = torch.full((4,), float(rank + 1), dtype=torch.float64)
-        comm.all_reduce_(part)
-        out.put((rank, bool(ok), float(part[0])))
-    finally:
-        dist.destroy_process_group()
-
-
-def test_gloo_world2_frequency_exchange():
-    """Exchange A of the frequency-sharded trainer over gloo: each rank receives every sample's
-    spectra restricted to its rows, in rank order (uneven row split 3 + 2)."""
-    import torch.multiprocessing as mp
-
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = sorted(q.get(timeout=120) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-    assert [r[1] for r in res] == [True, True]
-    assert [r[2] for r in res] == [3.0, 3.0]
 
 
 def test_overlap_entry_points_validate_on_the_host():

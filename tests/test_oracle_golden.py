@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import ocsc_oracle as O
+from paper_1706_06972_b200.workloads import synth_images
 from tests._layout import cols_to_planes, hw, planes_to_cols, rel
 
 
@@ -141,13 +142,13 @@ def test_train_online_passes(golden):
 
 
 def test_synth_images_standardised():
-    X = O.synth_images(3, (32, 32), (42, 42), 20, seed=0)
+    X = synth_images(3, (32, 32), (42, 42), 20, seed=0)
     assert X.shape == (3, 42, 42)
     core = X[:, :32, :32].reshape(3, -1)
     assert np.allclose(core.mean(axis=1), 0, atol=1e-12)
     assert np.allclose(core.std(axis=1), 1, atol=1e-12)
     assert not X[:, 32:, :].any() and not X[:, :, 32:].any()
-    assert np.array_equal(X, O.synth_images(3, (32, 32), (42, 42), 20, seed=0))
+    assert np.array_equal(X, synth_images(3, (32, 32), (42, 42), 20, seed=0))
 
 
 def test_oracle_config0_full_size(golden):
@@ -179,3 +180,21 @@ def test_oracle_preprocessing_matches_reference(golden):
     assert close(O.taper(g["gray"], 6, 1.0), g["taper_even"])
     for i, im in enumerate(g["stack"]):
         assert close(O.preprocess(im, seed=5 + i), g["pre_stack"][i])
+
+
+@pytest.mark.parametrize("name", ["cfg1_mb", "cfg2_mb", "cfg3_mb"])
+def test_config_golden_inputs_regenerate(golden, name):
+    """The BASELINE-config golden files store no images: the seeded workload generator must
+    reproduce the exact inputs the reference was run on (sha256 pinned at generation)."""
+    import hashlib
+    import os
+
+    from tests.conftest import GOLDEN
+
+    if not os.path.exists(os.path.join(GOLDEN, f"{name}.npz")):
+        pytest.skip(f"{name} not generated")
+    g = golden(name)
+    B, n = int(g["B"]), len(g["objectives"])
+    X = synth_images(n, tuple(g["dims0"]), tuple(g["grid"]), int(g["K0"]), seed=int(g["seed"]))
+    assert hashlib.sha256(X.tobytes()).hexdigest() == str(g["x_sha256"])
+    assert n % B == 0 and g["batch_filters"].shape[0] == n // B

@@ -17,6 +17,7 @@ if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes
 
 import paper_1706_06972_b200 as ob  # noqa: E402
 from oracle import ocsc_oracle as O  # noqa: E402
+from paper_1706_06972_b200.workloads import CONFIGS, synth_images  # noqa: E402
 from tests._layout import cols_to_planes, hw, planes_to_cols, rel  # noqa: E402
 
 TOL64 = 1e-9
@@ -262,7 +263,7 @@ def test_empty_stream_returns_init():
 
 def test_online_bitwise_repeatable():
     shape = ob.SignalShape((12, 12), (3, 3))
-    X = O.synth_images(4, (12, 12), (12, 12), 2, filter_dims=(3, 3), seed=4, density=0.05).reshape(4, -1)
+    X = synth_images(4, (12, 12), (12, 12), 2, filter_dims=(3, 3), seed=4, density=0.05).reshape(4, -1)
     cfg = ob.TrainConfig(n_filters=3, beta=0.5, seed=3, max_passes=2, stop_tol=1e-12, inner_iters=3,
                          code_max_iters=40, batch_size=2)
     a, b = ob.train_online(X, shape, cfg), ob.train_online(X, shape, cfg)
@@ -291,9 +292,9 @@ def test_config0_full_size_float64(golden):
 
 def test_float32_prefix_config1_shape():
     """Config-1 geometry (32x32 padded to 42x42, K=100) in float32 vs the float64 oracle on a prefix."""
-    c = O.CONFIGS[1]
+    c = CONFIGS[1]
     B, nb = 4, 2
-    X = O.synth_images(B * nb, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B * nb, -1)
+    X = synth_images(B * nb, c["dims0"], c["grid"], c["K0"], seed=1).reshape(B * nb, -1)
     kw = dict(beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0, code_max_iters=300)
     ora = O.Trainer(c["grid"], (11, 11), K=100, **kw)
     shape = ob.SignalShape(c["grid"], (11, 11))
@@ -309,7 +310,7 @@ def test_float32_prefix_config1_shape():
 
 def test_evaluate_dictionary_psnr():
     shape = ob.SignalShape((16, 16), (3, 3))
-    X = O.synth_images(3, (16, 16), (16, 16), 2, filter_dims=(3, 3), seed=2, density=0.05).reshape(3, -1)
+    X = synth_images(3, (16, 16), (16, 16), 2, filter_dims=(3, 3), seed=2, density=0.05).reshape(3, -1)
     f = ob.init_dictionary(shape, 4, 1)
     res = ob.evaluate_dictionary(f, X, shape, ob.CodingConfig(beta=0.2))
     dh = O.fwd(O.pad(f, 16, 16, 3, 3))
@@ -342,7 +343,7 @@ def test_fused_any_cluster_size_equals_cufft_path(cs, monkeypatch):
     from paper_1706_06972_b200 import _lib
     assert _lib.load().ocsc_code_fused_cluster(8, 30, 30, K, B) == cs
     shape = ob.SignalShape(dims, (3, 3))
-    X = O.synth_images(B, dims, dims, 3, filter_dims=(3, 3), seed=11, density=0.05).reshape(B, -1)
+    X = synth_images(B, dims, dims, 3, filter_dims=(3, 3), seed=11, density=0.05).reshape(B, -1)
     kw = dict(n_filters=K, beta=0.3, rho_code=1.0, rho_dict=1.0, inner_iters=2, seed=4, code_max_iters=60,
               batch_size=B, stop_tol=0.0)
     a = ob.OnlineTrainer(shape, ob.TrainConfig(fused=True, **kw))
@@ -387,7 +388,7 @@ def test_fused_single_sample_steps_match_reference(golden):
 @pytest.mark.parametrize("dims,K,B", [((14, 14), 7, 5), ((18, 18), 12, 3), ((10, 10), 4, 4), ((30, 30), 33, 2)])
 def test_fused_equals_cufft_path(dims, K, B):
     shape = ob.SignalShape(dims, (3, 3))
-    X = O.synth_images(2 * B, dims, dims, 3, filter_dims=(3, 3), seed=9, density=0.05).reshape(2 * B, -1)
+    X = synth_images(2 * B, dims, dims, 3, filter_dims=(3, 3), seed=9, density=0.05).reshape(2 * B, -1)
     kw = dict(n_filters=K, beta=0.3, rho_code=1.0, rho_dict=1.0, inner_iters=3, seed=2, code_max_iters=80,
               batch_size=B, stop_tol=0.0)
     a = ob.OnlineTrainer(shape, ob.TrainConfig(fused=True, **kw))
@@ -402,9 +403,9 @@ def test_fused_equals_cufft_path(dims, K, B):
 
 
 def test_fused_float32_matches_oracle_42x42():
-    c = O.CONFIGS[1]
+    c = CONFIGS[1]
     B = 6
-    X = O.synth_images(B, c["dims0"], c["grid"], c["K0"], seed=3).reshape(B, -1)
+    X = synth_images(B, c["dims0"], c["grid"], c["K0"], seed=3).reshape(B, -1)
     kw = dict(beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0, code_max_iters=300)
     ora = O.Trainer(c["grid"], (11, 11), K=100, **kw)
     tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)),
@@ -440,8 +441,8 @@ def test_woodbury_refresh_matches_direct_inverse():
 def test_overlapped_history_inverse_matches_serial_path(B):
     """Config-1 shapes: the tail-overlapped inverse (side-stream Gauss-Jordan of the main part +
     Woodbury refresh with the tail) trains like the serial accumulate-then-invert path."""
-    c = O.CONFIGS[1]
-    X = O.synth_images(2 * B, c["dims0"], c["grid"], c["K0"], seed=21).reshape(2 * B, -1)
+    c = CONFIGS[1]
+    X = synth_images(2 * B, c["dims0"], c["grid"], c["K0"], seed=21).reshape(2 * B, -1)
     kw = dict(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0, inner_iters=10)
     shape = ob.SignalShape(c["grid"], (11, 11))
     a = ob.OnlineTrainer(shape, ob.TrainConfig(overlap=True, **kw))
@@ -478,9 +479,9 @@ def test_new_entry_points_fail_loudly():
 def test_overlapped_inverse_does_not_drift():
     """Twelve config-1 mini-batches (600 samples): the Woodbury-refreshed inverse path stays on
     the serial path's objective trace and filters (no accumulation of refresh error)."""
-    c = O.CONFIGS[1]
+    c = CONFIGS[1]
     B, steps = 50, 12
-    X = O.synth_images(B * steps, c["dims0"], c["grid"], c["K0"], seed=31).reshape(B * steps, -1)
+    X = synth_images(B * steps, c["dims0"], c["grid"], c["K0"], seed=31).reshape(B * steps, -1)
     kw = dict(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0, inner_iters=10,
               code_max_iters=100)
     shape = ob.SignalShape(c["grid"], (11, 11))
@@ -498,9 +499,9 @@ def test_inverse_beside_stream_coding_matches_serial_path():
     """Config-2 shapes (plane-resident stream kernel): the history inverse claimed by persistent
     CTAs on the SMs coding leaves idle + a full-grid finish + a Woodbury refresh with the batch
     trains like the serial accumulate-then-invert path."""
-    c = O.CONFIGS[0]
+    c = CONFIGS[0]
     B = 10
-    X = O.synth_images(2 * B, (100, 100), (100, 100), 20, seed=23).reshape(2 * B, -1)
+    X = synth_images(2 * B, (100, 100), (100, 100), 20, seed=23).reshape(2 * B, -1)
     kw = dict(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0, inner_iters=10,
               code_max_iters=60)
     shape = ob.SignalShape((100, 100), (11, 11))
@@ -552,7 +553,8 @@ def _dense_rowsolve(z, x, v, th, t_rho_p):
     return out
 
 
-@pytest.mark.parametrize("K,solver", [(64, "chol"), (64, "gj"), (256, "chol"), (96, "chol"), (32, "chol"), (128, "chol")])
+@pytest.mark.parametrize("K,solver", [(64, "chol"), (64, "gj"), (256, "chol"), (96, "chol"), (32, "chol"), (128, "chol"),
+                                      (40, "chol"), (120, "chol"), (200, "chol"), (20, "chol")])
 def test_history_solvers_match_dense(K, solver):
     nfreq, B = 5, 12
     h, z, x = _random_history(K, nfreq, B, seed=K, solver=solver)
@@ -568,7 +570,7 @@ def test_history_solvers_match_dense(K, solver):
 
 def test_trainer_cholesky_path_equals_inverse_path():
     shape = ob.SignalShape((14, 14), (3, 3))
-    X = O.synth_images(8, (14, 14), (14, 14), 3, filter_dims=(3, 3), seed=5, density=0.05).reshape(8, -1)
+    X = synth_images(8, (14, 14), (14, 14), 3, filter_dims=(3, 3), seed=5, density=0.05).reshape(8, -1)
     kw = dict(n_filters=64, beta=0.3, rho_code=1.0, rho_dict=1.0, inner_iters=3, seed=2, code_max_iters=40,
               batch_size=4, stop_tol=0.0)
     a = ob.OnlineTrainer(shape, ob.TrainConfig(history_solver="gj", **kw))
@@ -583,7 +585,7 @@ def test_trainer_cholesky_path_equals_inverse_path():
 
 def test_checkpoint_resume_is_bit_identical(tmp_path):
     shape = ob.SignalShape((14, 14), (3, 3))
-    X = O.synth_images(16, (14, 14), (14, 14), 3, filter_dims=(3, 3), seed=8, density=0.05).reshape(16, -1)
+    X = synth_images(16, (14, 14), (14, 14), 3, filter_dims=(3, 3), seed=8, density=0.05).reshape(16, -1)
     cfg = ob.TrainConfig(n_filters=6, beta=0.3, rho_dict=1.0, inner_iters=3, code_max_iters=60, batch_size=4,
                          stop_tol=1e-9, dtype="float32")
     a = ob.OnlineTrainer(shape, cfg)
@@ -685,7 +687,7 @@ def test_stream_code_path_matches_cufft_path(dtype, H, K, B):
     rdt = torch.float32 if dtype == "float32" else torch.float64
     assert stream_supported(shape, rdt)
     tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=K, dtype=dtype, batch_size=B, beta=0.3))
-    x = torch.from_numpy(O.synth_images(B, (H - 10, H - 10), (H, H), 3, seed=5)).to("cuda", rdt)
+    x = torch.from_numpy(synth_images(B, (H - 10, H - 10), (H, H), 3, seed=5)).to("cuda", rdt)
     xh = rfft2_dev(x, shape)
     cc = ob.CodingConfig(beta=0.3, max_iters=60, rel_tol=1e-3)
     ref, got = CodeBuffers(shape, K, B, rdt), CodeBuffers(shape, K, B, rdt)
@@ -745,7 +747,7 @@ def test_sharded_trainer_world1_equals_online_trainer():
 
     shape = ob.SignalShape((18, 12), (3, 3))
     cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=3, beta=0.3, code_max_iters=80, inner_iters=4)
-    X = O.synth_images(6, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(6, -1)
+    X = synth_images(6, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(6, -1)
     a, b = ob.OnlineTrainer(shape, cfg), ShardedTrainer(shape, cfg)
     for i in range(2):
         ra, rb = a.partial_fit(X[3 * i:3 * i + 3]), b.partial_fit(X[3 * i:3 * i + 3])
@@ -774,65 +776,103 @@ def test_sharded_history_rows_equal_full_history_rows():
         assert torch.equal(part.S, full.S[u0 * Wh:u1 * Wh]) and torch.equal(part.c, full.c[u0 * Wh:u1 * Wh])
 
 
-def _sharded_worker(rank, world, port, exchange, out):
+def _sharded_worker(rank, world, port, exchange, B, nan_rank, out):
     import torch.distributed as dist
 
-    from paper_1706_06972_b200.sharded import DistComm, ShardedTrainer
+    from paper_1706_06972_b200.sharded import DistComm, ShardedTrainer, sample_shards
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         shape = ob.SignalShape((18, 12), (3, 3))
-        cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=2, beta=0.3, code_max_iters=80, inner_iters=4)
-        X = O.synth_images(8, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(8, -1)
+        cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=B, beta=0.3, code_max_iters=80, inner_iters=4)
+        X = synth_images(2 * B, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(2 * B, -1)
         tr = ShardedTrainer(shape, cfg, DistComm(), exchange=exchange)
+        mine = sample_shards(B, world)[rank]
+        if nan_rank is not None:  # divergence on one rank must raise on every rank, not hang
+            g = X[:B].copy()
+            if rank == nan_rank:
+                g[mine.start, 5] = np.nan
+            try:
+                tr.partial_fit(g[mine])
+            except ob.DivergenceError as e:
+                out.put((rank, "raised", str(e), tr.history.count))
+            else:
+                out.put((rank, "no error", "", tr.history.count))
+            return
         objs = []
-        for i in range(2):  # global mini-batches of 4 = 2 ranks x 2
-            g = X[4 * i:4 * i + 4]
-            objs.append(tr.partial_fit(g[2 * rank:2 * rank + 2]).objectives)
-        out.put((rank, tr.alpha.cpu().numpy(), np.concatenate(objs), tr.final_filters(), tr.dict_change))
+        for i in range(2):  # global mini-batches of B samples, ragged shards
+            g = X[B * i:B * (i + 1)]
+            objs.append(tr.partial_fit(g[mine]).objectives)
+        ds = tr.dict_state
+        out.put((rank, tr.alpha.cpu().numpy(), np.concatenate(objs), tr.final_filters(), tr.dict_change,
+                 ds.freq, tr.history.count))
+    except Exception:  # surface worker failures instead of a queue timeout
+        import traceback
+        out.put((rank, "error", traceback.format_exc(), None))
+        raise
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["all_to_all", "reduce_scatter"])
-def test_sharded_trainer_two_ranks_matches_single_gpu(exchange):
-    """Two frequency-sharded ranks (gloo, host-staged collectives, both on cuda:0 -- no device
-    collective waits on another rank's kernels) reproduce the single-GPU trainer fed the global
-    mini-batches: history rows, per-round K x M all-reduce, exchange C."""
+def _spawn_sharded(world, exchange, B, nan_rank=None):
     import socket
 
     import torch.multiprocessing as mp
 
-    shape = ob.SignalShape((18, 12), (3, 3))
-    cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=4, beta=0.3, code_max_iters=80, inner_iters=4)
-    X = O.synth_images(8, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(8, -1)
-    ref = ob.OnlineTrainer(shape, cfg)
-    ref_obj = np.concatenate([ref.partial_fit(X[4 * i:4 * i + 4]).objectives for i in range(2)])
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, exchange, q)) for r in range(2)]
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, exchange, B, nan_rank, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=300) for _ in procs), key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
-    for rank, alpha, objs, filt, dchg in res:
+    for r in res:
+        assert not (isinstance(r[1], str) and r[1] == "error"), r[2]
+    return res
+
+
+@pytest.mark.parametrize("exchange,world,B", [("all_to_all", 2, 5), ("reduce_scatter", 2, 5), ("all_to_all", 3, 2)])
+def test_sharded_trainer_ragged_ranks_match_single_gpu(exchange, world, B):
+    """Frequency-sharded ranks (gloo, host-staged collectives, all on cuda:0 -- no device
+    collective waits on another rank's kernels) with ragged sample shards (B=5 over 2 ranks =
+    3 + 2; B=2 over 3 ranks leaves one rank empty) reproduce the single-GPU trainer fed the same
+    global mini-batches: history rows, per-round K x M all-reduce, exchange C, dict_state."""
+    shape = ob.SignalShape((18, 12), (3, 3))
+    cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=B, beta=0.3, code_max_iters=80, inner_iters=4)
+    X = synth_images(2 * B, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(2 * B, -1)
+    ref = ob.OnlineTrainer(shape, cfg)
+    ref_obj = [ref.partial_fit(X[B * i:B * (i + 1)]).objectives for i in range(2)]
+    from paper_1706_06972_b200.sharded import sample_shards
+
+    for rank, alpha, objs, filt, dchg, dfreq, count in _spawn_sharded(world, exchange, B):
+        mine = sample_shards(B, world)[rank]
+        assert count == 2 * B
         assert rel(alpha, ref.alpha.cpu().numpy()) < 1e-11
-        mine = np.concatenate([ref_obj[4 * i + 2 * rank:4 * i + 2 * rank + 2] for i in range(2)])
-        assert rel(objs, mine) < 1e-11
+        if mine.stop > mine.start:
+            assert rel(objs, np.concatenate([o[mine] for o in ref_obj])) < 1e-11
         assert rel(filt, ref.final_filters()) < 1e-11
+        assert rel(dfreq, ref.dict_state.freq) < 1e-11
         assert abs(dchg - ref.dict_change) <= 1e-9 * abs(ref.dict_change)
+
+
+def test_sharded_divergence_raises_on_every_rank():
+    """A NaN sample on rank 1 makes every rank raise DivergenceError before the history is
+    touched (the agreement all-gather), instead of rank 1 raising while rank 0 blocks."""
+    res = _spawn_sharded(2, "all_to_all", 4, nan_rank=1)
+    assert [r[1] for r in res] == ["raised", "raised"]
+    assert all("iteration" in r[2] for r in res) and all(r[3] == 0 for r in res)
 
 
 def test_train_online_ragged_and_empty_batches():
     """N not divisible by the mini-batch (ragged last batch, training.py:193-198 order) and an
     empty corpus (no records, the initial filters), against the oracle in float64."""
     shape = ob.SignalShape((14, 12), (3, 3))
-    X = O.synth_images(7, (12, 10), (14, 12), 2, filter_dims=(3, 3), seed=4).reshape(7, -1)
+    X = synth_images(7, (12, 10), (14, 12), 2, filter_dims=(3, 3), seed=4).reshape(7, -1)
     kw = dict(K=3, beta=0.4, rho_code=1.0, rho_dict=2.0, inner_iters=3, seed=5, code_max_iters=60,
               code_rel_tol=1e-3, stop_tol=0.0)
     ref = O.train_online(X, (14, 12), (3, 3), batch_size=3, max_passes=2, **kw)
@@ -888,3 +928,67 @@ def test_circular_convolve_matches_direct_sum():
             for b in range(M1):
                 want += dd[a, b] * np.roll(np.roll(zz, a, axis=0), b, axis=1)
         assert np.abs(got - want).max() < 1e-12 * max(np.abs(want).max(), 1.0)
+
+
+@pytest.mark.parametrize("K,dtype", [(120, torch.complex128), (40, torch.complex128), (200, torch.complex64)])
+def test_cholesky_inv_gram_any_K(K, dtype):
+    """inv_gram on the Cholesky path (K not a multiple of 32 -> padded factor) equals the direct
+    inverse of the averaged Gram + rho P I (dictionary.py:94-111 semantics)."""
+    nfreq, B = 3, 7
+    h, z, _ = _random_history(K, nfreq, B, seed=K, dtype=dtype, solver="chol")
+    gram = np.einsum("bpi,bpj->pij", z, z.conj()) / B
+    want = np.linalg.inv(gram + 1.0 * nfreq * np.eye(K))
+    tol = 1e-11 if dtype == torch.complex128 else 2e-5
+    assert rel(h.inv_gram, want) < tol
+
+
+def test_default_history_any_K_through_trainer():
+    """TrainConfig(n_filters=120) under the default float64 history: K > 118 routes to the
+    (padded) Cholesky solver; the trainer matches the oracle at 1e-9 (the reference accepts any
+    K, dictionary.py:57-66)."""
+    shape = ob.SignalShape((10, 10), (3, 3))
+    X = synth_images(4, (10, 10), (10, 10), 3, filter_dims=(3, 3), seed=12, density=0.05).reshape(4, -1)
+    kw = dict(beta=0.3, rho_code=1.0, rho_dict=1.0, inner_iters=3, seed=1, code_max_iters=60)
+    tr = ob.OnlineTrainer(shape, ob.TrainConfig(n_filters=120, batch_size=2, stop_tol=0.0, **kw))
+    assert tr.history.solver == "chol"
+    ora = O.Trainer((10, 10), (3, 3), K=120, **kw)
+    for m in range(2):
+        got = tr.partial_fit(X[2 * m:2 * m + 2]).objectives
+        want = [o for _, o in ora.step_batch(X[2 * m:2 * m + 2])]
+        assert np.allclose(got, want, rtol=TOL64, atol=0)
+    assert rel(tr.final_filters(), ora.final_filters()) < TOL64
+    assert rel(tr.history.inv_gram, ora.hist.inv.reshape(-1, 120, 120)) < TOL64
+
+
+def test_evaluate_dictionary_rejects_bad_filters():
+    shape = ob.SignalShape((8, 8), (3, 3))
+    X = np.random.default_rng(0).normal(size=(2, 64))
+    with pytest.raises(ob.ShapeMismatchError):
+        ob.evaluate_dictionary(np.zeros((8, 2)), X, shape)
+    with pytest.raises(ob.ShapeMismatchError):
+        ob.evaluate_dictionary(np.zeros(9), X, shape)
+    bad = X.copy()
+    bad[1, 3] = np.nan
+    with pytest.raises(ob.DivergenceError, match="iteration"):
+        ob.evaluate_dictionary(ob.init_dictionary(shape, 2, 0), bad, shape)
+
+
+def test_sharded_checkpoint_resume_is_bit_identical(tmp_path):
+    """ShardedTrainer (world 1) checkpoint: per-rank file, reload, identical continuation."""
+    from paper_1706_06972_b200.sharded import LocalComm, ShardedTrainer
+
+    shape = ob.SignalShape((18, 12), (3, 3))
+    cfg = ob.TrainConfig(n_filters=4, dtype="float64", batch_size=3, beta=0.3, code_max_iters=80, inner_iters=4,
+                         stop_tol=1e-9)
+    X = synth_images(12, (16, 10), (18, 12), 2, filter_dims=(3, 3), seed=9).reshape(12, -1)
+    a = ShardedTrainer(shape, cfg)
+    objs_a = [a.partial_fit(X[3 * m:3 * m + 3]).objectives for m in range(4)]
+    b = ShardedTrainer(shape, cfg)
+    objs_b = [b.partial_fit(X[3 * m:3 * m + 3]).objectives for m in range(2)]
+    f = ob.save_checkpoint(b, tmp_path / "s")
+    assert f.endswith(".rank0of1.npz")
+    c = ShardedTrainer.load_checkpoint(tmp_path / "s", LocalComm())
+    objs_b += [c.partial_fit(X[3 * m:3 * m + 3]).objectives for m in range(2, 4)]
+    assert all(np.array_equal(p, q) for p, q in zip(objs_a, objs_b))
+    assert np.array_equal(a.final_filters(), c.final_filters())
+    assert a.history.count == c.history.count and a.dict_change == c.dict_change
