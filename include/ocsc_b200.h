@@ -57,6 +57,9 @@ int64_t ocsc_kernel_launches(void);
  * transforms.py:82-87, 148-158 (forward_dft[_cols]); :90-109, 161-176
  * (inverse_dft[_cols] + the imaginary-residue guard). */
 
+/* Create (and cache) the R2C and C2R plans for nplanes planes of H x W now, so the first
+ * transform of that batch does not pay plan creation (OnlineTrainer's per-sample step path). */
+int ocsc_fft_prepare(int dtype, int H, int W, int nplanes);
 /* xh[n] = rfft2(x[n]) for n < nplanes; x (nplanes,H,W) real -> xh (nplanes,H,Wh). */
 int ocsc_rfft2(int dtype, int H, int W, int nplanes, const void* x, void* xh, void* stream);
 /* x[n] = irfft2(xh[n]) / P.  xh is CLOBBERED (cuFFT C2R). */

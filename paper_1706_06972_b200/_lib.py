@@ -30,6 +30,7 @@ SIGNATURES = {
     "ocsc_last_error": [],
     "ocsc_abi_version": [],
     "ocsc_kernel_launches": [],
+    "ocsc_fft_prepare": [_I, _I, _I, _I],
     "ocsc_rfft2": [_I, _I, _I, _I, _P, _P, _P],
     "ocsc_irfft2": [_I, _I, _I, _I, _P, _P, _P],
     "ocsc_dft_cols": [_I, _I, _I, _I, _P, _I, _P, _I, _P],

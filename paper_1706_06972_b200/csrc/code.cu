@@ -12,6 +12,12 @@
 // iteration the reference would, without a host sync.
 #include <cufft.h>
 
+#include <deque>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
 #include "common.cuh"
 #include "transforms.cuh"
 
@@ -241,14 +247,77 @@ static int32_t* pinned_flags() {
   return p;
 }
 
+// One ADMM iteration of the batch (R2C, residual, C2R, update, decide) enqueued on stream s.
+template <typename T>
+static int admm_iteration(int dtype, int H, int W, int K, int B, const CodeWork& w, const void* xh, const void* Wh,
+                          const void* den, T invP, T kappa, double rel_tol, void* u, void* t, bool want_z,
+                          int32_t* iters, int32_t* status, cudaStream_t s) {
+  const int nf = H * (W / 2 + 1);
+  const int64_t n = (int64_t)K * H * W;
+  int32_t* flags = w.flags;
+  const dim3 rgrid(ceil_div(nf, 256), B);
+  int ux = ceil_div(n, 256 * 4);
+  if (ux > 1024) ux = 1024;
+  const dim3 ugrid(ux, B);
+  int rc = exec_r2c(dtype, H, W, B * K, t, w.spec, s);
+  if (rc) return rc;
+  k_residual<T><<<rgrid, 256, 0, s>>>(B, K, nf, (const cx<T>*)Wh, (const cx<T>*)xh, (const T*)den,
+                                       (cx<T>*)w.spec, flags, flags + 2 * B);
+  rc = exec_c2r(dtype, H, W, B * K, w.spec, w.cbuf, s);
+  if (rc) return rc;
+  if (want_z)
+    k_update<T, true><<<ugrid, 256, 0, s>>>(n, invP, kappa, (T*)u, (T*)t, (const T*)w.cbuf, (T*)w.zsp, flags,
+                                             flags + B, flags + 2 * B, w.acc);
+  else
+    k_update<T, false><<<ugrid, 256, 0, s>>>(n, invP, kappa, (T*)u, (T*)t, (const T*)w.cbuf, nullptr, flags,
+                                              flags + B, flags + 2 * B, w.acc);
+  k_decide<<<1, 256, 0, s>>>(B, rel_tol, w.acc, flags, iters, status);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? OCSC_OK : cuda_fail(e, "code ADMM launch");
+}
+
+// Chunks of iterations as CUDA graphs: the cuFFT path of a small problem (the reference's B = 1
+// OnlineTrainer.step, evaluation) is launch-bound at ~5 launches per iteration; one graph launch
+// per poll interval replaces them.  Graphs are captured on a private stream (the caller's may be
+// the legacy default stream, which cannot be captured), cached per argument set (the trainer's
+// buffers are stable across calls), and replayed on the caller's stream.  OCSC_NO_GRAPH=1 keeps
+// plain stream launches.
+namespace {
+using GraphKey = std::tuple<int, int, int, int, int, int, std::vector<const void*>, double, double, double, int>;
+std::map<GraphKey, cudaGraphExec_t>& graph_cache() {
+  static std::map<GraphKey, cudaGraphExec_t> m;
+  return m;
+}
+std::deque<GraphKey>& graph_order() {  // insertion order: the cache keeps the newest kMaxGraphs
+  static std::deque<GraphKey> q;
+  return q;
+}
+std::map<GraphKey, int>& graph_seen() {  // capture on the second call with an argument set only
+  static std::map<GraphKey, int> m;
+  return m;
+}
+constexpr size_t kMaxGraphs = 64;
+std::mutex& graph_mu() {
+  static std::mutex m;
+  return m;
+}
+cudaStream_t capture_stream(int dev) {
+  static std::map<int, cudaStream_t> m;
+  auto it = m.find(dev);
+  if (it != m.end()) return it->second;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  m[dev] = st;
+  return st;
+}
+}  // namespace
+
 template <typename T>
 static int code_admm_impl(int dtype, int H, int W, int K, int B, const void* xh, const void* Wh, const void* den,
                           double beta, double rho, int max_iters, double rel_tol, void* u, void* t, void* zh,
                           void* work, int32_t* iters, int32_t* status, int poll, cudaStream_t s) {
   CodeWork w;
   layout(dtype, H, W, K, B, zh != nullptr, &w, (char*)work);
-  const int nf = H * (W / 2 + 1);
-  const int64_t n = (int64_t)K * H * W;
   int32_t* flags = w.flags;
   OCSC_CUDA(cudaMemsetAsync(w.acc, 0, sizeof(double) * 4 * B, s));
   OCSC_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * (2 * B + 2), s));
@@ -263,12 +332,57 @@ static int code_admm_impl(int dtype, int H, int W, int K, int B, const void* xh,
   rc = get_plan(1, dtype, H, W, B * K, &ph);
   if (rc) return rc;
 
-  const dim3 rgrid(ceil_div(nf, 256), B);
-  int ux = ceil_div(n, 256 * 4);
-  if (ux > 1024) ux = 1024;
-  const dim3 ugrid(ux, B);
   const T invP = (T)(1.0 / ((double)H * W));
   const T kappa = (T)(beta / rho);
+  const bool want_z = zh != nullptr;
+  const int step = poll > 0 ? poll : 16;  // iterations per graph / per convergence poll
+  static const bool no_graph = getenv("OCSC_NO_GRAPH") != nullptr;
+  int dev = 0;
+  OCSC_CUDA(cudaGetDevice(&dev));
+
+  // the graph of n iterations for these arguments (captured on first use)
+  auto chunk_graph = [&](int n, cudaGraphExec_t* out) -> int {
+    GraphKey key{dev, dtype, H, W, K, B, {xh, Wh, den, u, t, zh, work, iters, status}, beta, rho, rel_tol, n};
+    std::lock_guard<std::mutex> lk(graph_mu());
+    auto it = graph_cache().find(key);
+    if (it != graph_cache().end()) {
+      *out = it->second;
+      return OCSC_OK;
+    }
+    *out = nullptr;
+    if (graph_seen()[key]++ == 0) return OCSC_OK;  // a one-off argument set runs as plain launches
+    if (graph_seen().size() > 4 * kMaxGraphs) graph_seen().clear();
+    cudaStream_t cap = capture_stream(dev);
+    if (!cap) return fail(OCSC_ECUDA, "code_admm: capture stream");
+    OCSC_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    int rc2 = OCSC_OK;
+    for (int i = 0; i < n && rc2 == OCSC_OK; ++i)
+      rc2 = admm_iteration<T>(dtype, H, W, K, B, w, xh, Wh, den, invP, kappa, rel_tol, u, t, want_z, iters, status,
+                              cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap, &g);
+    if (rc2) {
+      if (g) cudaGraphDestroy(g);
+      return rc2;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "code_admm: end capture");
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "code_admm: instantiate");
+    graph_cache()[key] = ex;
+    graph_order().push_back(key);
+    if (graph_order().size() > kMaxGraphs) {
+      auto old = graph_cache().find(graph_order().front());
+      if (old != graph_cache().end()) {
+        cudaGraphExecDestroy(old->second);
+        graph_cache().erase(old);
+      }
+      graph_order().pop_front();
+    }
+    *out = ex;
+    return OCSC_OK;
+  };
 
   int32_t* host = poll > 0 ? pinned_flags() : nullptr;
   cudaEvent_t ev[2] = {nullptr, nullptr};
@@ -278,24 +392,21 @@ static int code_admm_impl(int dtype, int H, int W, int K, int B, const void* xh,
   }
   int chunk = 0;
   bool stop = false;
-  for (int it = 1; it <= max_iters && !stop; ++it) {
-    rc = exec_r2c(dtype, H, W, B * K, t, w.spec, s);
-    if (rc) break;
-    k_residual<T><<<rgrid, 256, 0, s>>>(B, K, nf, (const cx<T>*)Wh, (const cx<T>*)xh, (const T*)den,
-                                         (cx<T>*)w.spec, flags, flags + 2 * B);
-    rc = exec_c2r(dtype, H, W, B * K, w.spec, w.cbuf, s);
-    if (rc) break;
-    if (zh)
-      k_update<T, true><<<ugrid, 256, 0, s>>>(n, invP, kappa, (T*)u, (T*)t, (const T*)w.cbuf, (T*)w.zsp, flags,
-                                               flags + B, flags + 2 * B, w.acc);
-    else
-      k_update<T, false><<<ugrid, 256, 0, s>>>(n, invP, kappa, (T*)u, (T*)t, (const T*)w.cbuf, nullptr, flags,
-                                                flags + B, flags + 2 * B, w.acc);
-    k_decide<<<1, 256, 0, s>>>(B, rel_tol, w.acc, flags, iters, status);
-    count_launches(3);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) { rc = cuda_fail(e, "code ADMM launch"); break; }
-    if (host && it % poll == 0 && it < max_iters) {
+  for (int it = 0; it < max_iters && !stop && rc == OCSC_OK;) {
+    const int n = std::min(step, max_iters - it);
+    cudaGraphExec_t ex = nullptr;
+    if (!no_graph) rc = chunk_graph(n, &ex);
+    if (rc == OCSC_OK && ex) {
+      cudaError_t e = cudaGraphLaunch(ex, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "code_admm: graph launch");
+    } else {
+      for (int i = 0; i < n && rc == OCSC_OK; ++i)
+        rc = admm_iteration<T>(dtype, H, W, K, B, w, xh, Wh, den, invP, kappa, rel_tol, u, t, want_z, iters, status,
+                               s);
+    }
+    count_launches(3 * n);
+    it += n;
+    if (host && it < max_iters && rc == OCSC_OK) {
       const int slot = chunk & 1;
       cudaMemcpyAsync(host + slot, flags + 2 * B, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
       cudaEventRecord(ev[slot], s);

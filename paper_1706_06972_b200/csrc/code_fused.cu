@@ -153,7 +153,13 @@ __device__ __forceinline__ T clampk(T w, T k) {
   return fmin(fmax(w, -k), k);  // Gamma = clip(w); NaN maps to -k so U = w - Gamma stays NaN
 }
 
-// half spectrum row[0..M] of a real row  ->  z = conj(Ze + i Zo) (inverse through the forward FFT)
+// Real rows of N = 2M pixels as M-point complex FFTs of p[m] = x[2m] + i x[2m+1].  Both
+// conversions below are written in 2-wide form (FFMA2 with swizzled operands, the +-1 factors
+// exact) and carry a factor 2 against the textbook split, which the callers fold elsewhere.
+//
+// half spectrum row[0..M] of a real row  ->  z with FFT_M(z) = 2 M conj(p) (inverse through the
+// forward FFT):  z_k = conj(Ze' + i Zo'),  Ze' = A + conj(B),  Zo' = (A - conj(B)) e^{+2 pi i k/N},
+// A = row[k], B = row[M - k]  (the textbook Ze, Zo are half of these)
 template <typename C, int N>
 __device__ __forceinline__ void row_inverse_pre(const C* row, C (&z)[N / 2]) {
   using T = decltype(C::x);
@@ -165,16 +171,17 @@ __device__ __forceinline__ void row_inverse_pre(const C* row, C (&z)[N / 2]) {
       A_.y = 0;
       B_.y = 0;
     }
-    const T zex = (T)0.5 * (A_.x + B_.x), zey = (T)0.5 * (A_.y - B_.y);
-    const T dx = (T)0.5 * (A_.x - B_.x), dy = (T)0.5 * (A_.y + B_.y);
     constexpr T c = (T)sfft::ce_cos(2.0 * sfft::kPi * k / N);
     constexpr T s = (T)sfft::ce_sin(2.0 * sfft::kPi * k / N);
-    const T zox = c * dx - s * dy, zoy = c * dy + s * dx;  // Zo = D e^{+2 pi i k/N}
-    z[k] = mkc<C>(zex - zoy, -(zey + zox));                // conj(Ze + i Zo)
+    const C d = vfma(B_, mkc<C>(-1, 1), A_);                 // A - conj(B)
+    const C ze = vfma(A_, mkc<C>(1, -1), B_);                // conj(A) + B = conj(Ze')
+    // conj(Ze' + i Zo') = conj(Ze') - c swap(d) + s (-d.x, d.y)
+    z[k] = vfma(d, mkc<C>(-s, s), vfma(vswap(d), vsplat<C>(-c), ze));
   });
 }
 
-// Z = FFT_M(even + i odd)  ->  half spectrum row[0..M] of the real row
+// Z = FFT_M(p / 2)  ->  half spectrum row[0..M] of the real row:
+// X_k = Ze + W^k Zo with Ze = Z_k + conj(Z_{M-k}), Zo = -i (Z_k - conj(Z_{M-k})), W = e^{-2 pi i/N}
 template <typename C, int N>
 __device__ __forceinline__ void row_forward_post(const C (&Z)[N / 2], C* row) {
   using T = decltype(C::x);
@@ -182,11 +189,12 @@ __device__ __forceinline__ void row_forward_post(const C (&Z)[N / 2], C* row) {
   sfft::static_for<0, M + 1>([&](auto Kk) {
     constexpr int k = decltype(Kk)::value;
     const C a = Z[k % M], bb = Z[(M - k) % M];
-    const T zex = (T)0.5 * (a.x + bb.x), zey = (T)0.5 * (a.y - bb.y);
-    const T zox = (T)0.5 * (a.y + bb.y), zoy = (T)0.5 * (bb.x - a.x);  // Zo = -i (a - conj bb)/2
     constexpr T c = (T)sfft::ce_cos(2.0 * sfft::kPi * k / N);
     constexpr T s = (T)sfft::ce_sin(2.0 * sfft::kPi * k / N);
-    row[k] = mkc<C>(zex + c * zox + s * zoy, zey + c * zoy - s * zox);  // Ze + e^{-2 pi i k/N} Zo
+    const C ze = vfma(bb, mkc<C>(1, -1), a);   // a + conj(bb)
+    const C dm = vfma(bb, mkc<C>(-1, 1), a);   // a - conj(bb)
+    // W^k (-i) dm = (-s - i c) dm = -s dm + c (dm.y, -dm.x)
+    row[k] = vfma(vswap(dm), mkc<C>(c, -c), vfma(dm, vsplat<C>(-s), ze));
   });
 }
 
@@ -223,7 +231,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
   const T kappa = a.kappa;
-  const T cscl = (T)(2.0 / ((double)N * N));  // c = (2/P) IFFT_M(z): the M-point inverse covers half a row
+  const T cscl = (T)(1.0 / ((double)N * N));  // c = (1/P) FFT_M(z): z carries 2x (row_inverse_pre)
   const C* Dg = a.Wh + (int64_t)k0 * NF;
 
   // column task of this lane: item (plane cj, column cv) shared by lanes l and l^16, index parity h
@@ -247,6 +255,11 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     dsl[i] = f < NF ? (T)1 / a.den[f] : (T)0;
   }
   const int nwarps = nt >> 5;
+  __shared__ void* gtab_[16];  // gS of every CTA of the cluster (DSMEM addresses)
+  __shared__ int s_stat;       // this iteration's stopping decision (warp 0)
+  C** gtab = reinterpret_cast<C**>(gtab_);
+  if (tid < CS) gtab[tid] = cl.map_shared_rank(gS, tid);
+  if (tid == 0) s_stat = 0;
   __syncthreads();
 
   // ---- column transform of item (cj, cv): Good-Thomas 2 x M across lanes l, l^16 ----------
@@ -255,9 +268,24 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   const int dpx = hpar ? M * RS : 0;  // +M rows in the workspace
   const int dpd = hpar ? M * Wh : 0;  // +M rows in D / F(U)
   const T sgn = hpar ? (T)-1 : (T)1;
-  auto col_phase = [&](auto mode_c, C* emit) {
+  // the D values a COL_I pass multiplies by, loaded ahead (before the cluster barrier that
+  // precedes the pass, so their L2 latency hides under the barrier wait)
+  struct ColRegs {
+    C v[M];
+  };
+  auto load_dcol = [&](ColRegs& dz) {
+    sfft::static_for<0, M>([&](auto Nn) {
+      constexpr int n2 = decltype(Nn)::value;
+      constexpr int u0 = 2 * n2;
+      constexpr int sh = (u0 < M) ? 1 : -1;
+      dz.v[n2] = dcol[u0 * Wh + sh * dpd];
+    });
+  };
+  // COL_F / COL_FE: forward column transform of the row-transformed planes (raw, the D multiply
+  // happens in reduce_push); COL_I: inverse column transform of conj(D) g (z holds D on entry)
+  auto col_phase = [&](auto mode_c, C* emit, ColRegs& zr) {
     constexpr int mode = decltype(mode_c)::value;
-    C z[M];
+    C (&z)[M] = zr.v;
     sfft::static_for<0, M>([&](auto Nn) {
       constexpr int n2 = decltype(Nn)::value;
       constexpr int u0 = 2 * n2;                  // row for h = 0
@@ -265,7 +293,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       const int ox = u0 * RS + sh * dpx;
       if constexpr (mode == COL_I) {
         const C g = gS[ox + cv];
-        z[n2] = cmul(dcol[u0 * Wh + sh * dpd], mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
+        z[n2] = cmul2(z[n2], mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
       } else {
         z[n2] = colp[ox];
       }
@@ -282,9 +310,8 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
         if constexpr (mode == COL_I) {
           colp[ox] = mkc<C>(o.x, -o.y);
         } else {
-          const int od = kA * Wh + sh * dpd;
-          if constexpr (mode == COL_FE) emit[(int64_t)cj * NF + od + cv] = o;
-          colp[ox] = cmul(dcol[od], o);
+          if constexpr (mode == COL_FE) emit[(int64_t)cj * NF + kA * Wh + sh * dpd + cv] = o;
+          colp[ox] = o;
         }
       }
     });
@@ -292,22 +319,44 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   // partial synthesis sum over own filters, pushed straight into the owner CTA's receive slot
   // (owner of frequency f = the CTA whose slice [f0, f1) contains it); part is CS x slice
   const int slice = (NF + CS - 1) / CS;
+  // thread -> frequencies f = tid + i nt (consecutive across lanes: coalesced D loads); the
+  // workspace offset and the owner's receive slot are computed once
+  constexpr int RP = 3;  // frequencies per thread: NF <= RP * threads for every launch shape
+  int ro[RP];
+  C* rdst[RP];
+  const C* rdg[RP];
+#pragma unroll
+  for (int i = 0; i < RP; ++i) {
+    const int f = tid + i * nt;
+    ro[i] = -1;
+    rdst[i] = nullptr;
+    rdg[i] = Dg;
+    if (f < NF) {
+      const int u = f / Wh, v = f - u * Wh, owner = f / slice;
+      ro[i] = u * RS + v;
+      rdst[i] = cl.map_shared_rank(part, owner) + r * slice + (f - owner * slice);
+      rdg[i] = Dg + f;
+    }
+  }
+  // partial synthesis sum_k D_k F(t_k) over own filters, pushed into the owner CTA's slot;
+  // the nk (D, X) loads of a frequency are independent, so they issue back to back
+  auto push_item = [&](int o, const C* dg, C* dst) {
+    C s = mkc<C>(0, 0), s2 = mkc<C>(0, 0);
+    int j = 0;
+    for (; j + 1 < nk; j += 2) {
+      s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
+      s2 = vfma_c(dg[(int64_t)(j + 1) * NF], X[(j + 1) * PS + o], s2);
+    }
+    if (j < nk) s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
+    *dst = vadd(s, s2);
+  };
   auto reduce_push = [&]() {
-    // iterate the workspace index o = u*RS + v (v < Wh) so a warp reads contiguous words
-    for (int o = tid; o < N * RS; o += nt) {
-      const int u = o / RS, v = o - u * RS;
-      if (v >= Wh) continue;
-      C s = mkc<C>(0, 0), s2 = mkc<C>(0, 0);  // two chains: the loads issue back to back
-      int j = 0;
-      for (; j + 1 < nk; j += 2) {
-        s = vadd(s, X[j * PS + o]);
-        s2 = vadd(s2, X[(j + 1) * PS + o]);
-      }
-      if (j < nk) s = vadd(s, X[j * PS + o]);
-      s = vadd(s, s2);
-      const int f = u * Wh + v;
-      const int owner = f / slice;
-      cl.map_shared_rank(part, owner)[r * slice + (f - owner * slice)] = s;
+#pragma unroll
+    for (int i = 0; i < RP; ++i)
+      if (ro[i] >= 0) push_item(ro[i], rdg[i], rdst[i]);
+    for (int f = tid + RP * nt; f < NF; f += nt) {  // small launch shapes only
+      const int u = f / Wh, v = f - u * Wh, owner = f / slice;
+      push_item(u * RS + v, Dg + f, cl.map_shared_rank(part, owner) + r * slice + (f - owner * slice));
     }
   };
   // y[f] for my slice from the CS received partials (local loads only)
@@ -329,9 +378,12 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       itl[it] = global_ns();
       itl[512 + it] = clock64();
     }
-    // ---- A: forward column transforms times D, partial synthesis ------------------------
+    // ---- A: forward column transforms, partial synthesis sum_k D_k F(t_k) ----------------
     OCSC_STAMP(0);
-    col_phase(std::integral_constant<int, COL_F>{}, nullptr);
+    {
+      ColRegs zc;
+      col_phase(std::integral_constant<int, COL_F>{}, nullptr, zc);
+    }
     __syncthreads();
     OCSC_STAMP(1);
     reduce_push();
@@ -348,13 +400,13 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
         const int fl = f - f0;
         const C g = cscale(csub(xsl[fl], y), dsl[fl]);
         const int o = (f / Wh) * RS + f % Wh;
-        for (int qq = 0; qq < CS; ++qq) cl.map_shared_rank(gS, qq)[o] = g;
+        for (int qq = 0; qq < CS; ++qq) gtab[qq][o] = g;
       }
     }
-    bool stop = false;
-    if (it > 0) {
-      // every warp reduces the CS x nwarps partials in the same fixed order (lane-strided,
-      // then a fixed butterfly): identical decision everywhere, no block barrier
+    if (warp == 0 && it > 0) {
+      // warp 0 of every CTA reduces the CS x nwarps partials in the same fixed order
+      // (lane-strided, then a fixed butterfly): the same decision in every CTA, published to
+      // the CTA through shared memory and read after the cluster barrier below
       T n4[5] = {0, 0, 0, 0, 0};
       for (int qq = 0; qq < CS; ++qq) {
         if (lane < nwarps) {
@@ -373,19 +425,22 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       int st_ = 0;
       if (n4[4] > (T)0) st_ = 2;
       else if (n4[0] <= tol2 * fmax(n4[1], fl2) && n4[2] <= tol2 * fmax(fmax(n4[1], n4[3]), fl2)) st_ = 1;
-      if (st_) {
-        stat = st_;
-        stop = true;
-      }
+      if (lane == 0) s_stat = st_;
     }
-    if (!stop && it == a.max_iters) stop = true;
-    if (stop) break;
-    ++it;
+    // D for the inverse column pass, loaded before the barrier (its L2 latency hides there)
+    ColRegs zi;
+    load_dcol(zi);
     OCSC_STAMP(4);
-    cl.sync();  // #2: g complete in every CTA
+    cl.sync();  // #2: g complete in every CTA; this CTA's stopping decision visible
     OCSC_STAMP(5);
+    if (it > 0 && s_stat) {
+      stat = s_stat;
+      break;
+    }
+    if (it == a.max_iters) break;
+    ++it;
     // ---- B: inverse column transforms of conj(D) g ---------------------------------------
-    col_phase(std::integral_constant<int, COL_I>{}, nullptr);
+    col_phase(std::integral_constant<int, COL_I>{}, nullptr, zi);
     __syncthreads();
     // ---- C: row IFFT -> c -> update w (registers) -> t -> row FFT --------------------------
     // (even, odd) pixel pairs run as 2-wide FP32x2 arithmetic
@@ -394,15 +449,14 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       C z[M];
       row_inverse_pre<C, N>(xrow, z);
       sfft::fft<C, M, false>(z);
-      const C cs2 = mkc<C>(cscl, -cscl);  // c = (Re, -Im) * 2/P of the conjugated result
+      const C cs2 = mkc<C>(cscl, -cscl);  // c = (Re, -Im) / P of the conjugated result
       C* w2 = reinterpret_cast<C*>(wrow);
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        const C c = vmul(z[m], cs2);
         const C wo = w2[m];
         const C go = mkc<C>(clampk(wo.x, kappa), clampk(wo.y, kappa));
         const C uo = vsub(wo, go);
-        const C wn = vadd(uo, c);
+        const C wn = vfma(z[m], cs2, uo);  // w' = S(w) + c
         const C gn = mkc<C>(clampk(wn.x, kappa), clampk(wn.y, kappa));
         const C un = vsub(wn, gn);
         const C d0 = vsub(un, uo), d2 = vsub(gn, go);  // a non-finite code poisons these sums
@@ -411,7 +465,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
         s2 = vfma(d2, d2, s2);
         s3 = vfma(gn, gn, s3);
         w2[m] = wn;
-        z[m] = vsub(un, gn);  // t for the next iteration
+        z[m] = vfma(wn, vsplat<C>((T)0.5), mkc<C>(-gn.x, -gn.y));  // t / 2 = (w' - 2 clip(w')) / 2 (row_forward_post)
       }
       sfft::fft<C, M, false>(z);
       row_forward_post<C, N>(z, xrow);
@@ -457,14 +511,17 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
         to[2 * m + 1] = ub - gb;
       }
       l1 += fabs((double)ua) + fabs((double)ub);
-      z[m] = mkc<C>(ua, ub);
+      z[m] = mkc<C>((T)0.5 * ua, (T)0.5 * ub);  // row_forward_post takes the half-scaled row
     }
     sfft::fft<C, M, false>(z);
     row_forward_post<C, N>(z, xrow);
   }
   __syncthreads();
   if (itl) itl[506] = global_ns();
-  col_phase(std::integral_constant<int, COL_FE>{}, a.uh_out + ((int64_t)b * K + k0) * NF);
+  {
+    ColRegs zc;
+    col_phase(std::integral_constant<int, COL_FE>{}, a.uh_out + ((int64_t)b * K + k0) * NF, zc);
+  }
   __syncthreads();
   if (itl) itl[507] = global_ns();
   reduce_push();

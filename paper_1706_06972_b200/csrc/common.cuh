@@ -95,6 +95,39 @@ __device__ __forceinline__ double2 vfma(double2 a, double2 b, double2 c) {
 __device__ __forceinline__ double2 vsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 template <typename C> __device__ __forceinline__ C vsplat(decltype(C::x) s) { return mkc<C>(s, s); }
 
+// ---- complex products and +-i combinations in 2-wide form ----------------------------------
+// float2: FMUL2 / FFMA2 with a broadcast scalar and a swizzled (LO_HI) operand -- two
+// instructions per complex product, one per a -+ i b (the +-1 multiplies are exact, so the
+// latter round exactly like the scalar form).  double2: the scalar forms.
+__device__ __forceinline__ float2 cmul2(float2 a, float2 b) {  // a * b
+  return __ffma2_rn(make_float2(b.y, b.x), make_float2(-a.y, a.y), __fmul2_rn(make_float2(a.x, a.x), b));
+}
+__device__ __forceinline__ float2 cmulc2(float2 a, float2 b) {  // conj(a) * b
+  return __ffma2_rn(make_float2(b.y, b.x), make_float2(a.y, -a.y), __fmul2_rn(make_float2(a.x, a.x), b));
+}
+__device__ __forceinline__ float2 sub_i(float2 a, float2 b) {  // a - i b
+  return __ffma2_rn(make_float2(b.y, b.x), make_float2(1.f, -1.f), a);
+}
+__device__ __forceinline__ float2 add_i(float2 a, float2 b) {  // a + i b
+  return __ffma2_rn(make_float2(b.y, b.x), make_float2(-1.f, 1.f), a);
+}
+__device__ __forceinline__ float2 vswap(float2 a) { return make_float2(a.y, a.x); }
+__device__ __forceinline__ float2 vfma_c(float2 a, float2 b, float2 acc) {  // acc + a * b
+  return __ffma2_rn(make_float2(b.y, b.x), make_float2(-a.y, a.y), __ffma2_rn(make_float2(a.x, a.x), b, acc));
+}
+__device__ __forceinline__ double2 vfma_c(double2 a, double2 b, double2 acc) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ double2 cmul2(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulc2(double2 a, double2 b) {
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 sub_i(double2 a, double2 b) { return make_double2(a.x + b.y, a.y - b.x); }
+__device__ __forceinline__ double2 add_i(double2 a, double2 b) { return make_double2(a.x - b.y, a.y + b.x); }
+__device__ __forceinline__ double2 vswap(double2 a) { return make_double2(a.y, a.x); }
+
 template <typename To, typename From> __device__ __forceinline__ cx<To> ccast(From a) {
   return mkc<cx<To>>((To)a.x, (To)a.y);
 }

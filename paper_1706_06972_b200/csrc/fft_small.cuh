@@ -89,7 +89,7 @@ __device__ __forceinline__ C twiddle(C v) {
   } else {
     constexpr T c = (T)ce_cos(2.0 * kPi * e / N);
     constexpr T s = (T)((INV ? 1.0 : -1.0) * ce_sin(2.0 * kPi * e / N));
-    return mkc<C>(v.x * c - v.y * s, v.x * s + v.y * c);
+    return vfma(vswap(v), mkc<C>(-s, s), vmul(v, vsplat<C>(c)));  // (v.x c - v.y s, v.y c + v.x s)
   }
 }
 
@@ -128,11 +128,11 @@ __device__ __forceinline__ void dft_prime(C (&x)[R]) {
       });
       // forward: X[k] = a - i*b, X[R-k] = a + i*b (b = sum d_j sin); inverse swaps
       if constexpr (!INV) {
-        x[k] = mkc<C>(a.x + bsum.y, a.y - bsum.x);
-        x[R - k] = mkc<C>(a.x - bsum.y, a.y + bsum.x);
+        x[k] = sub_i(a, bsum);
+        x[R - k] = add_i(a, bsum);
       } else {
-        x[k] = mkc<C>(a.x - bsum.y, a.y + bsum.x);
-        x[R - k] = mkc<C>(a.x + bsum.y, a.y - bsum.x);
+        x[k] = add_i(a, bsum);
+        x[R - k] = sub_i(a, bsum);
       }
     });
     x[0] = sum;

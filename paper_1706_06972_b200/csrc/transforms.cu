@@ -206,6 +206,14 @@ using namespace ocsc;
     else return fail(OCSC_EARG, "dtype must be 4 or 8");     \
   } while (0)
 
+extern "C" int ocsc_fft_prepare(int dtype, int H, int W, int nplanes) {
+  if (H <= 0 || W <= 0 || nplanes <= 0) return fail(OCSC_ESHAPE, "fft_prepare: bad extents");
+  if (dtype != OCSC_F32 && dtype != OCSC_F64) return fail(OCSC_EARG, "dtype must be 4 or 8");
+  cufftHandle h;
+  int rc = get_plan(0, dtype, H, W, nplanes, &h);
+  return rc ? rc : get_plan(1, dtype, H, W, nplanes, &h);
+}
+
 extern "C" int ocsc_rfft2(int dtype, int H, int W, int nplanes, const void* x, void* xh, void* stream) {
   if (H <= 0 || W <= 0 || nplanes < 0) return fail(OCSC_ESHAPE, "rfft2: bad extents");
   if (dtype != OCSC_F32 && dtype != OCSC_F64) return fail(OCSC_EARG, "dtype must be 4 or 8");

@@ -195,6 +195,11 @@ class OnlineTrainer:
         self._x = None
         self._obj = None
         self._fused_ok = {}
+        # the reference's per-sample `step` path (B = 1, want_z): buffers and cuFFT plans made
+        # here, so the first step does not pay one-time plan creation
+        self._buffers(1, want_z=True)
+        _lib.call("ocsc_fft_prepare", _lib.code(self.dtype), self.H, self.W, self.K)
+        _lib.call("ocsc_fft_prepare", _lib.code(self.dtype), self.H, self.W, 1)
         self._side = None          # side stream + scratch of the overlapped history inverse
         self._tl = None            # dev aid: list collecting (label, timing event) of the overlap
         self.last_path = None      # device path of the last partial_fit (see partial_fit)
@@ -214,6 +219,7 @@ class OnlineTrainer:
             self._buf = CodeBuffers(self.shape, self.K, B, self.dtype, want_z=want_z)
             self._uh = torch.empty((B, self.K, self.H, self.W // 2 + 1), dtype=self.cdtype, device=self.dev)
             self._x = torch.empty((B, self.H, self.W), dtype=self.dtype, device=self.dev)
+            self._xh = torch.empty((B, self.H, self.W // 2 + 1), dtype=self.cdtype, device=self.dev)
             self._obj = torch.empty(B, dtype=torch.float64, device=self.dev)
         return self._buf
 
@@ -440,7 +446,8 @@ class OnlineTrainer:
         buf = self._buffers(B, want_z)
         x = self._x[:B]
         x.copy_(xs, non_blocking=True)
-        xh = rfft2_dev(x, self.shape)
+        # persistent spectrum buffer: the cuFFT path's CUDA graphs are keyed on stable pointers
+        xh = rfft2_dev(x, self.shape, out=self._xh[:B])
         uh = self._uh[:B]
         fused = self.use_fused(B) and not want_z
         stream = not fused and not want_z and self.config.stream and stream_supported(self.shape, self.dtype)

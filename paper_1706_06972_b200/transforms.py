@@ -154,12 +154,13 @@ def hermitian_defect(cols: torch.Tensor, shape: SignalShape) -> tuple[float, flo
     return a, b
 
 
-def rfft2_dev(planes: torch.Tensor, shape: SignalShape) -> torch.Tensor:
-    """(n, H, W) real -> (n, H, Wh) half spectra."""
+def rfft2_dev(planes: torch.Tensor, shape: SignalShape, out: torch.Tensor | None = None) -> torch.Tensor:
+    """(n, H, W) real -> (n, H, Wh) half spectra (into `out` when given)."""
     H, W = shape.grid
     n = planes.shape[0]
     cdt = torch.complex64 if planes.dtype == torch.float32 else torch.complex128
-    out = torch.empty((n, H, W // 2 + 1), dtype=cdt, device=planes.device)
+    if out is None:
+        out = torch.empty((n, H, W // 2 + 1), dtype=cdt, device=planes.device)
     _lib.call("ocsc_rfft2", _lib.code(planes.dtype), H, W, n, _lib.ptr(planes), _lib.ptr(out), _lib.stream())
     return out
 
