@@ -109,7 +109,7 @@ struct Smem {
     return al(sizeof(cx<T>) * (size_t)cs * ((G::NF + cs - 1) / cs));
   }
   // per-warp norm partials from every CTA of the cluster: [CS][32 warps][8] (arithmetic type)
-  static __host__ __device__ size_t n_bytes(int cs) { return al(sizeof(T) * 8 * 32 * (size_t)cs); }
+  static __host__ __device__ size_t n_bytes(int cs) { return al(sizeof(T) * 2 * 8 * 32 * (size_t)cs); }
   // this CTA's slice of the sample spectrum and of den
   static __host__ __device__ size_t s_bytes(int cs) {
     const size_t sl = (G::NF + cs - 1) / cs;
@@ -200,6 +200,52 @@ __device__ __forceinline__ void row_forward_post(const C (&Z)[N / 2], C* row) {
 
 enum ColMode : int { COL_F = 0, COL_I = 1, COL_FE = 2 };
 
+// ---- cluster exchange without cluster barriers: remote stores that complete a transaction count
+// on the receiver's mbarrier (st.async ... mbarrier::complete_tx), local waits on that mbarrier.
+// A receiver proceeds once its own data has landed; no GPU-scope fence or L1 invalidation (what
+// barrier.cluster.arrive.release / wait.acquire compile to) sits in the iteration.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(a), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* m, uint32_t tx) {  // the phase's one arrival + tx bytes
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t dst, float2 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(dst),
+               "f"(v.x), "f"(v.y), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t dst, double2 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+               "d"(v.x), "d"(v.y), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t dst, float v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(dst), "f"(v),
+               "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(v),
+               "r"(mbar)
+               : "memory");
+}
+
 template <typename T, int N>
 __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   using C = cx<T>;
@@ -255,12 +301,31 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     dsl[i] = f < NF ? (T)1 / a.den[f] : (T)0;
   }
   const int nwarps = nt >> 5;
-  __shared__ void* gtab_[16];  // gS of every CTA of the cluster (DSMEM addresses)
-  __shared__ int s_stat;       // this iteration's stopping decision (warp 0)
-  C** gtab = reinterpret_cast<C**>(gtab_);
-  if (tid < CS) gtab[tid] = cl.map_shared_rank(gS, tid);
-  if (tid == 0) s_stat = 0;
-  __syncthreads();
+  const int slice = (NF + CS - 1) / CS;
+  // exchange state: mb_part completes when every CTA's partial synthesis for this CTA's slice
+  // (and, from the second iteration on, every warp's stopping norms) has landed; mb_g when the
+  // g slices of every owner have landed.  Cluster addresses of every CTA's buffers, per rank.
+  __shared__ __align__(8) uint64_t mb_part, mb_g;
+  __shared__ uint32_t t_g[16], t_mbg[16], t_part[16], t_mbp[16], t_nrm[16];
+  if (tid < CS) {
+    t_g[tid] = mapa_u32(smem_u32(gS), tid);
+    t_mbg[tid] = mapa_u32(smem_u32(&mb_g), tid);
+    t_part[tid] = mapa_u32(smem_u32(part), tid);
+    t_mbp[tid] = mapa_u32(smem_u32(&mb_part), tid);
+    t_nrm[tid] = mapa_u32(smem_u32(nrm), tid);
+  }
+  const int my_slice = min(NF, (r + 1) * slice) - r * slice;
+  const uint32_t part_bytes = (uint32_t)(CS * my_slice * sizeof(C));
+  const uint32_t nrm_bytes = (uint32_t)(CS * nwarps * 5 * sizeof(T));
+  if (tid == 0) {
+    mbar_init(&mb_part, 1);
+    mbar_init(&mb_g, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arm(&mb_part, part_bytes);  // phase 0: partials only
+    mbar_arm(&mb_g, (uint32_t)(NF * sizeof(C)));
+  }
+  uint32_t ph_part = 0, ph_g = 0;
+  cl.sync();  // every CTA's barriers initialised before the first remote st.async
 
   // ---- column transform of item (cj, cv): Good-Thomas 2 x M across lanes l, l^16 ----------
   // lane parity h shifts every input/output row index by +-M (mod N): the shift's sign is a
@@ -318,29 +383,30 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   };
   // partial synthesis sum over own filters, pushed straight into the owner CTA's receive slot
   // (owner of frequency f = the CTA whose slice [f0, f1) contains it); part is CS x slice
-  const int slice = (NF + CS - 1) / CS;
   // thread -> frequencies f = tid + i nt (consecutive across lanes: coalesced D loads); the
   // workspace offset and the owner's receive slot are computed once
   constexpr int RP = 3;  // frequencies per thread: NF <= RP * threads for every launch shape
-  int ro[RP];
-  C* rdst[RP];
+  int ro[RP], rown[RP];
+  uint32_t rdst[RP];
   const C* rdg[RP];
 #pragma unroll
   for (int i = 0; i < RP; ++i) {
     const int f = tid + i * nt;
     ro[i] = -1;
-    rdst[i] = nullptr;
+    rdst[i] = 0;
+    rown[i] = 0;
     rdg[i] = Dg;
     if (f < NF) {
       const int u = f / Wh, v = f - u * Wh, owner = f / slice;
       ro[i] = u * RS + v;
-      rdst[i] = cl.map_shared_rank(part, owner) + r * slice + (f - owner * slice);
+      rown[i] = owner;
+      rdst[i] = t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C));
       rdg[i] = Dg + f;
     }
   }
   // partial synthesis sum_k D_k F(t_k) over own filters, pushed into the owner CTA's slot;
   // the nk (D, X) loads of a frequency are independent, so they issue back to back
-  auto push_item = [&](int o, const C* dg, C* dst) {
+  auto push_item = [&](int o, const C* dg, uint32_t dst, int owner) {
     C s = mkc<C>(0, 0), s2 = mkc<C>(0, 0);
     int j = 0;
     for (; j + 1 < nk; j += 2) {
@@ -348,15 +414,16 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       s2 = vfma_c(dg[(int64_t)(j + 1) * NF], X[(j + 1) * PS + o], s2);
     }
     if (j < nk) s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
-    *dst = vadd(s, s2);
+    st_async(dst, vadd(s, s2), t_mbp[owner]);
   };
   auto reduce_push = [&]() {
 #pragma unroll
     for (int i = 0; i < RP; ++i)
-      if (ro[i] >= 0) push_item(ro[i], rdg[i], rdst[i]);
+      if (ro[i] >= 0) push_item(ro[i], rdg[i], rdst[i], rown[i]);
     for (int f = tid + RP * nt; f < NF; f += nt) {  // small launch shapes only
       const int u = f / Wh, v = f - u * Wh, owner = f / slice;
-      push_item(u * RS + v, Dg + f, cl.map_shared_rank(part, owner) + r * slice + (f - owner * slice));
+      push_item(u * RS + v, Dg + f, t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C)),
+                owner);
     }
   };
   // y[f] for my slice from the CS received partials (local loads only)
@@ -388,29 +455,19 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     OCSC_STAMP(1);
     reduce_push();
     OCSC_STAMP(3);
-    cl.sync();  // #1: partials and the previous iteration's norms are visible
+    // #1: this CTA's slice of every partial (and every warp's stopping norms) has landed
+    mbar_wait(&mb_part, ph_part);
+    ph_part ^= 1;
     OCSC_STAMP(2);
-    // ---- y on my slice from the pushed partials, g = (X - y)/den, pushed to every rank -----
-    // (issued before the stopping decision so its latency overlaps; a stopping iteration just
-    // discards it)
-    {
-      const int f0 = r * slice, f1 = min(NF, f0 + slice);
-      for (int f = f0 + tid; f < f1; f += nt) {
-        const C y = gather_y(f);
-        const int fl = f - f0;
-        const C g = cscale(csub(xsl[fl], y), dsl[fl]);
-        const int o = (f / Wh) * RS + f % Wh;
-        for (int qq = 0; qq < CS; ++qq) gtab[qq][o] = g;
-      }
-    }
-    if (warp == 0 && it > 0) {
-      // warp 0 of every CTA reduces the CS x nwarps partials in the same fixed order
-      // (lane-strided, then a fixed butterfly): the same decision in every CTA, published to
-      // the CTA through shared memory and read after the cluster barrier below
+    const T* nr = nrm + (it & 1) * (8 * 32 * CS);  // the norms pushed by the last row phase
+    bool stop = false;
+    if (it > 0) {
+      // every warp reduces the CS x nwarps partials in the same fixed order (lane-strided,
+      // then a fixed butterfly): the same decision in every warp of every CTA, no barrier
       T n4[5] = {0, 0, 0, 0, 0};
       for (int qq = 0; qq < CS; ++qq) {
         if (lane < nwarps) {
-          const T* src = nrm + qq * 8 * 32 + lane;  // [qq][i][warp]: lanes read consecutive words
+          const T* src = nr + qq * 8 * 32 + lane;  // [qq][i][warp]: lanes read consecutive words
 #pragma unroll
           for (int i = 0; i < 5; ++i) n4[i] += src[i * 32];
         }
@@ -422,23 +479,36 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       // coding.py:113-118 on squared norms: num <= tol max(den, 1e-12) and
       // gap <= tol max(den, |dual|, 1e-12)
       const T tol2 = (T)(a.tol * a.tol), fl2 = (T)1e-24;
-      int st_ = 0;
-      if (n4[4] > (T)0) st_ = 2;
-      else if (n4[0] <= tol2 * fmax(n4[1], fl2) && n4[2] <= tol2 * fmax(fmax(n4[1], n4[3]), fl2)) st_ = 1;
-      if (lane == 0) s_stat = st_;
+      if (n4[4] > (T)0) stat = 2;
+      else if (n4[0] <= tol2 * fmax(n4[1], fl2) && n4[2] <= tol2 * fmax(fmax(n4[1], n4[3]), fl2)) stat = 1;
+      stop = stat != 0;
     }
-    // D for the inverse column pass, loaded before the barrier (its L2 latency hides there)
+    if (it == a.max_iters) stop = true;
+    // arm the next partial phase: the output stage's (partials only) or the next iteration's
+    // (partials + the norms of the row phase below)
+    if (tid == 0) mbar_arm(&mb_part, stop ? part_bytes : part_bytes + nrm_bytes);
+    if (stop) break;
+    ++it;
+    // ---- y on my slice from the pushed partials, g = (X - y)/den, pushed to every rank -----
+    {
+      const int f0 = r * slice, f1 = min(NF, f0 + slice);
+      for (int f = f0 + tid; f < f1; f += nt) {
+        const C y = gather_y(f);
+        const int fl = f - f0;
+        const C g = cscale(csub(xsl[fl], y), dsl[fl]);
+        const uint32_t o = (uint32_t)(((f / Wh) * RS + f % Wh) * sizeof(C));
+        for (int qq = 0; qq < CS; ++qq) st_async(t_g[qq] + o, g, t_mbg[qq]);
+      }
+    }
+    OCSC_STAMP(4);
+    // D for the inverse column pass, loaded before the wait (its L2 latency hides there)
     ColRegs zi;
     load_dcol(zi);
-    OCSC_STAMP(4);
-    cl.sync();  // #2: g complete in every CTA; this CTA's stopping decision visible
+    // #2: every owner's g slice has landed in this CTA
+    mbar_wait(&mb_g, ph_g);
+    ph_g ^= 1;
+    if (tid == 0) mbar_arm(&mb_g, (uint32_t)(NF * sizeof(C)));
     OCSC_STAMP(5);
-    if (it > 0 && s_stat) {
-      stat = s_stat;
-      break;
-    }
-    if (it == a.max_iters) break;
-    ++it;
     // ---- B: inverse column transforms of conj(D) g ---------------------------------------
     col_phase(std::integral_constant<int, COL_I>{}, nullptr, zi);
     __syncthreads();
@@ -479,10 +549,10 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       for (int i = 0; i < 5; ++i)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
-      if (lane < CS) {
-        T* dst = cl.map_shared_rank(nrm, lane) + r * 8 * 32 + warp;
+      if (lane < CS) {  // into the buffer the next decision reads (parity of the incremented it)
+        const uint32_t dst = t_nrm[lane] + (uint32_t)((((it & 1) * CS + r) * 8 * 32 + warp) * sizeof(T));
 #pragma unroll
-        for (int i = 0; i < 5; ++i) dst[i * 32] = q[i];
+        for (int i = 0; i < 5; ++i) st_async(dst + (uint32_t)(i * 32 * sizeof(T)), q[i], t_mbp[lane]);
       }
     }
     OCSC_STAMP(6);
@@ -525,7 +595,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   __syncthreads();
   if (itl) itl[507] = global_ns();
   reduce_push();
-  cl.sync();
+  mbar_wait(&mb_part, ph_part);
   if (itl) itl[508] = global_ns();
   double e = 0.0;
   {

@@ -195,11 +195,16 @@ class OnlineTrainer:
         self._x = None
         self._obj = None
         self._fused_ok = {}
-        # the reference's per-sample `step` path (B = 1, want_z): buffers and cuFFT plans made
-        # here, so the first step does not pay one-time plan creation
-        self._buffers(1, want_z=True)
-        _lib.call("ocsc_fft_prepare", _lib.code(self.dtype), self.H, self.W, self.K)
-        _lib.call("ocsc_fft_prepare", _lib.code(self.dtype), self.H, self.W, 1)
+        # the reference's per-sample `step` path (B = 1, want_z): buffers, cuFFT plans and the
+        # code ADMM's iteration graph (ocsc_code_admm captures it on the second use of an argument
+        # set) made here, so the first steps do not pay one-time setup
+        if config.batch_size == 1:
+            buf = self._buffers(1, want_z=True)
+            _lib.call("ocsc_fft_prepare", _lib.code(self.dtype), self.H, self.W, self.K)
+            _lib.call("ocsc_fft_prepare", _lib.code(self.dtype), self.H, self.W, 1)
+            self._xh[:1].zero_()  # a zero sample converges at iteration 1; the run is scratch only
+            infer_codes(self._xh[:1], self.Wh, self.den, shape, self.coding_config, buf, 1,
+                        max_iters=max(2 * config.poll, 1), poll=config.poll)
         self._side = None          # side stream + scratch of the overlapped history inverse
         self._tl = None            # dev aid: list collecting (label, timing event) of the overlap
         self.last_path = None      # device path of the last partial_fit (see partial_fit)
@@ -449,6 +454,8 @@ class OnlineTrainer:
         # persistent spectrum buffer: the cuFFT path's CUDA graphs are keyed on stable pointers
         xh = rfft2_dev(x, self.shape, out=self._xh[:B])
         uh = self._uh[:B]
+        nvtx = torch.cuda.nvtx
+        nvtx.range_push("ocsc.code")  # NVTX phase ranges (tracing); no-ops without a profiler
         fused = self.use_fused(B) and not want_z
         stream = not fused and not want_z and self.config.stream and stream_supported(self.shape, self.dtype)
         split = self._split_plan(B) if fused else 0
@@ -496,6 +503,7 @@ class OnlineTrainer:
             self._mark("coded")
             self._finish_inverse(B, inv_zeroed)
             self._mark("inverse finished")
+        nvtx.range_pop()
         if check or self._collective:
             it = -1
             if B:
@@ -507,6 +515,7 @@ class OnlineTrainer:
                 if pre:
                     side_done.synchronize()
                 raise DivergenceError(f"code solver diverged at iteration {it}")
+        nvtx.range_push("ocsc.fold")
         if not fused:
             obj, _ = code_objectives(xh, self.Wh, buf.u, self.shape, self.config.beta, B, uh)
         if split:
@@ -516,7 +525,10 @@ class OnlineTrainer:
             self._mark("woodbury")
         else:
             self._fold(uh, xh, B)
+        nvtx.range_pop()
+        nvtx.range_push("ocsc.dictionary")
         self._dictionary_update()
+        nvtx.range_pop()
         self._mark("dict end")
         track = self.config.stop_tol > 0
         if track:
