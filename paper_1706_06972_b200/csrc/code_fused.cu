@@ -216,13 +216,16 @@ __device__ __forceinline__ void mbar_init(uint64_t* m, int count) {
 __device__ __forceinline__ void mbar_arm(uint64_t* m, uint32_t tx) {  // the phase's one arrival + tx bytes
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(tx) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* m) {  // plain arrival (release: prior stores visible)
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(m)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)  // suspend-time hint: the warp sleeps instead of spinning
       : "memory");
 }
 __device__ __forceinline__ void st_async(uint32_t dst, float2 v, uint32_t mbar) {
@@ -306,6 +309,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   // (and, from the second iteration on, every warp's stopping norms) has landed; mb_g when the
   // g slices of every owner have landed.  Cluster addresses of every CTA's buffers, per rank.
   __shared__ __align__(8) uint64_t mb_part, mb_g;
+  __shared__ int s_stat;  // the stopping decision of this iteration (last warp)
   __shared__ uint32_t t_g[16], t_mbg[16], t_part[16], t_mbp[16], t_nrm[16];
   if (tid < CS) {
     t_g[tid] = mapa_u32(smem_u32(gS), tid);
@@ -319,12 +323,13 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   const uint32_t nrm_bytes = (uint32_t)(CS * nwarps * 5 * sizeof(T));
   if (tid == 0) {
     mbar_init(&mb_part, 1);
-    mbar_init(&mb_g, 1);
+    mbar_init(&mb_g, 2);  // tid 0's expect_tx + the last warp's arrival after it publishes the decision
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arm(&mb_part, part_bytes);  // phase 0: partials only
     mbar_arm(&mb_g, (uint32_t)(NF * sizeof(C)));
   }
   uint32_t ph_part = 0, ph_g = 0;
+  if (tid == 0) s_stat = 0;
   cl.sync();  // every CTA's barriers initialised before the first remote st.async
 
   // ---- column transform of item (cj, cv): Good-Thomas 2 x M across lanes l, l^16 ----------
@@ -460,10 +465,10 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     ph_part ^= 1;
     OCSC_STAMP(2);
     const T* nr = nrm + (it & 1) * (8 * 32 * CS);  // the norms pushed by the last row phase
-    bool stop = false;
-    if (it > 0) {
-      // every warp reduces the CS x nwarps partials in the same fixed order (lane-strided,
-      // then a fixed butterfly): the same decision in every warp of every CTA, no barrier
+    if (warp == nwarps - 1 && it > 0) {
+      // the last warp (no g work below) reduces the CS x nwarps partials in a fixed order
+      // (lane-strided, then a fixed butterfly): the same decision in every CTA; the rest of the
+      // CTA reads it after the g wait below (which orders it: this warp's own g stores follow)
       T n4[5] = {0, 0, 0, 0, 0};
       for (int qq = 0; qq < CS; ++qq) {
         if (lane < nwarps) {
@@ -479,16 +484,19 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       // coding.py:113-118 on squared norms: num <= tol max(den, 1e-12) and
       // gap <= tol max(den, |dual|, 1e-12)
       const T tol2 = (T)(a.tol * a.tol), fl2 = (T)1e-24;
-      if (n4[4] > (T)0) stat = 2;
-      else if (n4[0] <= tol2 * fmax(n4[1], fl2) && n4[2] <= tol2 * fmax(fmax(n4[1], n4[3]), fl2)) stat = 1;
-      stop = stat != 0;
+      int st_ = 0;
+      if (n4[4] > (T)0) st_ = 2;
+      else if (n4[0] <= tol2 * fmax(n4[1], fl2) && n4[2] <= tol2 * fmax(fmax(n4[1], n4[3]), fl2)) st_ = 1;
+      if (lane == 0) {
+        s_stat = st_;
+        // arm the next partial phase: the output stage's (partials only) or the next
+        // iteration's (partials + the norms of the row phase below)
+        mbar_arm(&mb_part, st_ || it == a.max_iters ? part_bytes : part_bytes + nrm_bytes);
+      }
+    } else if (warp == nwarps - 1 && lane == 0) {
+      mbar_arm(&mb_part, it == a.max_iters ? part_bytes : part_bytes + nrm_bytes);
     }
-    if (it == a.max_iters) stop = true;
-    // arm the next partial phase: the output stage's (partials only) or the next iteration's
-    // (partials + the norms of the row phase below)
-    if (tid == 0) mbar_arm(&mb_part, stop ? part_bytes : part_bytes + nrm_bytes);
-    if (stop) break;
-    ++it;
+    if (warp == nwarps - 1 && lane == 0) mbar_arrive(&mb_g);  // s_stat is published with this phase
     // ---- y on my slice from the pushed partials, g = (X - y)/den, pushed to every rank -----
     {
       const int f0 = r * slice, f1 = min(NF, f0 + slice);
@@ -504,9 +512,16 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     // D for the inverse column pass, loaded before the wait (its L2 latency hides there)
     ColRegs zi;
     load_dcol(zi);
-    // #2: every owner's g slice has landed in this CTA
+    // #2: every owner's g slice has landed in this CTA (g of a stopping iteration is pushed and
+    // waited for too, so no remote store is in flight when the CTAs leave the loop)
     mbar_wait(&mb_g, ph_g);
     ph_g ^= 1;
+    if (it > 0 && s_stat) {
+      stat = s_stat;
+      break;
+    }
+    if (it == a.max_iters) break;
+    ++it;
     if (tid == 0) mbar_arm(&mb_g, (uint32_t)(NF * sizeof(C)));
     OCSC_STAMP(5);
     // ---- B: inverse column transforms of conj(D) g ---------------------------------------
