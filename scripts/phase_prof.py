@@ -24,10 +24,15 @@ _lib.call("ocsc_code_fused", 4, 42, 42, 100, B, xh.data_ptr(), tr.Wh.data_ptr(),
 torch.cuda.synchronize()
 _lib.call("ocsc_debug_fused_profile", None)
 t = pbuf.cpu().numpy().reshape(8, 8)
-names = ["colF", "reduce+cs1", "exchange+decide", "(it++)", "cs2", "colI+row", "norm-push+sync"]
-d = np.diff(t, axis=1)
-print("cycles per phase (median over iters 8..14):")
-for i, n in enumerate(names): print(f"  {n:12s} {int(np.median(d[:7, i]))}")
+# stamp slots in time order (code_fused.cu OCSC_STAMP): 0 colF start, 1 after colF barrier,
+# 3 after reduce_push, 2 after the partials wait, 4 after g push, 5 after the g wait,
+# 6 after COL_I + rows + norm push, 7 after the end-of-iteration barrier
+order = [0, 1, 3, 2, 4, 5, 6, 7]
+names = ["colF+bar", "reduce_push", "wait partials", "decide+g push", "Dprefetch+wait g", "colI+bar+rows", "bar"]
+tt = t[:, order]
+d = np.diff(tt, axis=1)
+print("cycles per phase, CTA 0 thread 0 (median over iters 8..14):")
+for i, n in enumerate(names): print(f"  {n:18s} {int(np.median(d[:7, i]))}")
 print("  iteration  ", int(np.median(np.diff(t[:, 0]))))
 # wall-clock of the fused launch alone (events) to convert cycles -> time
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
