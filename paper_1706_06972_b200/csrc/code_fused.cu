@@ -421,10 +421,30 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     if (j < nk) s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
     st_async(dst, vadd(s, s2), t_mbp[owner]);
   };
+  // The D values of the RP precomputed items are loaded RC planes at a time, all items' loads of
+  // a chunk issued before any is consumed (the sum is L2-latency bound otherwise: one
+  // dependent round trip per plane pair)
+  constexpr int RC = 6;
   auto reduce_push = [&]() {
+    C acc[RP];
+#pragma unroll
+    for (int i = 0; i < RP; ++i) acc[i] = mkc<C>(0, 0);
+    for (int j0 = 0; j0 < nk; j0 += RC) {
+      C dv[RP][RC];
+#pragma unroll
+      for (int i = 0; i < RP; ++i)
+#pragma unroll
+        for (int u = 0; u < RC; ++u)
+          dv[i][u] = (ro[i] >= 0 && j0 + u < nk) ? rdg[i][(int64_t)(j0 + u) * NF] : mkc<C>(0, 0);
+#pragma unroll
+      for (int i = 0; i < RP; ++i)
+#pragma unroll
+        for (int u = 0; u < RC; ++u)
+          if (ro[i] >= 0 && j0 + u < nk) acc[i] = vfma_c(dv[i][u], X[(j0 + u) * PS + ro[i]], acc[i]);
+    }
 #pragma unroll
     for (int i = 0; i < RP; ++i)
-      if (ro[i] >= 0) push_item(ro[i], rdg[i], rdst[i], rown[i]);
+      if (ro[i] >= 0) st_async(rdst[i], acc[i], t_mbp[rown[i]]);
     for (int f = tid + RP * nt; f < NF; f += nt) {  // small launch shapes only
       const int u = f / Wh, v = f - u * Wh, owner = f / slice;
       push_item(u * RS + v, Dg + f, t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C)),
@@ -527,6 +547,7 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     // ---- B: inverse column transforms of conj(D) g ---------------------------------------
     col_phase(std::integral_constant<int, COL_I>{}, nullptr, zi);
     __syncthreads();
+    OCSC_STAMP(7);
     // ---- C: row IFFT -> c -> update w (registers) -> t -> row FFT --------------------------
     // (even, odd) pixel pairs run as 2-wide FP32x2 arithmetic
     C s0 = mkc<C>(0, 0), s1 = mkc<C>(0, 0), s2 = mkc<C>(0, 0), s3 = mkc<C>(0, 0);
@@ -572,7 +593,6 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     }
     OCSC_STAMP(6);
     __syncthreads();  // row outputs complete before the next column phase
-    OCSC_STAMP(7);
   }
 
   // ---- outputs: U = S(w) (and t), F(U), objective -------------------------------------------

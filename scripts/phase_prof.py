@@ -26,9 +26,9 @@ _lib.call("ocsc_debug_fused_profile", None)
 t = pbuf.cpu().numpy().reshape(8, 8)
 # stamp slots in time order (code_fused.cu OCSC_STAMP): 0 colF start, 1 after colF barrier,
 # 3 after reduce_push, 2 after the partials wait, 4 after g push, 5 after the g wait,
-# 6 after COL_I + rows + norm push, 7 after the end-of-iteration barrier
-order = [0, 1, 3, 2, 4, 5, 6, 7]
-names = ["colF+bar", "reduce_push", "wait partials", "decide+g push", "Dprefetch+wait g", "colI+bar+rows", "bar"]
+# 7 after COL_I + its barrier, 6 after rows + norm push (then the end-of-iteration barrier)
+order = [0, 1, 3, 2, 4, 5, 7, 6]
+names = ["colF+bar", "reduce_push", "wait partials", "decide+g push", "Dprefetch+wait g", "colI+bar", "rows+norms"]
 tt = t[:, order]
 d = np.diff(tt, axis=1)
 print("cycles per phase, CTA 0 thread 0 (median over iters 8..14):")
