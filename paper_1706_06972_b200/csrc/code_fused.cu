@@ -421,30 +421,12 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
     if (j < nk) s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
     st_async(dst, vadd(s, s2), t_mbp[owner]);
   };
-  // The D values of the RP precomputed items are loaded RC planes at a time, all items' loads of
-  // a chunk issued before any is consumed (the sum is L2-latency bound otherwise: one
-  // dependent round trip per plane pair)
-  constexpr int RC = 6;
+  // (the D loads of a frequency's planes are L2-bandwidth bound: ~100 KB per CTA per
+  // iteration; issuing all of a thread's loads at once measured slower, profiles/README.md)
   auto reduce_push = [&]() {
-    C acc[RP];
-#pragma unroll
-    for (int i = 0; i < RP; ++i) acc[i] = mkc<C>(0, 0);
-    for (int j0 = 0; j0 < nk; j0 += RC) {
-      C dv[RP][RC];
-#pragma unroll
-      for (int i = 0; i < RP; ++i)
-#pragma unroll
-        for (int u = 0; u < RC; ++u)
-          dv[i][u] = (ro[i] >= 0 && j0 + u < nk) ? rdg[i][(int64_t)(j0 + u) * NF] : mkc<C>(0, 0);
-#pragma unroll
-      for (int i = 0; i < RP; ++i)
-#pragma unroll
-        for (int u = 0; u < RC; ++u)
-          if (ro[i] >= 0 && j0 + u < nk) acc[i] = vfma_c(dv[i][u], X[(j0 + u) * PS + ro[i]], acc[i]);
-    }
 #pragma unroll
     for (int i = 0; i < RP; ++i)
-      if (ro[i] >= 0) st_async(rdst[i], acc[i], t_mbp[rown[i]]);
+      if (ro[i] >= 0) push_item(ro[i], rdg[i], rdst[i], rown[i]);
     for (int f = tid + RP * nt; f < NF; f += nt) {  // small launch shapes only
       const int u = f / Wh, v = f - u * Wh, owner = f / slice;
       push_item(u * RS + v, Dg + f, t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C)),
