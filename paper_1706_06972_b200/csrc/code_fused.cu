@@ -250,7 +250,7 @@ __device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t mbar) 
 }
 
 template <typename T, int N>
-__global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
+__global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T> a) {
   using C = cx<T>;
   using G = Geo<N>;
   using S = Smem<T, N>;
@@ -338,11 +338,14 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   const int dpx = hpar ? M * RS : 0;  // +M rows in the workspace
   const int dpd = hpar ? M * Wh : 0;  // +M rows in D / F(U)
   const T sgn = hpar ? (T)-1 : (T)1;
-  // the D values a COL_I pass multiplies by, loaded ahead (before the cluster barrier that
-  // precedes the pass, so their L2 latency hides under the barrier wait)
   struct ColRegs {
     C v[M];
   };
+  // D of this lane's column task: the lane of index parity h touches the rows of parity h both as
+  // COL_I inputs (row 2n (+-M), n = 0..M-1) and as COL_F outputs (row (M+1) k2 mod N = 2n (+-M)),
+  // so one array of M values covers both passes.  float: loaded once for the whole solve and kept
+  // in registers (no per-iteration D traffic); double: reloaded from L2 before each COL_I pass.
+  constexpr bool DREG = sizeof(T) == 4;
   auto load_dcol = [&](ColRegs& dz) {
     sfft::static_for<0, M>([&](auto Nn) {
       constexpr int n2 = decltype(Nn)::value;
@@ -351,8 +354,11 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       dz.v[n2] = dcol[u0 * Wh + sh * dpd];
     });
   };
-  // COL_F / COL_FE: forward column transform of the row-transformed planes (raw, the D multiply
-  // happens in reduce_push); COL_I: inverse column transform of conj(D) g (z holds D on entry)
+  ColRegs dreg;
+  if constexpr (DREG) load_dcol(dreg);
+  // COL_F / COL_FE: forward column transform of the row-transformed planes times D (COL_FE also
+  // emits the raw transform, F(U) for the history); COL_I: inverse column transform of conj(D) g
+  // (double: z holds D on entry)
   auto col_phase = [&](auto mode_c, C* emit, ColRegs& zr) {
     constexpr int mode = decltype(mode_c)::value;
     C (&z)[M] = zr.v;
@@ -363,7 +369,8 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       const int ox = u0 * RS + sh * dpx;
       if constexpr (mode == COL_I) {
         const C g = gS[ox + cv];
-        z[n2] = cmul2(z[n2], mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
+        const C d = DREG ? dreg.v[n2] : z[n2];
+        z[n2] = cmul2(d, mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
       } else {
         z[n2] = colp[ox];
       }
@@ -381,7 +388,8 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
           colp[ox] = mkc<C>(o.x, -o.y);
         } else {
           if constexpr (mode == COL_FE) emit[(int64_t)cj * NF + kA * Wh + sh * dpd + cv] = o;
-          colp[ox] = o;
+          if constexpr (DREG) colp[ox] = cmul2(dreg.v[kA / 2], o);  // kA is even (M + 1 is)
+          else colp[ox] = o;
         }
       }
     });
@@ -414,11 +422,19 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
   auto push_item = [&](int o, const C* dg, uint32_t dst, int owner) {
     C s = mkc<C>(0, 0), s2 = mkc<C>(0, 0);
     int j = 0;
-    for (; j + 1 < nk; j += 2) {
-      s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
-      s2 = vfma_c(dg[(int64_t)(j + 1) * NF], X[(j + 1) * PS + o], s2);
+    if constexpr (DREG) {  // X already holds D F(t): a plain sum over the CTA's planes
+      for (; j + 3 < nk; j += 4) {
+        s = vadd(s, vadd(X[j * PS + o], X[(j + 1) * PS + o]));
+        s2 = vadd(s2, vadd(X[(j + 2) * PS + o], X[(j + 3) * PS + o]));
+      }
+      for (; j < nk; ++j) s = vadd(s, X[j * PS + o]);
+    } else {
+      for (; j + 1 < nk; j += 2) {
+        s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
+        s2 = vfma_c(dg[(int64_t)(j + 1) * NF], X[(j + 1) * PS + o], s2);
+      }
+      if (j < nk) s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
     }
-    if (j < nk) s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
     st_async(dst, vadd(s, s2), t_mbp[owner]);
   };
   // (the D loads of a frequency's planes are L2-bandwidth bound: ~100 KB per CTA per
@@ -511,9 +527,9 @@ __global__ void __maxnreg__(96) k_code_fused(FusedArgs<T> a) {
       }
     }
     OCSC_STAMP(4);
-    // D for the inverse column pass, loaded before the wait (its L2 latency hides there)
+    // double: D for the inverse column pass, loaded before the wait (its L2 latency hides there)
     ColRegs zi;
-    load_dcol(zi);
+    if constexpr (!DREG) load_dcol(zi);
     // #2: every owner's g slice has landed in this CTA (g of a stopping iteration is pushed and
     // waited for too, so no remote store is in flight when the CTAs leave the loop)
     mbar_wait(&mb_g, ph_g);
