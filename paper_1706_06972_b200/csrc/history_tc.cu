@@ -120,33 +120,46 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
     uint32_t* Tb = T + buf * BUF_WORDS;
     const int b0 = ch * TKC;
     // ---- stage 8 samples (4 per thread): TF32 hi / lo split, K-major core-matrix layout ----
+    // a thread's 4 samples of one row are one 16-byte k-unit of every tile: one vector store per
+    // tile (a warp's 32 rows then fill 512 contiguous bytes, no bank conflicts)
+    {
+      uint32_t xh[4], xl[4], yh[4], yl[4], jxh[4], jxl[4], jyh[4], jyl[4];
 #pragma unroll
-    for (int s4 = 0; s4 < TKC / 2; ++s4) {
-      const int s = thalf * (TKC / 2) + s4;
-      const int b = b0 + s;
-      const uint32_t off = (s >> 2) * (TB * 4) + trow * 4 + (s & 3);  // word offset inside a tile
-      float2 vi = make_float2(0.f, 0.f), vj = make_float2(0.f, 0.f);
-      if (b < B) {
-        const int64_t base = (int64_t)b * z_sb + (int64_t)p * z_sp;
-        if (ri < K) vi = z[base + (int64_t)ri * z_sk];
-        if (!diag && rj < K) vj = z[base + (int64_t)rj * z_sk];
-        if (diag && ri < K) {  // cross term c_i += conj(x_b) z_bi on CUDA cores
-          const float2 xb = x[(int64_t)b * x_sb + (int64_t)p * x_sp];
-          cacc.x += xb.x * vi.x + xb.y * vi.y;
-          cacc.y += xb.x * vi.y - xb.y * vi.x;
+      for (int s4 = 0; s4 < TKC / 2; ++s4) {
+        const int b = b0 + thalf * (TKC / 2) + s4;
+        float2 vi = make_float2(0.f, 0.f), vj = make_float2(0.f, 0.f);
+        if (b < B) {
+          const int64_t base = (int64_t)b * z_sb + (int64_t)p * z_sp;
+          if (ri < K) vi = z[base + (int64_t)ri * z_sk];
+          if (!diag && rj < K) vj = z[base + (int64_t)rj * z_sk];
+          if (diag && ri < K) {  // cross term c_i += conj(x_b) z_bi on CUDA cores
+            const float2 xb = x[(int64_t)b * x_sb + (int64_t)p * x_sp];
+            cacc.x += xb.x * vi.x + xb.y * vi.y;
+            cacc.y += xb.x * vi.y - xb.y * vi.x;
+          }
         }
+        xh[s4] = to_tf32(vi.x);
+        xl[s4] = to_tf32(vi.x - __uint_as_float(xh[s4]));
+        yh[s4] = to_tf32(vi.y);
+        yl[s4] = to_tf32(vi.y - __uint_as_float(yh[s4]));
+        jxh[s4] = to_tf32(vj.x);
+        jxl[s4] = to_tf32(vj.x - __uint_as_float(jxh[s4]));
+        jyh[s4] = to_tf32(vj.y);
+        jyl[s4] = to_tf32(vj.y - __uint_as_float(jyh[s4]));
       }
-      const uint32_t xh = to_tf32(vi.x), yh = to_tf32(vi.y);
-      Tb[0 * TILE_WORDS + off] = xh;
-      Tb[1 * TILE_WORDS + off] = to_tf32(vi.x - __uint_as_float(xh));
-      Tb[2 * TILE_WORDS + off] = yh;
-      Tb[3 * TILE_WORDS + off] = to_tf32(vi.y - __uint_as_float(yh));
+      const uint32_t off = thalf * (TB * 4) + trow * 4;  // word offset of the k-unit inside a tile
+      auto st4 = [&](int tile, const uint32_t (&v)[4]) {
+        *reinterpret_cast<uint4*>(Tb + tile * TILE_WORDS + off) = make_uint4(v[0], v[1], v[2], v[3]);
+      };
+      st4(0, xh);
+      st4(1, xl);
+      st4(2, yh);
+      st4(3, yl);
       if (!diag) {
-        const uint32_t xjh = to_tf32(vj.x), yjh = to_tf32(vj.y);
-        Tb[4 * TILE_WORDS + off] = xjh;
-        Tb[5 * TILE_WORDS + off] = to_tf32(vj.x - __uint_as_float(xjh));
-        Tb[6 * TILE_WORDS + off] = yjh;
-        Tb[7 * TILE_WORDS + off] = to_tf32(vj.y - __uint_as_float(yjh));
+        st4(4, jxh);
+        st4(5, jxl);
+        st4(6, jyh);
+        st4(7, jyl);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy writes -> visible to the MMA
@@ -188,7 +201,8 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
 
   // ---- epilogue: TMEM -> shared memory -> coalesced row updates.  Warp w reads TMEM lanes
   // 32(w%4)..+31 (= rows), the real accumulator for w < 4, the imaginary one for w >= 4 ----
-  float* E = reinterpret_cast<float*>(smem);  // [TB][33] complex (interleaved re, im)
+  float* E = reinterpret_cast<float*>(smem);  // [2][TB][33]: the Re plane, then the Im plane (odd row
+                                              // stride: conflict-free column writes and row reads)
   const int64_t npk = (int64_t)K * (K + 1) / 2;
   const uint32_t lanebase = (uint32_t)((warp & 3) * 32) << 16;
   const int part = warp >> 2;  // 0: Re, 1: Im
@@ -198,7 +212,7 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
     tmem_ld32(tmem + lanebase + part * TB + c0, v);
     const int r = (warp & 3) * 32 + lane;
 #pragma unroll
-    for (int q = 0; q < 32; ++q) E[(r * 33 + q) * 2 + part] = __uint_as_float(v[q]);
+    for (int q = 0; q < 32; ++q) E[part * (TB * 33) + r * 33 + q] = __uint_as_float(v[q]);
     __syncthreads();
     const int col = J * TB + c0 + lane;
     // lanes = 32 consecutive columns of one row; each warp's 16 rows go in batches of 8 whose
@@ -219,8 +233,8 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
       for (int u = 0; u < 8; ++u) {
         const int rr = warp + 8 * (rb + u);
         if (ok[u]) {
-          const float2 v2 = reinterpret_cast<const float2*>(E)[rr * 33 + lane];
-          S[at[u]] = mkc<cx<Th>>(cur[u].x + (Th)v2.x, cur[u].y + (Th)v2.y);
+          const float vr = E[rr * 33 + lane], vi = E[TB * 33 + rr * 33 + lane];
+          S[at[u]] = mkc<cx<Th>>(cur[u].x + (Th)vr, cur[u].y + (Th)vi);
         }
       }
     }
