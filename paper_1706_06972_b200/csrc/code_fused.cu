@@ -115,16 +115,11 @@ struct Smem {
     const size_t sl = (G::NF + cs - 1) / cs;
     return al(sizeof(cx<T>) * sl) + al(sizeof(T) * sl);
   }
-  // D of the DC and Nyquist columns of the CTA's planes, [nk][2][N] (their column pair is one task)
-  static __host__ __device__ size_t q_bytes(int nk) { return al(sizeof(cx<T>) * (size_t)nk * 2 * N); }
   static __host__ __device__ size_t total(int nk, int cs) {
-    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes(cs) + n_bytes(cs) + s_bytes(cs) + q_bytes(nk) +
-           6 * 32 * sizeof(double);
+    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes(cs) + n_bytes(cs) + s_bytes(cs) + 6 * 32 * sizeof(double);
   }
-  // column tasks: Wh - 2 complex columns per plane plus one task for the (DC, Nyquist) pair of
-  // real columns; two lanes per task
   static __host__ __device__ int threads(int nk) {
-    const int wc = (nk * (G::Wh - 1) + 15) / 16, wr = (nk * N + 31) / 32;
+    const int wc = (nk * G::Wh + 15) / 16, wr = (nk * N + 31) / 32;
     return 32 * (wc > wr ? wc : wr);
   }
 };
@@ -255,7 +250,7 @@ __device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t mbar) 
 }
 
 template <typename T, int N>
-__global__ void __maxnreg__(sizeof(T) == 4 ? 128 : 96) k_code_fused(FusedArgs<T> a) {
+__global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T> a) {
   using C = cx<T>;
   using G = Geo<N>;
   using S = Smem<T, N>;
@@ -280,7 +275,6 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 128 : 96) k_code_fused(FusedArgs<T>
   const int slice_ = (NF + CS - 1) / CS;
   C* xsl = reinterpret_cast<C*>(smem + off);  off += S::al(sizeof(C) * slice_);
   T* dsl = reinterpret_cast<T*>(smem + off);  off += S::al(sizeof(T) * slice_);
-  C* dnq = reinterpret_cast<C*>(smem + off);  off += S::q_bytes(nkmax);
   double* scratch = reinterpret_cast<double*>(smem + off);
 
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -289,17 +283,11 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 128 : 96) k_code_fused(FusedArgs<T>
   const T cscl = (T)(1.0 / ((double)N * N));  // c = (1/P) FFT_M(z): z carries 2x (row_inverse_pre)
   const C* Dg = a.Wh + (int64_t)k0 * NF;
 
-  // column task of this lane: item (plane cj, column cv) shared by lanes l and l^16, index parity
-  // h.  Items [0, nk (Wh-2)) are the complex columns 1..Wh-2 of every plane; the last nk items are
-  // the planes' (DC, Nyquist) column pairs, both real sequences, transformed as one complex
-  // column (cv = 0 marks them; they sit at the end so only the last warp branches)
+  // column task of this lane: item (plane cj, column cv) shared by lanes l and l^16, index parity h
   const int citem = warp * 16 + (lane & 15);
   const int hpar = lane >> 4;
-  const int nreg = nk * (Wh - 2);
-  const bool cvalid = citem < nk * (Wh - 1);
-  const bool cpair = cvalid && citem >= nreg;
-  const int cj = !cvalid ? 0 : cpair ? citem - nreg : citem / (Wh - 2);
-  const int cv = !cvalid || cpair ? 0 : 1 + citem % (Wh - 2);
+  const bool cvalid = citem < nk * Wh;
+  const int cj = cvalid ? citem / Wh : 0, cv = cvalid ? citem % Wh : 0;
   C* colp = X + cj * PS + cv;
   const C* dcol = Dg + (int64_t)cj * NF + cv;
   // row task of this thread: plane rj, row rq
@@ -310,10 +298,6 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 128 : 96) k_code_fused(FusedArgs<T>
 
   for (int i = tid; i < nk * N * WP; i += nt) wS[i] = (T)0;
   for (int i = tid; i < nk * PS; i += nt) X[i] = mkc<C>(0, 0);
-  for (int i = tid; i < nk * 2 * N; i += nt) {  // D of the DC / Nyquist columns
-    const int j = i / (2 * N), e = i - j * 2 * N, q = e / N, u = e - q * N;
-    dnq[i] = Dg[(int64_t)j * NF + u * Wh + (q ? Wh - 1 : 0)];
-  }
   for (int i = tid; i < slice_; i += nt) {
     const int f = r * slice_ + i;
     xsl[i] = f < NF ? a.xh[(int64_t)b * NF + f] : mkc<C>(0, 0);
@@ -375,7 +359,6 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 128 : 96) k_code_fused(FusedArgs<T>
   // COL_F / COL_FE: forward column transform of the row-transformed planes times D (COL_FE also
   // emits the raw transform, F(U) for the history); COL_I: inverse column transform of conj(D) g
   // (double: z holds D on entry)
-  const C* dq0 = dnq + cj * 2 * N;  // D of this pair task's DC column (Nyquist at + N)
   auto col_phase = [&](auto mode_c, C* emit, ColRegs& zr) {
     constexpr int mode = decltype(mode_c)::value;
     C (&z)[M] = zr.v;
@@ -385,68 +368,28 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 128 : 96) k_code_fused(FusedArgs<T>
       constexpr int sh = (u0 < M) ? 1 : -1;       // row for h = 1 is u0 + sh*M
       const int ox = u0 * RS + sh * dpx;
       if constexpr (mode == COL_I) {
-        if (!cpair) {
-          const C g = gS[ox + cv];
-          const C d = DREG ? dreg.v[n2] : z[n2];
-          z[n2] = cmul2(d, mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
-        } else {  // conj(conj(D0) g0 + i conj(D21) g21) = D0 conj(g0) - i D21 conj(g21)
-          const int u = u0 + sh * (dpx ? M : 0);
-          const C g0 = gS[ox], g1 = gS[ox + Wh - 1];
-          z[n2] = sub_i(cmul2(dq0[u], mkc<C>(g0.x, -g0.y)), cmul2(dq0[N + u], mkc<C>(g1.x, -g1.y)));
-        }
+        const C g = gS[ox + cv];
+        const C d = DREG ? dreg.v[n2] : z[n2];
+        z[n2] = cmul2(d, mkc<C>(g.x, -g.y));  // conj(conj(D) g): inverse via forward FFT
       } else {
-        if (!cpair) {
-          z[n2] = colp[ox];
-        } else {  // the two real columns as one complex sequence
-          z[n2] = mkc<C>(X[cj * PS + ox].x, X[cj * PS + ox + Wh - 1].x);
-        }
+        z[n2] = colp[ox];
       }
     });
     sfft::fft<C, M, false>(z);
     sfft::static_for<0, M>([&](auto Kk) {
       constexpr int k2 = decltype(Kk)::value;
-      const C p = mkc<C>(__shfl_xor_sync(0xffffffffu, z[k2].x, 16), __shfl_xor_sync(0xffffffffu, z[k2].y, 16));
-      z[k2] = vfma(z[k2], vsplat<C>(sgn), p);  // h=0: z+p, h=1: p-z
-    });
-    if (!cvalid) return;
-    sfft::static_for<0, M>([&](auto Kk) {
-      constexpr int k2 = decltype(Kk)::value;
       constexpr int kA = ((M + 1) * k2) % N;      // output row for h = 0; h = 1 is kA + sh*M
       constexpr int sh = (kA < M) ? 1 : -1;
-      const int ox = kA * RS + sh * dpx;
-      const C o = z[k2];
-      if (!cpair) {
+      const C p = mkc<C>(__shfl_xor_sync(0xffffffffu, z[k2].x, 16), __shfl_xor_sync(0xffffffffu, z[k2].y, 16));
+      const C o = vfma(z[k2], vsplat<C>(sgn), p);  // h=0: z+p, h=1: p-z
+      if (cvalid) {
+        const int ox = kA * RS + sh * dpx;
         if constexpr (mode == COL_I) {
           colp[ox] = mkc<C>(o.x, -o.y);
         } else {
           if constexpr (mode == COL_FE) emit[(int64_t)cj * NF + kA * Wh + sh * dpd + cv] = o;
           if constexpr (DREG) colp[ox] = cmul2(dreg.v[kA / 2], o);  // kA is even (M + 1 is)
           else colp[ox] = o;
-        }
-      } else {
-        C* xr = X + cj * PS + ox;
-        if constexpr (mode == COL_I) {  // N IFFT(A + iB) = conj(o): real parts of the two columns
-          xr[0] = mkc<C>(o.x, (decltype(o.x))0);
-          xr[Wh - 1] = mkc<C>(-o.y, (decltype(o.x))0);
-        } else {
-          // split the spectra of the two real columns: row -k of this lane's row k is output
-          // (M - k2) % M of the same lane
-          const C op = z[(M - k2) % M];
-          const C f0 = vmul(vfma(op, mkc<C>(1, -1), o), vsplat<C>((decltype(o.x))0.5));       // (Z_k + conj Z_-k)/2
-          const C dd = vfma(op, mkc<C>(-1, 1), o);                                         // Z_k - conj Z_-k
-          const C f1 = vmul(vswap(dd), mkc<C>((decltype(o.x))0.5, (decltype(o.x))-0.5));  // dd / (2i)
-          const int u = kA + sh * (dpx ? M : 0);
-          if constexpr (mode == COL_FE) {
-            emit[(int64_t)cj * NF + u * Wh] = f0;
-            emit[(int64_t)cj * NF + u * Wh + Wh - 1] = f1;
-          }
-          if constexpr (DREG) {
-            xr[0] = cmul2(dq0[u], f0);
-            xr[Wh - 1] = cmul2(dq0[N + u], f1);
-          } else {
-            xr[0] = f0;
-            xr[Wh - 1] = f1;
-          }
         }
       }
     });
