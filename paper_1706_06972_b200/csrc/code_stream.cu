@@ -163,18 +163,18 @@ __device__ __forceinline__ void row_stage2_oop(const C* src, C* dst, int nr, int
 // bins {2 n2, 2 n2 + RB} and task RB - n2 their partners, so one thread runs both tasks with the
 // pre-processing fused in; every stage-2 task holds both bins of each pair in registers, so the
 // post-processing is fused into its stores.
+// (2-wide forms: s = x1 + conj(x2), d = x1 - conj(x2) are one FFMA2 each, the products with the
+// twiddle t two more; same arithmetic as the scalar textbook split)
 template <typename C>
-__device__ __forceinline__ C herm_pre(C x1, C x2, C t) {  // Z[k] from X[k], X[NR-k]
-  const C s = mkc<C>(x1.x + x2.x, x1.y - x2.y), d = mkc<C>(x1.x - x2.x, x1.y + x2.y);
-  const C r = mkc<C>(d.x * t.x + d.y * t.y, d.y * t.x - d.x * t.y);
-  return mkc<C>(s.x - r.y, s.y + r.x);
+__device__ __forceinline__ C herm_pre(C x1, C x2, C t) {  // Z[k] from X[k], X[NR-k]: s + i conj(t) d
+  const C s = vfma(x2, mkc<C>(1, -1), x1), d = vfma(x2, mkc<C>(-1, 1), x1);
+  return add_i(s, cmulc2(t, d));
 }
 template <typename C>
-__device__ __forceinline__ C herm_post(C z1, C z2, C t) {  // X[k] from Z[k], Z[NR-k]
+__device__ __forceinline__ C herm_post(C z1, C z2, C t) {  // X[k] from Z[k], Z[NR-k]: (s - i t d) / 2
   using T = decltype(C::x);
-  const C s = mkc<C>((z1.x + z2.x) * (T)0.5, (z1.y - z2.y) * (T)0.5);
-  const C q = mkc<C>((z1.y + z2.y) * (T)0.5, -(z1.x - z2.x) * (T)0.5);
-  return mkc<C>(s.x + q.x * t.x - q.y * t.y, s.y + q.x * t.y + q.y * t.x);
+  const C s = vfma(z2, mkc<C>(1, -1), z1), d = vfma(z2, mkc<C>(-1, 1), z1);
+  return vmul(sub_i(s, cmul2(t, d)), vsplat<C>((T)0.5));
 }
 
 // Hermitian pre-processing + inverse row stage 1, in place on rows of S; ends synced
@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   C* SB = SA + H * PR;                  // [H][PR] second plane: stage-2 passes run out of place
   C* WB = SB + H * PR;                  // [H][NR] state plane (pairs)
   C* PT = WB + H * NR;                  // [NF] the group's synthesis partial
+  C* DK = PT + NF;                      // [NF] D_k of the next plane's inverse input (cp.async prefetch)
   __shared__ double scratch[4 * 32];
   __shared__ C tws[NR + 1];  // e^{-2 pi i k / W}, k <= NR
   const int b = blockIdx.y, grp = blockIdx.x;
@@ -594,24 +595,32 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   bool nonfinite = false;
   const C ip2 = mkc<C>(a.invP, a.invP);
   long long* prof = (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ? g_plane_prof : nullptr;
+  // D of a plane: prefetched into DK for the inverse input (a) while the previous plane runs;
+  // cp.async groups in commit order: D(k), W(k) (state), D(k+1), W(k+1), ...
+  auto prefetch_d = [&](int k) {
+    const C* src = a.Wh + (int64_t)k * NF;
+    for (int e = 2 * tid; e < NF; e += 2 * NT) cp_async<16>(DK + e, src + e);  // NF even, 16-byte aligned
+    cp_async_commit();
+  };
+  static_assert(sizeof(C) == 8 && NF % 2 == 0, "k_plane is the float path");
+  prefetch_d(k0);
   for (int k = k0; k < k1; ++k) {
     PLANE_STAMP(0)
     C* wpl = reinterpret_cast<C*>(a.w + ((int64_t)b * a.K + k) * H * W);  // H x NR pairs
     const C* dk = a.Wh + (int64_t)k * NF;
-    if (!a.first) {
-      if constexpr (sizeof(C) == 8) {  // 16-byte copies (two complex; H * NR is even)
-        for (int e = 2 * tid; e < H * NR; e += 2 * NT) cp_async<16>(WB + e, wpl + e);
-      } else {
-        for (int e = tid; e < H * NR; e += NT) cp_async<sizeof(C)>(WB + e, wpl + e);
-      }
-      cp_async_commit();
+    if (!a.first) {  // 16-byte copies (two complex; H * NR is even)
+      for (int e = 2 * tid; e < H * NR; e += 2 * NT) cp_async<16>(WB + e, wpl + e);
     }
+    cp_async_commit();  // (an empty group on the cold start keeps the group count)
+    cp_async_wait<1>();  // D(k) has landed (only the state copy may still be in flight)
+    __syncthreads();
     // (a) inverse input conj(D_k) g
     for (int f = tid; f < NF; f += NT) {
       const int u = f / WH, v = f - u * WH;
-      SA[u * PR + v] = cmulc(dk[f], gb[f]);
+      SA[u * PR + v] = cmulc2(DK[f], gb[f]);
     }
     __syncthreads();
+    if (k + 1 < k1) prefetch_d(k + 1);  // DK is free until the next plane's (a)
     PLANE_STAMP(1)
     // (b) column IFFT (length H along u, WH columns)
     for (int e = tid; e < G::CB * WH; e += NT) {
@@ -639,7 +648,8 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
     PLANE_STAMP(6)
     // (e) update w (pairs), norms, t' packed
     if (!a.first) {
-      cp_async_wait<0>();
+      if (k + 1 < k1) cp_async_wait<1>();  // the state copy (the next D prefetch may stay in flight)
+      else cp_async_wait<0>();
       __syncthreads();
     }
     PLANE_STAMP(7)
@@ -696,7 +706,7 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
 #pragma unroll 4
     for (int f = tid; f < NF; f += NT) {
       const int u = f / WH, v = f - u * WH;
-      cfma(PT[f], dk[f], SA[u * PR + v]);
+      PT[f] = vfma_c(dk[f], SA[u * PR + v], PT[f]);
     }
     __syncthreads();  // SA / WB are rewritten by the next plane
     PLANE_STAMP(14)
@@ -836,7 +846,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   }
   PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
                      (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
-  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + NF) * sizeof(cx<T>);
+  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + 2 * NF) * sizeof(cx<T>);
   if constexpr (G::PLANE)
     OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
   int rc = OCSC_OK, chunk = 0;
