@@ -82,6 +82,21 @@ struct Flags {
   const int32_t* all_done;
 };
 
+// e = tid, tid + step, ... over rows of length L: (row, column) kept incrementally instead of a
+// division per element (step < 2 L for every launch shape here)
+template <int L>
+struct RowWalk {
+  int i, k;
+  __device__ __forceinline__ RowWalk(int e0) : i(e0 / L), k(e0 - (e0 / L) * L) {}
+  __device__ __forceinline__ void advance(int step) {
+    k += step;
+    while (k >= L) {
+      k -= L;
+      ++i;
+    }
+  }
+};
+
 // ---------------------------------------------------------------- line FFTs --
 // Good-Thomas line transform of length N = A * B on a shared-memory line (stride 1):
 // stage 1 (tasks n2 < B): A-point DFTs on positions (B n1 + A n2) mod N, in place;
@@ -289,22 +304,18 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   }
   __syncthreads();
   // 2. Hermitian pre-processing (pairs k, NR-k): Z = (X_k + X*_{NR-k}) + i e^{+i 2pi k/W}(X_k - X*_{NR-k})
-  for (int e = tid; e < nr * (NR / 2 + 1); e += G::NTR) {
-    const int i = e / (NR / 2 + 1), k = e - i * (NR / 2 + 1);
-    const int k2 = NR - k;
-    C* row = SA + i * PR;
-    const C x1 = row[k], x2 = row[k2];
-    const C t1 = a.tw[k], t2 = a.tw[k2];  // forward twiddles; inverse uses the conjugate
-    // Z[k]
-    const C s1 = mkc<C>(x1.x + x2.x, x1.y - x2.y), d1 = mkc<C>(x1.x - x2.x, x1.y + x2.y);
-    const C r1 = mkc<C>(d1.x * t1.x + d1.y * t1.y, d1.y * t1.x - d1.x * t1.y);  // d1 * conj(t1)
-    const C z1 = mkc<C>(s1.x - r1.y, s1.y + r1.x);
-    // Z[NR-k] (k2 in (0, NR]; for k = 0 it would be Z[NR] which does not exist)
-    const C s2 = mkc<C>(x2.x + x1.x, x2.y - x1.y), d2 = mkc<C>(x2.x - x1.x, x2.y + x1.y);
-    const C r2 = mkc<C>(d2.x * t2.x + d2.y * t2.y, d2.y * t2.x - d2.x * t2.y);
-    const C z2 = mkc<C>(s2.x - r2.y, s2.y + r2.x);
-    row[k] = z1;
-    if (k != 0 && k2 != k) row[k2] = z2;
+  {
+    constexpr int NP = NR / 2 + 1;
+    RowWalk<NP> rw(tid);
+    for (int e = tid; e < nr * NP; e += G::NTR, rw.advance(G::NTR)) {
+      const int i = rw.i, k = rw.k, k2 = NR - k;
+      C* row = SA + i * PR;
+      const C x1 = row[k], x2 = row[k2];
+      const C z1 = herm_pre(x1, x2, a.tw[k]);   // (forward twiddles; the inverse uses the conjugate)
+      const C z2 = herm_pre(x2, x1, a.tw[k2]);  // Z[NR-k] (k2 in (0, NR]; for k = 0 there is no Z[NR])
+      row[k] = z1;
+      if (k != 0 && k2 != k) row[k2] = z2;
+    }
   }
   __syncthreads();
   // 3. inverse FFT_NR in place: stage 1, then stage 2 through registers (one round of tasks)
@@ -323,8 +334,9 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
     __syncthreads();
   }
   const C ip2 = mkc<C>(a.invP, a.invP);
-  for (int e = tid; e < nr * NR; e += G::NTR) {
-    const int i = e / NR, n = e - i * NR;
+  RowWalk<NR> uw(tid);
+  for (int e = tid; e < nr * NR; e += G::NTR, uw.advance(G::NTR)) {
+    const int i = uw.i, n = uw.k;
     const C z = SA[i * PR + n];
     C* wp = reinterpret_cast<C*>(w + (int64_t)i * W) + n;
     const C wo = a.first ? mkc<C>(0, 0) : WB[e];
@@ -358,15 +370,12 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   __syncthreads();
   row_stage2<C, G, false>(SA, nr, tid);
   // 6. post-processing X_k = (Z_k + Z*_{NR-k})/2 + e^{-i 2pi k/W} (Z_k - Z*_{NR-k})/(2i), k = 0..NR
-  for (int e = tid; e < nr * WH; e += G::NTR) {
-    const int i = e / WH, k = e - i * WH;
+  RowWalk<WH> pw(tid);
+  for (int e = tid; e < nr * WH; e += G::NTR, pw.advance(G::NTR)) {
+    const int i = pw.i, k = pw.k;
     const C* row = SA + i * PR;
     const C z1 = row[k == NR ? 0 : k], z2 = row[k == 0 ? 0 : NR - k];
-    const C s1 = mkc<C>((z1.x + z2.x) * (T)0.5, (z1.y - z2.y) * (T)0.5);
-    const C d1 = mkc<C>((z1.x - z2.x) * (T)0.5, (z1.y + z2.y) * (T)0.5);  // (Z - Z*)/2
-    const C q = mkc<C>(d1.y, -d1.x);                                          // / i
-    const C t = a.tw[k];
-    spec[(int64_t)i * WH + k] = mkc<C>(s1.x + q.x * t.x - q.y * t.y, s1.y + q.x * t.y + q.y * t.x);
+    spec[(int64_t)i * WH + k] = herm_post(z1, z2, a.tw[k]);
   }
 }
 
@@ -581,7 +590,6 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   C* SB = SA + H * PR;                  // [H][PR] second plane: stage-2 passes run out of place
   C* WB = SB + H * PR;                  // [H][NR] state plane (pairs)
   C* PT = WB + H * NR;                  // [NF] the group's synthesis partial
-  C* DK = PT + NF;                      // [NF] D_k of the next plane's inverse input (cp.async prefetch)
   __shared__ double scratch[4 * 32];
   __shared__ C tws[NR + 1];  // e^{-2 pi i k / W}, k <= NR
   const int b = blockIdx.y, grp = blockIdx.x;
@@ -595,32 +603,22 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   bool nonfinite = false;
   const C ip2 = mkc<C>(a.invP, a.invP);
   long long* prof = (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ? g_plane_prof : nullptr;
-  // D of a plane: prefetched into DK for the inverse input (a) while the previous plane runs;
-  // cp.async groups in commit order: D(k), W(k) (state), D(k+1), W(k+1), ...
-  auto prefetch_d = [&](int k) {
-    const C* src = a.Wh + (int64_t)k * NF;
-    for (int e = 2 * tid; e < NF; e += 2 * NT) cp_async<16>(DK + e, src + e);  // NF even, 16-byte aligned
-    cp_async_commit();
-  };
-  static_assert(sizeof(C) == 8 && NF % 2 == 0, "k_plane is the float path");
-  prefetch_d(k0);
+  static_assert(sizeof(C) == 8, "k_plane is the float path");
   for (int k = k0; k < k1; ++k) {
     PLANE_STAMP(0)
     C* wpl = reinterpret_cast<C*>(a.w + ((int64_t)b * a.K + k) * H * W);  // H x NR pairs
     const C* dk = a.Wh + (int64_t)k * NF;
     if (!a.first) {  // 16-byte copies (two complex; H * NR is even)
       for (int e = 2 * tid; e < H * NR; e += 2 * NT) cp_async<16>(WB + e, wpl + e);
+      cp_async_commit();
     }
-    cp_async_commit();  // (an empty group on the cold start keeps the group count)
-    cp_async_wait<1>();  // D(k) has landed (only the state copy may still be in flight)
-    __syncthreads();
-    // (a) inverse input conj(D_k) g
+    // (a) inverse input conj(D_k) g (a shared-memory copy of D_k prefetched during the previous
+    // plane measured slower: the g loads stay exposed and the extra group waits cost more)
     for (int f = tid; f < NF; f += NT) {
       const int u = f / WH, v = f - u * WH;
-      SA[u * PR + v] = cmulc2(DK[f], gb[f]);
+      SA[u * PR + v] = cmulc2(dk[f], gb[f]);
     }
     __syncthreads();
-    if (k + 1 < k1) prefetch_d(k + 1);  // DK is free until the next plane's (a)
     PLANE_STAMP(1)
     // (b) column IFFT (length H along u, WH columns)
     for (int e = tid; e < G::CB * WH; e += NT) {
@@ -648,8 +646,7 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
     PLANE_STAMP(6)
     // (e) update w (pairs), norms, t' packed
     if (!a.first) {
-      if (k + 1 < k1) cp_async_wait<1>();  // the state copy (the next D prefetch may stay in flight)
-      else cp_async_wait<0>();
+      cp_async_wait<0>();
       __syncthreads();
     }
     PLANE_STAMP(7)
@@ -846,7 +843,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   }
   PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
                      (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
-  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + 2 * NF) * sizeof(cx<T>);
+  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + NF) * sizeof(cx<T>);
   if constexpr (G::PLANE)
     OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
   int rc = OCSC_OK, chunk = 0;
