@@ -82,17 +82,19 @@ struct Flags {
   const int32_t* all_done;
 };
 
-// e = tid, tid + step, ... over rows of length L: (row, column) kept incrementally instead of a
-// division per element (step < 2 L for every launch shape here)
-template <int L>
+// e = tid, tid + STEP, ... over rows of length L: (row, column) kept incrementally instead of a
+// division per element; branch-free (ceil(STEP / L) conditional subtractions)
+template <int L, int STEP>
 struct RowWalk {
   int i, k;
   __device__ __forceinline__ RowWalk(int e0) : i(e0 / L), k(e0 - (e0 / L) * L) {}
-  __device__ __forceinline__ void advance(int step) {
-    k += step;
-    while (k >= L) {
-      k -= L;
-      ++i;
+  __device__ __forceinline__ void advance() {
+    k += STEP;
+#pragma unroll
+    for (int r = 0; r < (STEP + L - 1) / L; ++r) {
+      const int q = k >= L;
+      k -= q * L;
+      i += q;
     }
   }
 };
@@ -263,8 +265,10 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   C* SA = reinterpret_cast<C*>(smraw);
   __shared__ double scratch[4 * 32];
+  __shared__ C tws[WH];  // e^{-2 pi i k / W}, k <= NR
   const int b = blockIdx.y;
   if (*a.fl.all_done || a.fl.done[b]) return;
+  for (int k = threadIdx.x; k < WH; k += G::NTR) tws[k] = a.tw[k];
   const int64_t rows = (int64_t)a.K * H;
   const int64_t r0 = (int64_t)blockIdx.x * R;
   const int nr = (int)(rows - r0 < R ? rows - r0 : R);
@@ -306,13 +310,13 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   // 2. Hermitian pre-processing (pairs k, NR-k): Z = (X_k + X*_{NR-k}) + i e^{+i 2pi k/W}(X_k - X*_{NR-k})
   {
     constexpr int NP = NR / 2 + 1;
-    RowWalk<NP> rw(tid);
-    for (int e = tid; e < nr * NP; e += G::NTR, rw.advance(G::NTR)) {
+    RowWalk<NP, G::NTR> rw(tid);
+    for (int e = tid; e < nr * NP; e += G::NTR, rw.advance()) {
       const int i = rw.i, k = rw.k, k2 = NR - k;
       C* row = SA + i * PR;
       const C x1 = row[k], x2 = row[k2];
-      const C z1 = herm_pre(x1, x2, a.tw[k]);   // (forward twiddles; the inverse uses the conjugate)
-      const C z2 = herm_pre(x2, x1, a.tw[k2]);  // Z[NR-k] (k2 in (0, NR]; for k = 0 there is no Z[NR])
+      const C z1 = herm_pre(x1, x2, tws[k]);   // (forward twiddles; the inverse uses the conjugate)
+      const C z2 = herm_pre(x2, x1, tws[k2]);  // Z[NR-k] (k2 in (0, NR]; for k = 0 there is no Z[NR])
       row[k] = z1;
       if (k != 0 && k2 != k) row[k2] = z2;
     }
@@ -334,11 +338,11 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
     __syncthreads();
   }
   const C ip2 = mkc<C>(a.invP, a.invP);
-  RowWalk<NR> uw(tid);
-  for (int e = tid; e < nr * NR; e += G::NTR, uw.advance(G::NTR)) {
+  RowWalk<NR, G::NTR> uw(tid);
+  for (int e = tid; e < nr * NR; e += G::NTR, uw.advance()) {
     const int i = uw.i, n = uw.k;
     const C z = SA[i * PR + n];
-    C* wp = reinterpret_cast<C*>(w + (int64_t)i * W) + n;
+    C* wp = reinterpret_cast<C*>(w) + e;  // state rows are contiguous pairs (W = 2 NR)
     const C wo = a.first ? mkc<C>(0, 0) : WB[e];
     const C go = mkc<C>(clip(wo.x, a.kappa), clip(wo.y, a.kappa));
     const C uo = vsub(wo, go);
@@ -370,12 +374,13 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   __syncthreads();
   row_stage2<C, G, false>(SA, nr, tid);
   // 6. post-processing X_k = (Z_k + Z*_{NR-k})/2 + e^{-i 2pi k/W} (Z_k - Z*_{NR-k})/(2i), k = 0..NR
-  RowWalk<WH> pw(tid);
-  for (int e = tid; e < nr * WH; e += G::NTR, pw.advance(G::NTR)) {
+  RowWalk<WH, G::NTR> pw(tid);
+  C* sp = spec + tid;
+  for (int e = tid; e < nr * WH; e += G::NTR, pw.advance(), sp += G::NTR) {  // (spec rows are contiguous)
     const int i = pw.i, k = pw.k;
     const C* row = SA + i * PR;
     const C z1 = row[k == NR ? 0 : k], z2 = row[k == 0 ? 0 : NR - k];
-    spec[(int64_t)i * WH + k] = herm_post(z1, z2, a.tw[k]);
+    *sp = herm_post(z1, z2, tws[k]);
   }
 }
 
