@@ -105,20 +105,18 @@ struct Smem {
   static __host__ __device__ size_t w_bytes(int nk) { return al(sizeof(T) * (size_t)nk * N * G::WP); }
   static __host__ __device__ size_t x_bytes(int nk) { return al(sizeof(cx<T>) * (size_t)nk * G::PS); }
   static __host__ __device__ size_t g_bytes() { return al(sizeof(cx<T>) * (size_t)N * G::RS); }
-  // frequencies per owner CTA, even so a slice of complex floats is a multiple of 16 bytes
-  static __host__ __device__ int slice(int cs) { return (((G::NF + cs - 1) / cs) + 1) & ~1; }
-  static __host__ __device__ size_t p_bytes(int cs) { return al(sizeof(cx<T>) * (size_t)cs * slice(cs)); }
+  static __host__ __device__ size_t p_bytes(int cs) {
+    return al(sizeof(cx<T>) * (size_t)cs * ((G::NF + cs - 1) / cs));
+  }
   // per-warp norm partials from every CTA of the cluster: [CS][32 warps][8] (arithmetic type)
   static __host__ __device__ size_t n_bytes(int cs) { return al(sizeof(T) * 2 * 8 * 32 * (size_t)cs); }
   // this CTA's slice of the sample spectrum and of den
   static __host__ __device__ size_t s_bytes(int cs) {
-    const size_t sl = slice(cs);
+    const size_t sl = (G::NF + cs - 1) / cs;
     return al(sizeof(cx<T>) * sl) + al(sizeof(T) * sl);
   }
-  // part (received partials) + pstage (this CTA's partials, staged for the bulk copies)
   static __host__ __device__ size_t total(int nk, int cs) {
-    return w_bytes(nk) + x_bytes(nk) + g_bytes() + 2 * p_bytes(cs) + n_bytes(cs) + s_bytes(cs) +
-           6 * 32 * sizeof(double);
+    return w_bytes(nk) + x_bytes(nk) + g_bytes() + p_bytes(cs) + n_bytes(cs) + s_bytes(cs) + 6 * 32 * sizeof(double);
   }
   static __host__ __device__ int threads(int nk) {
     const int wc = (nk * G::Wh + 15) / 16, wr = (nk * N + 31) / 32;
@@ -273,9 +271,8 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T>
   C* X = reinterpret_cast<C*>(smem + off);    off += S::x_bytes(nkmax);
   C* gS = reinterpret_cast<C*>(smem + off);   off += S::g_bytes();
   C* part = reinterpret_cast<C*>(smem + off); off += S::p_bytes(CS);
-  C* pstage = reinterpret_cast<C*>(smem + off); off += S::p_bytes(CS);
   T* nrm = reinterpret_cast<T*>(smem + off); off += S::n_bytes(CS);
-  const int slice_ = S::slice(CS);
+  const int slice_ = (NF + CS - 1) / CS;
   C* xsl = reinterpret_cast<C*>(smem + off);  off += S::al(sizeof(C) * slice_);
   T* dsl = reinterpret_cast<T*>(smem + off);  off += S::al(sizeof(T) * slice_);
   double* scratch = reinterpret_cast<double*>(smem + off);
@@ -307,7 +304,7 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T>
     dsl[i] = f < NF ? (T)1 / a.den[f] : (T)0;
   }
   const int nwarps = nt >> 5;
-  const int slice = S::slice(CS);
+  const int slice = (NF + CS - 1) / CS;
   // exchange state: mb_part completes when every CTA's partial synthesis for this CTA's slice
   // (and, from the second iteration on, every warp's stopping norms) has landed; mb_g when the
   // g slices of every owner have landed.  Cluster addresses of every CTA's buffers, per rank.
@@ -321,8 +318,8 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T>
     t_mbp[tid] = mapa_u32(smem_u32(&mb_part), tid);
     t_nrm[tid] = mapa_u32(smem_u32(nrm), tid);
   }
-  // every CTA sends its whole (padded) slice of partials for this owner in one bulk copy
-  const uint32_t part_bytes = (uint32_t)(CS * slice * sizeof(C));
+  const int my_slice = min(NF, (r + 1) * slice) - r * slice;
+  const uint32_t part_bytes = (uint32_t)(CS * my_slice * sizeof(C));
   const uint32_t nrm_bytes = (uint32_t)(CS * nwarps * 5 * sizeof(T));
   if (tid == 0) {
     mbar_init(&mb_part, 1);
@@ -402,22 +399,27 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T>
   // thread -> frequencies f = tid + i nt (consecutive across lanes: coalesced D loads); the
   // workspace offset and the owner's receive slot are computed once
   constexpr int RP = 3;  // frequencies per thread: NF <= RP * threads for every launch shape
-  int ro[RP];
+  int ro[RP], rown[RP];
+  uint32_t rdst[RP];
   const C* rdg[RP];
 #pragma unroll
   for (int i = 0; i < RP; ++i) {
     const int f = tid + i * nt;
     ro[i] = -1;
+    rdst[i] = 0;
+    rown[i] = 0;
     rdg[i] = Dg;
     if (f < NF) {
-      const int u = f / Wh, v = f - u * Wh;
+      const int u = f / Wh, v = f - u * Wh, owner = f / slice;
       ro[i] = u * RS + v;
+      rown[i] = owner;
+      rdst[i] = t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C));
       rdg[i] = Dg + f;
     }
   }
   // partial synthesis sum_k D_k F(t_k) over own filters, pushed into the owner CTA's slot;
   // the nk (D, X) loads of a frequency are independent, so they issue back to back
-  auto push_item = [&](int o, const C* dg, C* dst) {
+  auto push_item = [&](int o, const C* dg, uint32_t dst, int owner) {
     C s = mkc<C>(0, 0), s2 = mkc<C>(0, 0);
     int j = 0;
     if constexpr (DREG) {  // X already holds D F(t): a plain sum over the CTA's planes
@@ -433,31 +435,18 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T>
       }
       if (j < nk) s = vfma_c(dg[(int64_t)j * NF], X[j * PS + o], s);
     }
-    *dst = vadd(s, s2);
+    st_async(dst, vadd(s, s2), t_mbp[owner]);
   };
   // (the D loads of a frequency's planes are L2-bandwidth bound: ~100 KB per CTA per
   // iteration; issuing all of a thread's loads at once measured slower, profiles/README.md)
-  // the sums land in pstage (frequency order = owner slices back to back); then one bulk DSMEM
-  // copy per owner (cp.async.bulk ... mbarrier::complete_tx) moves a whole slice -- CS copies
-  // instead of one st.async per frequency.  pstage is rewritten only after every owner has sent
-  // g, i.e. after every copy out of it has landed.
   auto reduce_push = [&]() {
 #pragma unroll
     for (int i = 0; i < RP; ++i)
-      if (ro[i] >= 0) push_item(ro[i], rdg[i], pstage + tid + i * nt);
+      if (ro[i] >= 0) push_item(ro[i], rdg[i], rdst[i], rown[i]);
     for (int f = tid + RP * nt; f < NF; f += nt) {  // small launch shapes only
-      const int u = f / Wh, v = f - u * Wh;
-      push_item(u * RS + v, Dg + f, pstage + f);
-    }
-    __syncthreads();
-    if (tid < CS) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk copy
-      const uint32_t src = smem_u32(pstage + tid * slice);
-      const uint32_t dst = t_part[tid] + (uint32_t)(r * slice * sizeof(C));
-      asm volatile(
-          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-          "r"(src), "r"((uint32_t)(slice * sizeof(C))), "r"(t_mbp[tid])
-          : "memory");
+      const int u = f / Wh, v = f - u * Wh, owner = f / slice;
+      push_item(u * RS + v, Dg + f, t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C)),
+                owner);
     }
   };
   // y[f] for my slice from the CS received partials (local loads only)
