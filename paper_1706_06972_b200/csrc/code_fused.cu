@@ -249,8 +249,11 @@ __device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t mbar) 
                : "memory");
 }
 
-template <typename T, int N>
-__global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T> a) {
+// DREG_: keep the lane's D column in registers for the whole solve (float only, 120 registers,
+// at most 16 warps = 11 filters per CTA); otherwise reload D from L2 each iteration (96 registers,
+// up to 17 warps = 12 filters per CTA, or 18 warps with 13)
+template <typename T, int N, bool DREG_>
+__global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
   using C = cx<T>;
   using G = Geo<N>;
   using S = Smem<T, N>;
@@ -345,7 +348,8 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T>
   // COL_I inputs (row 2n (+-M), n = 0..M-1) and as COL_F outputs (row (M+1) k2 mod N = 2n (+-M)),
   // so one array of M values covers both passes.  float: loaded once for the whole solve and kept
   // in registers (no per-iteration D traffic); double: reloaded from L2 before each COL_I pass.
-  constexpr bool DREG = sizeof(T) == 4;
+  constexpr bool DREG = DREG_;
+  static_assert(!DREG || sizeof(T) == 4, "register-resident D is the float path");
   auto load_dcol = [&](ColRegs& dz) {
     sfft::static_for<0, M>([&](auto Nn) {
       constexpr int n2 = decltype(Nn)::value;
@@ -667,8 +671,15 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? 120 : 96) k_code_fused(FusedArgs<T>
 // ---------------------------------------------------------------- dispatch --
 struct FusedShape {
   int cs = 0, threads = 0, nk = 0, active = 0;
+  bool dreg = false;
   size_t smem = 0;
 };
+// the kernel instantiation of a shape's variant (double has only the L2-D variant)
+template <typename T, int N>
+static auto kernel_of(bool dreg) -> void (*)(FusedArgs<T>) {
+  if constexpr (sizeof(T) == 4) return dreg ? k_code_fused<T, N, true> : k_code_fused<T, N, false>;
+  else return k_code_fused<T, N, false>;
+}
 struct FusedPlan {
   FusedShape main, tail;  // main shape for the first b_main samples, tail shape for the rest
   int b_main = 0;
@@ -676,7 +687,7 @@ struct FusedPlan {
 
 template <typename T, int N>
 static int max_active_clusters(const FusedShape& sh, int B) {
-  auto kern = k_code_fused<T, N>;
+  auto kern = kernel_of<T, N>(sh.dreg);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
   if (sh.cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
@@ -709,30 +720,38 @@ static FusedPlan plan_for(int K, int B) {
   int dev = 0, max_smem = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return plan;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, k_code_fused<T, N>) != cudaSuccess) return plan;
-  FusedShape shapes[16];
+  FusedShape shapes[32];
   int ns = 0;
   const char* force = getenv("OCSC_FUSED_CS");  // dev knob: a single cluster size, no tail
   const int fcs = force ? atoi(force) : 0;
-  for (int cs = 2; cs <= 16; ++cs) {
-    if (cs > K) break;
-    if (fcs && cs != fcs) continue;
-    FusedShape sh;
-    sh.cs = cs;
-    sh.nk = (K + cs - 1) / cs;
-    sh.smem = Smem<T, N>::total(sh.nk, cs);
-    sh.threads = Smem<T, N>::threads(sh.nk);
-    if (sh.smem > (size_t)max_smem || sh.threads > fa.maxThreadsPerBlock) continue;
-    sh.active = max_active_clusters<T, N>(sh, B);
-    if (sh.active > 0) shapes[ns++] = sh;
+  const char* fdr = getenv("OCSC_FUSED_DREG");  // dev knob: 0 / 1 forces the D variant
+  for (int v = 0; v < (sizeof(T) == 4 ? 2 : 1); ++v) {
+    const bool dreg = sizeof(T) == 4 && v == 0;
+    if (fdr && atoi(fdr) != (int)dreg) continue;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, kernel_of<T, N>(dreg)) != cudaSuccess) continue;
+    for (int cs = 2; cs <= 16; ++cs) {
+      if (cs > K) break;
+      if (fcs && cs != fcs) continue;
+      FusedShape sh;
+      sh.cs = cs;
+      sh.dreg = dreg;
+      sh.nk = (K + cs - 1) / cs;
+      sh.smem = Smem<T, N>::total(sh.nk, cs);
+      sh.threads = Smem<T, N>::threads(sh.nk);
+      if (sh.smem > (size_t)max_smem || sh.threads > fa.maxThreadsPerBlock) continue;
+      sh.active = max_active_clusters<T, N>(sh, B);
+      if (sh.active > 0) shapes[ns++] = sh;
+    }
   }
   if (!ns) return plan;
   // makespan model: a wave of a shape costs (nk + 3.5) units (filters per CTA plus a fixed
   // per-iteration cluster overhead; fitted to scripts/cluster_sweep.py on a B200).  Take the
   // main shape and optional tail shape with the smallest total: full waves of the main shape,
   // then the remainder either as one more main wave or on the tail shape's waves.
-  auto cost = [](const FusedShape& sh) { return (double)sh.nk + 3.5; };
+  // (register-resident D: 17.8 k cycles per iteration at 10 filters per CTA against 23.9 k at 12
+  // filters with D reloaded from L2, profiles/r2_phase_*.log)
+  auto cost = [](const FusedShape& sh) { return ((double)sh.nk + 3.5) * (sh.dreg ? 0.856 : 1.0); };
   double best_t = 1e300;
   for (int m = 0; m < ns; ++m) {
     const FusedShape& M = shapes[m];
@@ -777,7 +796,7 @@ static const FusedPlan& cached_plan(int K, int B) {
 template <typename T, int N>
 static int launch_shape(FusedArgs<T> a, const FusedShape& sh, int b0, int nb, cudaStream_t s) {
   if (nb <= 0) return OCSC_OK;
-  auto kern = k_code_fused<T, N>;
+  auto kern = kernel_of<T, N>(sh.dreg);
   OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem));
   if (sh.cs > 8) OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   a.b0 = b0;
@@ -812,7 +831,7 @@ static int query_fused(int K, int B, int* info) {
   const FusedPlan& p = cached_plan<T, N>(K, B);
   if (info) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_code_fused<T, N>);
+    cudaFuncGetAttributes(&fa, kernel_of<T, N>(p.main.dreg));
     info[0] = p.main.cs;
     info[1] = p.main.threads;
     info[2] = (int)p.main.smem;
