@@ -21,7 +21,7 @@ B = an + bn
 X = synth_images(B, (32, 32), (42, 42), 20, seed=1).reshape(B, -1)
 tr = ob.OnlineTrainer(ob.SignalShape((42, 42), (11, 11)), ob.TrainConfig(n_filters=100, dtype="float32",
                       batch_size=B, stop_tol=0.0))
-tr.partial_fit(X)
+tr._buffers(B, False)  # (no partial_fit: every launch plan below is pinned fresh)
 xs = torch.as_tensor(X.reshape(B, 42, 42), dtype=torch.float32).cuda()
 xh = rfft2_dev(xs, tr.shape)
 buf = tr._buf
@@ -44,13 +44,14 @@ sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
 
 
 def go(which):
+    """which: "A", "B", "AB" (A enqueued first) or "BA" (B enqueued first)."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
     done = []
-    for b0, n, st in ((0, an, sa), (an, bn, sb)):
-        if (which == "A" and b0) or (which == "B" and not b0):
-            continue
+    jobs = {"A": (0, an, sa), "B": (an, bn, sb)}
+    for name in which:
+        b0, n, st = jobs[name]
         st.wait_event(e0)
         with torch.cuda.stream(st):
             tr._code_fused(xh, buf, uh, obj, b0, b0 + n)
@@ -64,5 +65,5 @@ def go(which):
     return e0.elapsed_time(e1)
 
 
-for which in ("A", "B", "AB", "AB"):
+for which in ("A", "B", "AB", "BA", "BA"):
     print(f"{which}: {go(which):.2f} ms", flush=True)
