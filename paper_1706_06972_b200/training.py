@@ -709,13 +709,14 @@ def train_batch(samples, shape: SignalShape, config: TrainConfig, test_samples=N
             raise DivergenceError(f"code solver diverged at iteration {it}")
         code_change = 0.0
         if prev_u is not None:
-            changes = []
+            # per-sample ||u - u_prev||^2 and ||u||^2 into one (n, 2) buffer: one host sync per
+            # outer iteration instead of one per sample
+            per = torch.zeros((n, 2), dtype=torch.float64, device=tr.dev)
             for b in range(n):
-                norms.zero_()
                 _lib.call("ocsc_norms2", _lib.code(tr.dtype), buf.u[b].numel(), _lib.ptr(buf.u[b]),
-                          _lib.ptr(prev_u[b]), _lib.ptr(norms), _lib.stream())
-                a2, b2 = norms.cpu().tolist()
-                changes.append(np.sqrt(a2) / max(np.sqrt(b2), 1e-12))
+                          _lib.ptr(prev_u[b]), _lib.ptr(per[b]), _lib.stream())
+            p2 = per.cpu().numpy()
+            changes = np.sqrt(p2[:, 0]) / np.maximum(np.sqrt(p2[:, 1]), 1e-12)
             code_change = float(np.mean(changes))
             prev_u.copy_(buf.u[:n])
         else:
