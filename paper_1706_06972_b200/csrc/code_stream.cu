@@ -595,6 +595,7 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   C* SB = SA + H * PR;                  // [H][PR] second plane: stage-2 passes run out of place
   C* WB = SB + H * PR;                  // [H][NR] state plane (pairs)
   C* PT = WB + H * NR;                  // [NF] the group's synthesis partial
+  C* GS = PT + NF;                      // [NF] the sample's g, loaded once for all the group's planes
   __shared__ double scratch[4 * 32];
   __shared__ C tws[NR + 1];  // e^{-2 pi i k / W}, k <= NR
   const int b = blockIdx.y, grp = blockIdx.x;
@@ -602,7 +603,10 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   const int tid = threadIdx.x;
   const int k0 = grp * a.kper, k1 = min(a.K, k0 + a.kper);
   const C* gb = a.g + (int64_t)b * NF;
-  for (int f = tid; f < NF; f += NT) PT[f] = mkc<C>(0, 0);
+  for (int f = tid; f < NF; f += NT) {
+    PT[f] = mkc<C>(0, 0);
+    GS[f] = gb[f];
+  }
   for (int i = tid; i <= NR; i += NT) tws[i] = a.tw[i];
   C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};
   bool nonfinite = false;
@@ -617,11 +621,11 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
       for (int e = 2 * tid; e < H * NR; e += 2 * NT) cp_async<16>(WB + e, wpl + e);
       cp_async_commit();
     }
-    // (a) inverse input conj(D_k) g (a shared-memory copy of D_k prefetched during the previous
-    // plane measured slower: the g loads stay exposed and the extra group waits cost more)
+    // (a) inverse input conj(D_k) g: g from shared memory (loaded once per CTA), D_k from L2
+    // (a shared-memory prefetch of D_k instead of g measured slower)
     for (int f = tid; f < NF; f += NT) {
       const int u = f / WH, v = f - u * WH;
-      SA[u * PR + v] = cmulc2(dk[f], gb[f]);
+      SA[u * PR + v] = cmulc2(dk[f], GS[f]);
     }
     __syncthreads();
     PLANE_STAMP(1)
@@ -848,7 +852,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   }
   PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
                      (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
-  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + NF) * sizeof(cx<T>);
+  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + 2 * NF) * sizeof(cx<T>);
   if constexpr (G::PLANE)
     OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
   int rc = OCSC_OK, chunk = 0;
