@@ -119,9 +119,18 @@ int ocsc_code_admm(int dtype, int H, int W, int K, int B, const void* xh, const 
 int ocsc_code_fused_cluster(int dtype, int H, int W, int K, int B);
 /* Launch plan of ocsc_code_fused (host array of 8 int32): main cluster size, threads per
  * CTA, dynamic shared memory bytes, registers per thread, main-shape resident clusters,
- * samples run with the main shape, tail cluster size (0 = none), tail resident clusters.
- * Returns the main cluster size (0 = unsupported). */
+ * b_split = samples the plan finishes before its last main round starts (B when it has
+ * one round), then the cluster size and resident clusters of the plan for the remaining
+ * B - b_split samples (0, 0 when b_split = B): a caller that splits the batch there can
+ * overlap work with the second part.  Returns the main cluster size (0 = unsupported). */
 int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32_t* info);
+/* Concurrent-plan details of ocsc_code_fused (host array of 8 int32): side cluster size
+ * (0 = the plan is sequential: main waves + optional tail), side clusters launched, side
+ * shape keeps D in registers, main clusters launched (persistent), samples per schedule
+ * row, main shape keeps D in registers, modelled makespan x 1000, concurrent flag.  A
+ * concurrent plan runs the main shape persistent and a narrower side shape on the SMs the
+ * main clusters leave free, launched programmatically behind it on the same stream. */
+int ocsc_code_fused_side_info(int dtype, int H, int W, int K, int B, int32_t* info);
 /* Development aid: device buffer of 64 int64 that receives clock64() phase stamps of CTA 0
  * for iterations 8..15 of the next fused launches (NULL disables). */
 int ocsc_debug_fused_profile(void* buf);

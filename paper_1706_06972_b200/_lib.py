@@ -46,6 +46,7 @@ SIGNATURES = {
     "ocsc_code_admm": [_I, _I, _I, _I, _I, _P, _P, _P, _D, _D, _I, _D, _P, _P, _P, _P, _P, _P, _I, _P],
     "ocsc_code_fused_cluster": [_I, _I, _I, _I, _I],
     "ocsc_code_fused_info": [_I, _I, _I, _I, _I, _P],
+    "ocsc_code_fused_side_info": [_I, _I, _I, _I, _I, _P],
     "ocsc_debug_fused_profile": [_P],
     "ocsc_debug_plane_profile": [_P],
     "ocsc_debug_fused_iterations": [_P],

@@ -22,11 +22,14 @@
 // produces F(U) (needed by the history), the code U, and the objective.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <tuple>
 
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "fft_small.cuh"
@@ -65,6 +68,15 @@ struct FusedArgs {
   double* resid;    // optional (B)
   int32_t* iters;   // (B)
   int32_t* status;  // (B)
+  // persistent schedule (concurrent plans): cluster c of this launch codes samples
+  // sched[(sched_c0 + c) * sched_w + i], i = 0.. until -1; null: cluster c codes sample b0 + c
+  const int32_t* sched = nullptr;
+  int sched_w = 0, sched_c0 = 0;
+  // residency probe (plan calibration): no coding; every CTA spins probe_ns, role 0 records its end,
+  // role 1 records when each cluster started
+  unsigned long long* probe = nullptr;
+  long long probe_ns = 0;
+  int probe_role = 0;
 };
 
 // Grid N x N with N = 2M, M odd (42 = 2 * 21 for BASELINE config 1).
@@ -259,10 +271,21 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
   using S = Smem<T, N>;
   constexpr int M = G::M, Wh = G::Wh, WP = G::WP, RS = G::RS, PS = G::PS, NF = G::NF;
 
+  // a concurrent plan launches its second cluster shape programmatically after this grid: let it
+  // start as soon as every cluster of this (persistent, fully resident) grid is running
+  asm volatile("griddepcontrol.launch_dependents;");
   cg::cluster_group cl = cg::this_cluster();
   const int CS = (int)cl.num_blocks();
   const int r = (int)cl.block_rank();
-  const int b = a.b0 + (int)(blockIdx.x / CS);
+  const int ci = (int)(blockIdx.x / CS);  // cluster index within this launch
+  if (a.probe) {  // both roles hold their SMs for probe_ns, so a side cluster that started
+    const long long t0 = global_ns();  // before the main grid's first exit was co-resident with it
+    if (a.probe_role == 1 && threadIdx.x == 0 && r == 0) a.probe[1 + ci] = (unsigned long long)t0;
+    while (global_ns() - t0 < a.probe_ns) {
+    }
+    if (a.probe_role == 0 && threadIdx.x == 0) atomicMin(a.probe, (unsigned long long)global_ns());
+    return;
+  }
   const int K = a.K;
   const int k0 = (int)((int64_t)r * K / CS), k1 = (int)((int64_t)(r + 1) * K / CS);
   const int nk = k1 - k0;
@@ -299,11 +322,8 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
   C* xrow = X + rj * PS + rq * RS;
   T* wrow = wS + (rj * N + rq) * WP;
 
-  for (int i = tid; i < nk * N * WP; i += nt) wS[i] = (T)0;
-  for (int i = tid; i < nk * PS; i += nt) X[i] = mkc<C>(0, 0);
   for (int i = tid; i < slice_; i += nt) {
     const int f = r * slice_ + i;
-    xsl[i] = f < NF ? a.xh[(int64_t)b * NF + f] : mkc<C>(0, 0);
     dsl[i] = f < NF ? (T)1 / a.den[f] : (T)0;
   }
   const int nwarps = nt >> 5;
@@ -328,8 +348,6 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
     mbar_init(&mb_part, 1);
     mbar_init(&mb_g, 2);  // tid 0's expect_tx + the last warp's arrival after it publishes the decision
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_arm(&mb_part, part_bytes);  // phase 0: partials only
-    mbar_arm(&mb_g, (uint32_t)(NF * sizeof(C)));
   }
   uint32_t ph_part = 0, ph_g = 0;
   if (tid == 0) s_stat = 0;
@@ -358,8 +376,7 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
       dz.v[n2] = dcol[u0 * Wh + sh * dpd];
     });
   };
-  ColRegs dreg;
-  if constexpr (DREG) load_dcol(dreg);
+  ColRegs dreg;  // (loaded at each sample's start: nothing of it stays live across samples)
   // COL_F / COL_FE: forward column transform of the row-transformed planes times D (COL_FE also
   // emits the raw transform, F(U) for the history); COL_I: inverse column transform of conj(D) g
   // (double: z holds D on entry)
@@ -406,21 +423,23 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
   int ro[RP], rown[RP];
   uint32_t rdst[RP];
   const C* rdg[RP];
+  auto reduce_items = [&]() {  // (recomputed per sample, like D: short live ranges)
 #pragma unroll
-  for (int i = 0; i < RP; ++i) {
-    const int f = tid + i * nt;
-    ro[i] = -1;
-    rdst[i] = 0;
-    rown[i] = 0;
-    rdg[i] = Dg;
-    if (f < NF) {
-      const int u = f / Wh, v = f - u * Wh, owner = f / slice;
-      ro[i] = u * RS + v;
-      rown[i] = owner;
-      rdst[i] = t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C));
-      rdg[i] = Dg + f;
+    for (int i = 0; i < RP; ++i) {
+      const int f = tid + i * nt;
+      ro[i] = -1;
+      rdst[i] = 0;
+      rown[i] = 0;
+      rdg[i] = Dg;
+      if (f < NF) {
+        const int u = f / Wh, v = f - u * Wh, owner = f / slice;
+        ro[i] = u * RS + v;
+        rown[i] = owner;
+        rdst[i] = t_part[owner] + (uint32_t)((r * slice + (f - owner * slice)) * sizeof(C));
+        rdg[i] = Dg + f;
+      }
     }
-  }
+  };
   // partial synthesis sum_k D_k F(t_k) over own filters, pushed into the owner CTA's slot;
   // the nk (D, X) loads of a frequency are independent, so they issue back to back
   auto push_item = [&](int o, const C* dg, uint32_t dst, int owner) {
@@ -461,11 +480,41 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
     return y;
   };
 
+  // ---- the samples of this cluster: one (plain launch) or a schedule row (persistent launch) --
+  // (the row position lives in shared memory and the sample is re-derived after the iterations,
+  // so the outer loop adds no register live across them)
+  __shared__ int s_sw;
+  auto sample_at = [&](int sw) {
+    if (a.sched) return sw < a.sched_w ? a.sched[(a.sched_c0 + ci) * a.sched_w + sw] : -1;
+    return sw == 0 ? a.b0 + ci : -1;
+  };
+  if (tid == 0) s_sw = 0;
+  __syncthreads();
+  for (;;) {
+  const int sw = s_sw;
+  const int b = sample_at(sw);
+  if (b < 0) break;
+  // per-sample state: a fresh phase of both exchange barriers (a remote transaction may land
+  // before the arm; the tx count just dips below zero), zero workspace, this sample's spectrum
+  if (tid == 0) {
+    mbar_arm(&mb_part, part_bytes);  // first phase of a sample: partials only
+    mbar_arm(&mb_g, (uint32_t)(NF * sizeof(C)));
+  }
+  for (int i = tid; i < nk * N * WP; i += nt) wS[i] = (T)0;
+  for (int i = tid; i < nk * PS; i += nt) X[i] = mkc<C>(0, 0);
+  for (int i = tid; i < slice_; i += nt) {
+    const int f = r * slice_ + i;
+    xsl[i] = f < NF ? a.xh[(int64_t)b * NF + f] : mkc<C>(0, 0);
+  }
+  if constexpr (DREG) load_dcol(dreg);
+  reduce_items();
+  __syncthreads();
   int it = 0, stat = 0;
-  long long* prof = (blockIdx.x == 0 && a.b0 == 0 && tid == 0) ? g_fused_prof : nullptr;
+  const bool first = blockIdx.x == 0 && a.b0 == 0 && sw == 0 && a.sched_c0 == 0 && tid == 0;
+  long long* prof = first ? g_fused_prof : nullptr;
   long long* tl = (r == 0 && tid == 0) ? g_fused_timeline : nullptr;
   if (tl) tl[2 * b] = global_ns();
-  long long* itl = (blockIdx.x == 0 && a.b0 == 0 && tid == 0) ? g_fused_iter : nullptr;
+  long long* itl = first ? g_fused_iter : nullptr;
   for (;;) {
     const int pit = it;
     if (itl && it < 512) {
@@ -599,6 +648,8 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
 
   // ---- outputs: U = S(w) (and t), F(U), objective -------------------------------------------
   if (itl) itl[505] = global_ns();
+  {
+  const int b = sample_at(s_sw);
   double l1 = 0.0;
   if (rvalid) {
     const int64_t rowoff = (((int64_t)b * K + k0 + rj) * N + rq) * N;
@@ -633,6 +684,7 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
   if (itl) itl[507] = global_ns();
   reduce_push();
   mbar_wait(&mb_part, ph_part);
+  ph_part ^= 1;
   if (itl) itl[508] = global_ns();
   double e = 0.0;
   {
@@ -666,6 +718,13 @@ __global__ void __maxnreg__(DREG_ ? 120 : 96) k_code_fused(FusedArgs<T> a) {
     a.status[b] = stat;
     if (tl) tl[2 * b + 1] = global_ns();
   }
+  }
+  if (tid == 0) s_sw = s_sw + 1;  // (every thread read it before the barriers above)
+  __syncthreads();
+  }  // samples of this cluster
+  // a programmatically launched grid completes only after the grid it overlaps (so stream order
+  // holds for whatever follows it); a no-op for a plain launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- dispatch --
@@ -680,9 +739,22 @@ static auto kernel_of(bool dreg) -> void (*)(FusedArgs<T>) {
   if constexpr (sizeof(T) == 4) return dreg ? k_code_fused<T, N, true> : k_code_fused<T, N, false>;
   else return k_code_fused<T, N, false>;
 }
+// A plan is one of two kinds.
+//  * sequential: `main` clusters in waves (one cluster per sample) for the first b_main samples,
+//    then the rest on `tail`, a wider shape, instead of a mostly idle last wave;
+//  * concurrent: `main` runs persistent (n_main resident clusters, each coding a row of a
+//    static schedule), and `side`, a smaller shape that fits the SMs the main clusters leave
+//    free (GPC packing: eleven 10-CTA clusters leave 38 of 148 SMs, which hold four 8-CTA
+//    clusters), is launched programmatically behind it on the same stream and codes its own
+//    schedule rows at the same time.
 struct FusedPlan {
-  FusedShape main, tail;  // main shape for the first b_main samples, tail shape for the rest
-  int b_main = 0;
+  FusedShape main, tail, side;
+  int b_main = 0;                  // sequential: samples on the main waves
+  int n_main = 0, n_side = 0;      // concurrent: clusters launched per shape
+  int sched_w = 0;                 // concurrent: samples per schedule row
+  int32_t* sched = nullptr;        // concurrent: device table [(main.active + n_side) x sched_w]
+  int b_split = 0;                 // samples the plan finishes before its last main round starts
+  double makespan = 0;             // modelled, in cost units
 };
 
 template <typename T, int N>
@@ -709,22 +781,142 @@ static int max_active_clusters(const FusedShape& sh, int B) {
   return n;
 }
 
-// Choose cluster shapes.  A wave runs `active` clusters at once and lasts ~ nk + const
-// (nk = filters per CTA).  The plan minimises the modelled makespan over (main shape, tail
-// shape) pairs: BASELINE config 1 runs 45 samples as 3 waves of 15 nine-CTA clusters and the
-// last 5 on fifteen-CTA clusters instead of a mostly idle fourth wave; a batch smaller than one
-// wave takes the shape that finishes soonest (the widest cluster that holds it).
+// launch `nclu` clusters of shape sh; pdl: programmatic launch behind the previous grid on s
 template <typename T, int N>
-static FusedPlan plan_for(int K, int B) {
+static cudaError_t launch_clusters(const FusedArgs<T>& a, const FusedShape& sh, int nclu, bool pdl, cudaStream_t s) {
+  auto kern = kernel_of<T, N>(sh.dreg);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+  if (e != cudaSuccess) return e;
+  if (sh.cs > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+    return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nclu * sh.cs, 1, 1);
+  cfg.blockDim = dim3(sh.threads, 1, 1);
+  cfg.dynamicSmemBytes = sh.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = sh.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+// How many clusters of `side` run while main.active clusters of `main` are resident: measured
+// once per shape pair with the kernels themselves in probe mode (the main grid spins for a
+// while, the side grid is launched programmatically behind it and stamps when each cluster
+// starts).  Cached; 0 when the probe cannot run (e.g. inside a stream capture).
+template <typename T, int N>
+static int side_capacity(const FusedShape& main, const FusedShape& side) {
+  static std::map<std::tuple<int, int, int, int, int, int, int, int>, int> cache;  // (caller holds the plan lock)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(dev, main.cs, (int)main.dreg, (int)main.smem, side.cs, (int)side.dreg,
+                                   (int)side.smem, side.threads);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaStream_t s = nullptr;
+  unsigned long long* rec = nullptr;
+  const int nrec = 1 + side.active;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaMalloc(&rec, sizeof(unsigned long long) * nrec) == cudaSuccess &&
+      cudaMemsetAsync(rec, 0xff, sizeof(unsigned long long) * nrec, s) == cudaSuccess) {
+    FusedArgs<T> pa{};
+    pa.probe = rec;
+    pa.probe_ns = 300000;  // 0.3 ms: every co-resident side cluster starts well inside it
+    pa.probe_role = 0;
+    bool ok = launch_clusters<T, N>(pa, main, main.active, false, s) == cudaSuccess;
+    pa.probe_role = 1;
+    ok = ok && launch_clusters<T, N>(pa, side, side.active, true, s) == cudaSuccess;
+    std::vector<unsigned long long> h(nrec);
+    ok = ok && cudaStreamSynchronize(s) == cudaSuccess &&
+         cudaMemcpy(h.data(), rec, sizeof(unsigned long long) * nrec, cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (ok)
+      for (int c = 0; c < side.active; ++c) n += h[1 + c] < h[0];
+    if (ok && getenv("OCSC_FUSED_PROBE_DEBUG")) {
+      unsigned long long t0 = h[0];
+      for (int c = 0; c < side.active; ++c) t0 = std::min(t0, h[1 + c]);
+      fprintf(stderr, "side_capacity main cs=%d x%d side cs=%d x%d: main end %+.1f us, side starts", main.cs,
+              main.active, side.cs, side.active, (h[0] - t0) * 1e-3);
+      for (int c = 0; c < side.active; ++c) fprintf(stderr, " %.1f", (h[1 + c] - t0) * 1e-3);
+      fprintf(stderr, " -> %d\n", n);
+    }
+  }
+  cudaGetLastError();
+  if (rec) cudaFree(rec);
+  if (s) cudaStreamDestroy(s);
+  cache.emplace(key, n);
+  return n;
+}
+
+// cost of one sample on a shape, in model units: filters per CTA plus a fixed per-iteration
+// cluster overhead (fitted to scripts/cluster_sweep.py on a B200); register-resident D: 17.8 k
+// cycles per iteration at 10 filters per CTA against 23.9 k at 12 filters with D reloaded from
+// L2 (profiles/r2_phase_*.log)
+static double shape_cost(const FusedShape& sh) { return ((double)sh.nk + 3.5) * (sh.dreg ? 0.856 : 1.0); }
+
+// Static list schedule of B equal-cost samples over nm clusters of cost cm and ns of cost cs_:
+// each sample goes to the cluster that would finish it first (main first on ties); samples are
+// then numbered in order of modelled completion, so [0, b) are the first b to finish.
+struct Schedule {
+  std::vector<std::vector<int>> rows;  // per cluster (main rows first), sample indices
+  double makespan = 0, last_main_start = 0;
+  int used_side = 0, b_split = 0;
+};
+static Schedule list_schedule(int B, int nm, double cm, int ns, double cs_) {
+  Schedule sc;
+  const int nc = nm + ns;
+  std::vector<double> fin(nc, 0.0);
+  std::vector<std::tuple<double, int, int>> slots;  // (completion, cluster, position in row)
+  std::vector<int> len(nc, 0);
+  for (int s = 0; s < B; ++s) {
+    int best = 0;
+    double bt = 1e300;
+    for (int c = 0; c < nc; ++c) {
+      const double t = fin[c] + (c < nm ? cm : cs_);
+      if (t < bt - 1e-9) {
+        bt = t;
+        best = c;
+      }
+    }
+    fin[best] = bt;
+    slots.emplace_back(bt, best, len[best]++);
+  }
+  std::sort(slots.begin(), slots.end());
+  sc.rows.assign(nc, {});
+  for (int c = 0; c < nc; ++c) sc.rows[c].assign(len[c], -1);
+  for (int i = 0; i < B; ++i) sc.rows[std::get<1>(slots[i])][std::get<2>(slots[i])] = i;
+  for (int c = 0; c < nc; ++c) {
+    sc.makespan = std::max(sc.makespan, fin[c]);
+    if (c < nm) sc.last_main_start = std::max(sc.last_main_start, fin[c] - cm);
+    if (c >= nm && len[c]) ++sc.used_side;
+  }
+  for (int i = 0; i < B; ++i) sc.b_split += std::get<0>(slots[i]) <= sc.last_main_start + 1e-9;
+  return sc;
+}
+
+// Choose the plan with the smallest modelled makespan: every (main, tail) pair of the
+// sequential kind, and (main, side) pairs of the concurrent kind for the three main shapes with
+// the highest throughput and every narrower side shape that co-resides with them.  BASELINE
+// config 1 (K = 100, B = 50, float): eleven 10-CTA clusters (register-resident D) plus four
+// 8-CTA clusters; 42 + 8 samples, four main rounds.
+template <typename T, int N>
+static FusedPlan plan_for(int K, int B, bool can_probe) {
   FusedPlan plan;
   int dev = 0, max_smem = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return plan;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   FusedShape shapes[32];
   int ns = 0;
-  const char* force = getenv("OCSC_FUSED_CS");  // dev knob: a single cluster size, no tail
+  const char* force = getenv("OCSC_FUSED_CS");  // dev knob: a single cluster size, no tail/side
   const int fcs = force ? atoi(force) : 0;
   const char* fdr = getenv("OCSC_FUSED_DREG");  // dev knob: 0 / 1 forces the D variant
+  const char* fside = getenv("OCSC_FUSED_SIDE");  // dev knob: 0 disables the concurrent kind
   for (int v = 0; v < (sizeof(T) == 4 ? 2 : 1); ++v) {
     const bool dreg = sizeof(T) == 4 && v == 0;
     if (fdr && atoi(fdr) != (int)dreg) continue;
@@ -740,29 +932,24 @@ static FusedPlan plan_for(int K, int B) {
       sh.smem = Smem<T, N>::total(sh.nk, cs);
       sh.threads = Smem<T, N>::threads(sh.nk);
       if (sh.smem > (size_t)max_smem || sh.threads > fa.maxThreadsPerBlock) continue;
-      sh.active = max_active_clusters<T, N>(sh, B);
+      sh.active = max_active_clusters<T, N>(sh, 1024);
       if (sh.active > 0) shapes[ns++] = sh;
     }
   }
   if (!ns) return plan;
-  // makespan model: a wave of a shape costs (nk + 3.5) units (filters per CTA plus a fixed
-  // per-iteration cluster overhead; fitted to scripts/cluster_sweep.py on a B200).  Take the
-  // main shape and optional tail shape with the smallest total: full waves of the main shape,
-  // then the remainder either as one more main wave or on the tail shape's waves.
-  // (register-resident D: 17.8 k cycles per iteration at 10 filters per CTA against 23.9 k at 12
-  // filters with D reloaded from L2, profiles/r2_phase_*.log)
-  auto cost = [](const FusedShape& sh) { return ((double)sh.nk + 3.5) * (sh.dreg ? 0.856 : 1.0); };
   double best_t = 1e300;
+  // sequential kind: full waves of the main shape, then the remainder either as one more main
+  // wave or on the tail shape's waves
   for (int m = 0; m < ns; ++m) {
     const FusedShape& M = shapes[m];
     const int nfull = B / M.active, rem = B - nfull * M.active;
-    double t = nfull * cost(M);
+    double t = nfull * shape_cost(M);
     int tail = -1;
     if (rem > 0) {
-      double tr = cost(M);
+      double tr = shape_cost(M);
       if (nfull > 0)
         for (int i = 0; i < ns; ++i) {
-          const double ti = (double)((rem + shapes[i].active - 1) / shapes[i].active) * cost(shapes[i]);
+          const double ti = (double)((rem + shapes[i].active - 1) / shapes[i].active) * shape_cost(shapes[i]);
           if (ti < tr * 0.98) {
             tr = ti;
             tail = i;
@@ -772,16 +959,69 @@ static FusedPlan plan_for(int K, int B) {
     }
     if (t < best_t * 0.999) {
       best_t = t;
+      plan = FusedPlan{};
       plan.main = M;
       plan.tail = tail >= 0 ? shapes[tail] : FusedShape{};
       plan.b_main = tail >= 0 ? nfull * M.active : B;
+      plan.b_split = tail >= 0 ? plan.b_main : B;
+      plan.makespan = t;
     }
   }
-  return plan;
+  // concurrent kind
+  if (!can_probe || fcs || (fside && atoi(fside) == 0) || B <= 1) return plan;
+  int order[32];
+  for (int i = 0; i < ns; ++i) order[i] = i;
+  std::sort(order, order + ns, [&](int x, int y) {
+    return shapes[x].active / shape_cost(shapes[x]) > shapes[y].active / shape_cost(shapes[y]);
+  });
+  Schedule best_sc;
+  int best_m = -1, best_s = -1, best_nside = 0;
+  for (int oi = 0; oi < std::min(ns, 3); ++oi) {
+    const FusedShape& M = shapes[order[oi]];
+    if (B <= M.active) continue;  // one round: nothing for a side shape to take
+    for (int si = 0; si < ns; ++si) {
+      const FusedShape& S = shapes[si];
+      if (S.cs > M.cs) continue;
+      const int cap = side_capacity<T, N>(M, S);
+      if (cap <= 0) continue;
+      Schedule sc = list_schedule(B, M.active, shape_cost(M), cap, shape_cost(S));
+      if (sc.used_side == 0) continue;
+      if (sc.makespan < best_t * 0.98) {
+        best_t = sc.makespan;
+        best_sc = sc;
+        best_m = order[oi];
+        best_s = si;
+        best_nside = cap;
+      }
+    }
+  }
+  if (best_m < 0) return plan;
+  FusedPlan cp;
+  cp.main = shapes[best_m];
+  cp.side = shapes[best_s];
+  cp.n_main = std::min(cp.main.active, B);
+  cp.n_side = best_sc.used_side;
+  cp.makespan = best_sc.makespan;
+  cp.b_split = best_sc.b_split;
+  cp.b_main = B;
+  int w = 0;
+  for (const auto& row : best_sc.rows) w = std::max(w, (int)row.size());
+  cp.sched_w = w;
+  const int rows = cp.main.active + best_nside;
+  std::vector<int32_t> h((size_t)rows * w, -1);
+  for (int c = 0; c < rows; ++c)
+    for (size_t i = 0; i < best_sc.rows[c].size(); ++i) h[(size_t)c * w + i] = best_sc.rows[c][i];
+  if (cudaMalloc(&cp.sched, h.size() * sizeof(int32_t)) != cudaSuccess ||
+      cudaMemcpy(cp.sched, h.data(), h.size() * sizeof(int32_t), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaGetLastError();
+    if (cp.sched) cudaFree(cp.sched);
+    return plan;  // (the table lives as long as the cached plan: the process)
+  }
+  return cp;
 }
 
 template <typename T, int N>
-static const FusedPlan& cached_plan(int K, int B) {
+static const FusedPlan& cached_plan(int K, int B, cudaStream_t s) {
   static std::mutex mu;
   static std::map<std::tuple<int, int, int>, FusedPlan> cache;  // map nodes are stable
   std::lock_guard<std::mutex> lk(mu);
@@ -789,46 +1029,60 @@ static const FusedPlan& cached_plan(int K, int B) {
   cudaGetDevice(&dev);
   auto key = std::make_tuple(dev, K, B);
   auto it = cache.find(key);
-  if (it == cache.end()) it = cache.emplace(key, plan_for<T, N>(K, B)).first;
+  if (it == cache.end()) {
+    // the side-shape probe launches and synchronises: not from inside a stream capture (such a
+    // plan is not cached, so a later uncaptured call still gets the concurrent kind)
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (s) cudaStreamIsCapturing(s, &cst);
+    cudaStreamCaptureStatus lst = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(cudaStreamLegacy, &lst);
+    cudaGetLastError();
+    const bool can_probe = cst == cudaStreamCaptureStatusNone && lst == cudaStreamCaptureStatusNone;
+    if (!can_probe) {
+      static thread_local FusedPlan tmp;
+      tmp = plan_for<T, N>(K, B, false);
+      return tmp;
+    }
+    it = cache.emplace(key, plan_for<T, N>(K, B, true)).first;
+  }
   return it->second;
 }
 
 template <typename T, int N>
 static int launch_shape(FusedArgs<T> a, const FusedShape& sh, int b0, int nb, cudaStream_t s) {
   if (nb <= 0) return OCSC_OK;
-  auto kern = kernel_of<T, N>(sh.dreg);
-  OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem));
-  if (sh.cs > 8) OCSC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   a.b0 = b0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nb * sh.cs, 1, 1);
-  cfg.blockDim = dim3(sh.threads, 1, 1);
-  cfg.dynamicSmemBytes = sh.smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = sh.cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  OCSC_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  a.sched = nullptr;
+  OCSC_CUDA((launch_clusters<T, N>(a, sh, nb, false, s)));
   OCSC_LAUNCHED("k_code_fused");
   return OCSC_OK;
 }
 
 template <typename T, int N>
 static int launch_fused(const FusedArgs<T>& a, cudaStream_t s) {
-  const FusedPlan& p = cached_plan<T, N>(a.K, a.B);
+  const FusedPlan& p = cached_plan<T, N>(a.K, a.B, s);
   if (!p.main.cs) return fail(OCSC_EARG, "fused code ADMM: no cluster shape fits this device");
+  if (p.sched) {  // concurrent: persistent main grid, the side grid programmatically behind it
+    FusedArgs<T> m = a;
+    m.b0 = 0;
+    m.sched = p.sched;
+    m.sched_w = p.sched_w;
+    m.sched_c0 = 0;
+    OCSC_CUDA((launch_clusters<T, N>(m, p.main, p.n_main, false, s)));
+    OCSC_LAUNCHED("k_code_fused");
+    m.sched_c0 = p.main.active;
+    OCSC_CUDA((launch_clusters<T, N>(m, p.side, p.n_side, true, s)));
+    OCSC_LAUNCHED("k_code_fused");
+    return OCSC_OK;
+  }
   int rc = launch_shape<T, N>(a, p.main, 0, p.b_main, s);
   if (rc) return rc;
   return launch_shape<T, N>(a, p.tail, p.b_main, a.B - p.b_main, s);
 }
 
 template <typename T, int N>
-static int query_fused(int K, int B, int* info) {
-  const FusedPlan& p = cached_plan<T, N>(K, B);
+static int query_fused(int K, int B, int* info, int* side) {
+  const FusedPlan& p = cached_plan<T, N>(K, B, nullptr);
   if (info) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, kernel_of<T, N>(p.main.dreg));
@@ -837,9 +1091,25 @@ static int query_fused(int K, int B, int* info) {
     info[2] = (int)p.main.smem;
     info[3] = fa.numRegs;
     info[4] = p.main.active;
-    info[5] = p.b_main;
-    info[6] = p.tail.cs;
-    info[7] = p.tail.active;
+    info[5] = p.b_split;
+    FusedShape rest = p.tail;
+    if (p.sched && p.b_split < B) {
+      const FusedPlan& q = cached_plan<T, N>(K, B - p.b_split, nullptr);
+      rest = q.main;
+      rest.active = q.main.active;
+    }
+    info[6] = p.b_split < B ? rest.cs : 0;
+    info[7] = p.b_split < B ? rest.active : 0;
+  }
+  if (side) {
+    side[0] = p.sched ? p.side.cs : 0;
+    side[1] = p.n_side;
+    side[2] = (int)p.side.dreg;
+    side[3] = p.n_main;
+    side[4] = p.sched_w;
+    side[5] = (int)p.main.dreg;
+    side[6] = (int)(p.makespan * 1000.0);
+    side[7] = p.sched ? 1 : 0;
   }
   return p.main.cs;
 }
@@ -849,9 +1119,9 @@ static int query_fused(int K, int B, int* info) {
 
 template <typename T>
 static int fused_dispatch(int H, int W, bool query, const FusedArgs<T>* a, int K, int B, cudaStream_t s,
-                          int* info = nullptr) {
+                          int* info = nullptr, int* side = nullptr) {
 #define OCSC_CASE(NN) \
-  if (H == NN && W == NN) return query ? query_fused<T, NN>(K, B, info) : launch_fused<T, NN>(*a, s);
+  if (H == NN && W == NN) return query ? query_fused<T, NN>(K, B, info, side) : launch_fused<T, NN>(*a, s);
   OCSC_FUSED_SIZES(OCSC_CASE)
 #undef OCSC_CASE
   return query ? 0 : fail(OCSC_EARG, "fused code ADMM: grid not instantiated");
@@ -884,6 +1154,14 @@ extern "C" int ocsc_code_fused_info(int dtype, int H, int W, int K, int B, int32
   if (K <= 0 || B <= 0) return 0;
   if (dtype == OCSC_F32) return fused_dispatch<float>(H, W, true, nullptr, K, B, nullptr, info);
   if (dtype == OCSC_F64) return fused_dispatch<double>(H, W, true, nullptr, K, B, nullptr, info);
+  return 0;
+}
+
+extern "C" int ocsc_code_fused_side_info(int dtype, int H, int W, int K, int B, int32_t* info) {
+  for (int i = 0; i < 8; ++i) info[i] = 0;
+  if (K <= 0 || B <= 0) return 0;
+  if (dtype == OCSC_F32) return fused_dispatch<float>(H, W, true, nullptr, K, B, nullptr, nullptr, info);
+  if (dtype == OCSC_F64) return fused_dispatch<double>(H, W, true, nullptr, K, B, nullptr, nullptr, info);
   return 0;
 }
 
