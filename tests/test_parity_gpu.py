@@ -402,6 +402,46 @@ def test_fused_equals_cufft_path(dims, K, B):
     assert rel(a.final_filters(), b.final_filters()) < 1e-11
 
 
+def _fused_side_info(dt, N, K, B):
+    import ctypes
+    from paper_1706_06972_b200 import _lib
+    side = (ctypes.c_int32 * 8)()
+    _lib.load().ocsc_code_fused_side_info(dt, N, N, K, B, side)
+    return list(side)
+
+
+def test_fused_concurrent_plan_main_samples_bitwise_side_samples_close(monkeypatch):
+    """The headline's concurrent plan: persistent 10-CTA main clusters each code a row of the
+    static schedule (the 2nd..4th sample of a row reuse the cluster's shared memory and exchange
+    barriers) while 8-CTA side clusters run on the SMs left free.  Every main-cluster sample is
+    bitwise the single-shape sequential plan's result; side samples agree to float32 rounding."""
+    c = CONFIGS[1]
+    B, K = 50, 100
+    side = _fused_side_info(4, 42, K, B)
+    assert side[7] == 1 and side[0] == 8 and side[1] >= 1 and side[3] == 11 and side[4] >= 2, side
+    shape = ob.SignalShape(c["grid"], (11, 11))
+    X = synth_images(B, c["dims0"], c["grid"], c["K0"], seed=5).reshape(B, -1)
+    kw = dict(n_filters=K, dtype="float32", stop_tol=0.0, beta=1.0, rho_code=1.0, rho_dict=1.0, inner_iters=1,
+              seed=3, code_max_iters=40, overlap=False)
+    a = ob.OnlineTrainer(shape, ob.TrainConfig(batch_size=B, **kw))
+    ra = a.partial_fit(X)
+    assert a.last_path == "fused"
+    # the sequential reference: every sample on 10-CTA register-D clusters, two fresh trainers
+    # with the same initial dictionary (a partial_fit updates it)
+    monkeypatch.setenv("OCSC_FUSED_CS", "10")
+    monkeypatch.setenv("OCSC_FUSED_DREG", "1")
+    h = B // 2
+    rb = [ob.OnlineTrainer(shape, ob.TrainConfig(batch_size=h, **kw)).partial_fit(X[i * h:(i + 1) * h])
+          for i in range(2)]
+    obj_b = np.concatenate([r.objectives for r in rb])
+    codes_b = np.concatenate([r.codes.cpu().numpy() for r in rb])
+    codes_a = ra.codes.cpu().numpy()
+    same = [np.array_equal(codes_a[i], codes_b[i]) and ra.objectives[i] == obj_b[i] for i in range(B)]
+    assert sum(same) >= B - side[1] * side[4], sum(same)  # at most the side rows' samples differ
+    assert np.max(np.abs(np.asarray(ra.objectives) - obj_b) / np.abs(obj_b)) < 1e-4
+    assert rel(codes_a, codes_b) < 1e-3
+
+
 def test_fused_float32_matches_oracle_42x42():
     c = CONFIGS[1]
     B = 6
