@@ -134,6 +134,7 @@ int ocsc_code_fused_side_info(int dtype, int H, int W, int K, int B, int32_t* in
 /* Development aid: device buffer of 64 int64 that receives clock64() phase stamps of CTA 0
  * for iterations 8..15 of the next fused launches (NULL disables). */
 int ocsc_debug_fused_profile(void* buf);
+int ocsc_debug_chol_profile(void* buf);  /* dev aid: clock64 phase stamps of the blocked Cholesky (CTA 0) */
 int ocsc_debug_plane_profile(void* buf);   /* debug: clock64 phase stamps of the plane-resident stream kernel */
 /* Development aid: device buffer of 2*B int64 receiving %globaltimer at each sample's start/end. */
 int ocsc_debug_fused_timeline(void* buf);

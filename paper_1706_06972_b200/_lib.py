@@ -48,6 +48,7 @@ SIGNATURES = {
     "ocsc_code_fused_info": [_I, _I, _I, _I, _I, _P],
     "ocsc_code_fused_side_info": [_I, _I, _I, _I, _I, _P],
     "ocsc_debug_fused_profile": [_P],
+    "ocsc_debug_chol_profile": [_P],
     "ocsc_debug_plane_profile": [_P],
     "ocsc_debug_fused_iterations": [_P],
     "ocsc_debug_fused_timeline": [_P],

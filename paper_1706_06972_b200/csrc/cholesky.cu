@@ -22,6 +22,11 @@ namespace ocsc {
 using sfft::static_for;
 constexpr int CT = 32;  // tile edge
 
+// optional phase stamps of CTA 0 (development aid): [0] start, [1] after the expansion, [2] after
+// diag(0), then per step kb: [3+4kb] panel done, [4+4kb] strips A done, [5+4kb] warp 0's diagonal
+// done, [6+4kb] step done (clock64)
+__device__ long long* g_chol_prof = nullptr;
+
 template <typename C>
 __device__ __forceinline__ C* tile_ptr(C* L, int K, int ib, int jb) {
   return L + (int64_t)ib * CT * K + (int64_t)jb * CT;
@@ -50,6 +55,98 @@ __device__ __forceinline__ void cmac_conj2(C& acc, C a, C as, decltype(C::x) bx,
   acc = vfma(as, vsplat<C>(by), acc);
 }
 
+// explicit shared-memory complex loads / stores (32-bit shared addresses: LDS / STS even where a
+// generic pointer would lose its address space)
+template <typename C>
+__device__ __forceinline__ C lds_c(uint32_t a);
+template <>
+__device__ __forceinline__ float2 lds_c<float2>(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ double2 lds_c<double2>(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_c(uint32_t a, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts_c(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Cholesky of one CT x CT diagonal tile by one warp (lane = row), in place in shared memory
+// (sD: [CT][CT + 1] complex), the lower triangle read from and written back to `tile` (global,
+// row stride K); 1 / L_jj into dinv.  Right-looking, one column per step: every lane reads the
+// pivot (broadcast), the rows below scale their entry of column j, then update their row of the
+// trailing triangle from the column (broadcast reads).  Rolled loops keep the routine small: it
+// runs once per tile column on the critical path, beside the trailing update of the other warps
+// (a register-resident, fully unrolled variant measured 2x slower: spills and code size).
+template <typename T>
+__device__ __noinline__ void diag_tile(cx<T>* tile, int K, uint32_t sD, T* dinv, int lane, int32_t* info, int p) {
+  using C = cx<T>;
+  constexpr int LD = CT + 1;
+  constexpr uint32_t SZ = sizeof(C);
+  const C* row = tile + (int64_t)lane * K;
+#pragma unroll 8
+  for (int j = 0; j < CT; ++j) sts_c(sD + (uint32_t)(lane * LD + j) * SZ, j <= lane ? row[j] : mkc<C>(0, 0));
+  __syncwarp();
+#pragma unroll 1
+  for (int j = 0; j < CT; ++j) {
+    T d = lds_c<C>(sD + (uint32_t)(j * LD + j) * SZ).x;
+    if (!(d > (T)0)) {
+      if (lane == 0) atomicCAS(info, 0, p + 1);
+      d = (T)NAN;
+    }
+    T ljj, inv;
+    if constexpr (sizeof(T) == 4) {  // one MUFU rsqrt + a Newton step (< 1 ulp off IEEE)
+      const T y = rsqrtf(d);
+      inv = y * ((T)1.5 - (T)0.5 * d * y * y);
+      ljj = d * inv;
+    } else {
+      ljj = sqrt(d);
+      inv = (T)1 / ljj;
+    }
+    C lij = mkc<C>(0, 0);
+    const uint32_t own = sD + (uint32_t)(lane * LD) * SZ;
+    if (lane > j) {
+      lij = cscale(lds_c<C>(own + j * SZ), inv);
+      sts_c(own + j * SZ, lij);
+    } else if (lane == j) {
+      sts_c(own + j * SZ, mkc<C>(ljj, (T)0));
+    }
+    if (lane == 0) dinv[j] = inv;
+    __syncwarp();
+    // D[i][k] -= L[i][j] conj(L[k][j]),  j < k <= i: eight columns at a time, all sixteen loads
+    // issued before the first store (the shared-memory asm keeps program order)
+#pragma unroll 1
+    for (int k0 = j + 1; k0 < CT; k0 += 8) {
+      C lk[8], t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        lk[u] = k0 + u < CT ? lds_c<C>(sD + (uint32_t)((k0 + u) * LD + j) * SZ) : mkc<C>(0, 0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = k0 + u <= lane ? lds_c<C>(own + (k0 + u) * SZ) : mkc<C>(0, 0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        t[u].x -= lij.x * lk[u].x + lij.y * lk[u].y;
+        t[u].y -= lij.y * lk[u].x - lij.x * lk[u].y;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u <= lane) sts_c(own + (k0 + u) * SZ, t[u]);
+    }
+    __syncwarp();
+  }
+  C* out = tile + (int64_t)lane * K;
+#pragma unroll 8
+  for (int j = 0; j < CT; ++j)
+    if (j <= lane) out[j] = lds_c<C>(sD + (uint32_t)(lane * LD + j) * SZ);
+}
+
 // A (packed lower, K(K+1)/2 per frequency) + ridge I -> full-layout lower L = chol(A).
 // One CTA (256 threads) per frequency, right-looking over 32-wide tile columns:
 //   diagonal tile: warp 0, lane = row, the row in registers, 32 shuffle steps (no CTA barrier);
@@ -61,7 +158,7 @@ __device__ __forceinline__ void cmac_conj2(C& acc, C a, C as, decltype(C::x) bx,
 // NT = 256 (8 warps; two CTAs per SM where shared memory allows) or 512 (16 warps, two 64 x 64
 // block pairs of the trailing update at a time: K = 512, where one CTA fills the SM anyway)
 template <typename T, int NT>
-__global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>* __restrict__ S, T ridge,
+__global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >= 256 ? 2 : 3)) k_chol_blocked(int K, int Kv, const cx<T>* __restrict__ S, T ridge,
                                                           cx<T>* Lall, int32_t* info) {
   // K: factored order (a multiple of 32); Kv <= K: the history's order (S packed with Kv). Rows
   // and columns Kv..K-1 are the decoupled padding ridge * I, so L = diag(chol(A), sqrt(ridge) I).
@@ -71,13 +168,16 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>*
   C* D = reinterpret_cast<C*>(smem_raw);  // L_kk [CT][LD]
   T* dinv = reinterpret_cast<T*>(D + CT * LD);   // 1 / L_jj [CT]
   C* PT = reinterpret_cast<C*>(smem_raw + chol_panel_offset<T>());  // panel, k-major: PT[k][r]
+  const uint32_t sD = (uint32_t)__cvta_generic_to_shared(D);
   const int nb = K / CT;
   const int p = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t npk = (int64_t)Kv * (Kv + 1) / 2;
   const C* Sp = S + (int64_t)p * npk;
   C* L = Lall + (int64_t)p * K * K;
-  const int PR = K - CT + 64;  // panel row stride: K - CT rows + slack for the last 64-block
+  const int PR = (K - CT + 63) / 64 * 64;  // panel row stride: K - CT rows rounded up to the 64-row blocks
+  long long* prof = (blockIdx.x == 0 && threadIdx.x == 0) ? g_chol_prof : nullptr;
+  if (prof) prof[0] = clock64();
 
   // expand the packed lower triangle (+ ridge) into the lower half of the full layout; each
   // lane issues up to 8 loads of its row before storing (the copy is latency-bound otherwise)
@@ -99,47 +199,12 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>*
     }
   }
   __syncthreads();
+  if (prof) prof[1] = clock64();
 
-  // ---- diagonal tile kbx: warp 0, lane i holds row i of the tile ----
+  // ---- diagonal tile kbx: warp 0, the tile in shared memory (D, lane = row), rolled loops:
+  // one column per step (broadcast pivot, scale the column, rank-1 update of the rows below)
   auto diag = [&](int kbx) {
-    C a[CT];
-    const C* row = L + (int64_t)(kbx * CT + lane) * K + kbx * CT;
-#pragma unroll
-    for (int j = 0; j < CT; ++j) a[j] = j <= lane ? row[j] : mkc<C>(0, 0);
-    static_for<0, CT>([&](auto J) {
-      constexpr int j = decltype(J)::value;
-      T d = __shfl_sync(0xffffffffu, a[j].x, j);
-      if (!(d > (T)0)) {
-        if (lane == 0) atomicCAS(info, 0, p + 1);
-        d = (T)NAN;
-      }
-      T ljj, inv;
-      if constexpr (sizeof(T) == 4) {  // one MUFU rsqrt + a Newton step (< 1 ulp off IEEE)
-        const T y = rsqrtf(d);
-        inv = y * ((T)1.5 - (T)0.5 * d * y * y);
-        ljj = d * inv;
-      } else {
-        ljj = sqrt(d);
-        inv = (T)1 / ljj;
-      }
-      if (lane == j) a[j] = mkc<C>(ljj, (T)0);
-      else if (lane > j) a[j] = cscale(a[j], inv);
-      if (lane == 0) dinv[j] = inv;
-      static_for<j + 1, CT>([&](auto Kk) {
-        constexpr int k = decltype(Kk)::value;
-        const T lx = __shfl_sync(0xffffffffu, a[j].x, k), ly = __shfl_sync(0xffffffffu, a[j].y, k);
-        if (lane >= k) {  // a[k] -= L[i][j] conj(L[k][j])
-          a[k].x -= a[j].x * lx + a[j].y * ly;
-          a[k].y -= a[j].y * lx - a[j].x * ly;
-        }
-      });
-    });
-    C* out = L + (int64_t)(kbx * CT + lane) * K + kbx * CT;
-#pragma unroll
-    for (int j = 0; j < CT; ++j) {
-      D[lane * LD + j] = a[j];
-      if (j <= lane) out[j] = a[j];
-    }
+    diag_tile<T>(L + (int64_t)(kbx * CT) * K + kbx * CT, K, sD, dinv, lane, info, p);
   };
   // ---- one warp's 8-row x 64-column strip of the trailing update A22 -= P P^H:
   // 64 x 64 block pair (bi, bj), rows ty * 4.. of the pair with ty = 2 tp + lane / 16 ----
@@ -183,6 +248,7 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>*
 
   if (warp == 0) diag(0);
   __syncthreads();
+  if (prof) prof[2] = clock64();
   for (int kb = 0; kb < nb; ++kb) {
     const int r0 = (kb + 1) * CT;  // first trailing row
     const int R = K - r0;          // trailing rows
@@ -195,14 +261,14 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>*
       for (int j = 0; j < CT; ++j) x[j] = row[j];
       static_for<0, CT>([&](auto J) {
         constexpr int j = decltype(J)::value;
-        C acc = x[j];
+        C acc[4] = {x[j], mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};  // four partial sums: short chains
         static_for<0, j>([&](auto Kk) {  // acc -= x_k conj(L_jk)
           constexpr int k = decltype(Kk)::value;
-          const C l = D[j * LD + k];
-          acc.x -= x[k].x * l.x + x[k].y * l.y;
-          acc.y -= x[k].y * l.x - x[k].x * l.y;
+          const C l = lds_c<C>(sD + (uint32_t)((j * LD + k) * sizeof(C)));
+          acc[k & 3].x -= x[k].x * l.x + x[k].y * l.y;
+          acc[k & 3].y -= x[k].y * l.x - x[k].x * l.y;
         });
-        x[j] = cscale(acc, dinv[j]);
+        x[j] = cscale(cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])), dinv[j]);
       });
 #pragma unroll
       for (int j = 0; j < CT; ++j) {
@@ -212,13 +278,16 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>*
     }
     if (tid == 0) ctr = 0;
     __syncthreads();
+    if (prof && kb < 16) prof[3 + 4 * kb] = clock64();
     // ---- lookahead: A. the first 64 trailing columns (next diagonal tile + next panel) ----
     const int nb64 = (R + 63) / 64;
     for (int sidx = warp; sidx < nb64 * 8; sidx += NW) strip(r0, R, sidx >> 3, 0, sidx & 7);
     __syncthreads();
+    if (prof && kb < 16) prof[4 + 4 * kb] = clock64();
     // ---- B. warp 0 factors the next diagonal tile while the other warps take the rest of the
     // trailing update (64 x 64 block pairs with bj >= 1, 8 strips each, dynamic); warp 0 joins ----
     if (warp == 0) diag(kb + 1);
+    if (prof && kb < 16) prof[5 + 4 * kb] = clock64();
     const int nB = 8 * (nb64 * (nb64 - 1) / 2);
     for (;;) {
       int sidx = 0;
@@ -232,6 +301,7 @@ __global__ void __launch_bounds__(NT) k_chol_blocked(int K, int Kv, const cx<T>*
       strip(r0, R, b + 1, q - b * (b + 1) / 2 + 1, sidx & 7);
     }
     __syncthreads();
+    if (prof && kb < 16) prof[6 + 4 * kb] = clock64();
   }
 }
 
@@ -562,6 +632,12 @@ using namespace ocsc;
 // the factor of a K that is not a multiple of 32 is stored padded to the next multiple
 static int chol_order(int K) { return K % CT ? (K / CT + 1) * CT : K; }
 
+extern "C" int ocsc_debug_chol_profile(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  OCSC_CUDA(cudaMemcpyToSymbol(g_chol_prof, &p, sizeof(p)));
+  return OCSC_OK;
+}
+
 extern "C" size_t ocsc_history_factor_bytes(int dtype_hist, int K, int nfreq) {
   const size_t Kp = (size_t)chol_order(K);
   return (size_t)(dtype_hist == OCSC_F64 ? 16 : 8) * Kp * Kp * nfreq;
@@ -614,14 +690,21 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
   }
   (void)nb;
   const size_t smem = (dtype_hist == OCSC_F64 ? (size_t)chol_panel_offset<double>() : (size_t)chol_panel_offset<float>()) +
-                      cs * (size_t)CT * (K - CT + 64);  // L_kk + 1/L_jj + panel with slack
+                      cs * (size_t)CT * ((K - CT + 63) / 64 * 64);  // L_kk + 1/L_jj + panel with slack
   if (smem > 227 * 1024) return fail(OCSC_EARG, "history_factor: panel exceeds shared memory for this K/dtype");
-  if (dtype_hist == OCSC_F32 && K >= 384) {
+  // float: 512 threads (one CTA per SM) from K = 384; up to K = 288, 128-thread CTAs, three per SM (measured
+  // at K = 256: 19.0 ms with 128, 20.8 with 256, 30.3 with 512 threads); OCSC_CHOL_NT overrides
+  int nt = dtype_hist == OCSC_F32 ? (K >= 384 ? 512 : (K <= 288 ? 128 : 256)) : 256;
+  if (const char* e = getenv("OCSC_CHOL_NT")) nt = atoi(e);
+  if (dtype_hist == OCSC_F32 && nt == 512) {
     OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_chol_blocked<float, 512><<<nfreq, 512, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
-  } else if (dtype_hist == OCSC_F32) {
+  } else if (dtype_hist == OCSC_F32 && nt == 256) {
     OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_chol_blocked<float, 256><<<nfreq, 256, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
+  } else if (dtype_hist == OCSC_F32) {
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_chol_blocked<float, 128><<<nfreq, 128, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
   } else if (dtype_hist == OCSC_F64) {
     OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<double, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_chol_blocked<double, 256><<<nfreq, 256, smem, s>>>(K, Kv, (const double2*)S, ridge, (double2*)L, info);
