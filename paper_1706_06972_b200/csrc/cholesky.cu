@@ -77,6 +77,17 @@ __device__ __forceinline__ void sts_c(uint32_t a, float2 v) {
 __device__ __forceinline__ void sts_c(uint32_t a, double2 v) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
 }
+// predicated store (no branch around the volatile asm)
+__device__ __forceinline__ void sts_c_if(bool c, uint32_t a, float2 v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.shared.v2.f32 [%0], {%1, %2};\n}" ::"r"(a),
+               "f"(v.x), "f"(v.y), "r"((int)c)
+               : "memory");
+}
+__device__ __forceinline__ void sts_c_if(bool c, uint32_t a, double2 v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(a),
+               "d"(v.x), "d"(v.y), "r"((int)c)
+               : "memory");
+}
 
 // Cholesky of one CT x CT diagonal tile by one warp (lane = row), in place in shared memory
 // (sD: [CT][CT + 1] complex), the lower triangle read from and written back to `tile` (global,
@@ -110,14 +121,13 @@ __device__ __noinline__ void diag_tile(cx<T>* tile, int K, uint32_t sD, T* dinv,
       ljj = sqrt(d);
       inv = (T)1 / ljj;
     }
-    C lij = mkc<C>(0, 0);
     const uint32_t own = sD + (uint32_t)(lane * LD) * SZ;
-    if (lane > j) {
-      lij = cscale(lds_c<C>(own + j * SZ), inv);
-      sts_c(own + j * SZ, lij);
-    } else if (lane == j) {
-      sts_c(own + j * SZ, mkc<C>(ljj, (T)0));
-    }
+    // (loads are unconditional and stores predicated: no branches around the shared-memory asm; a
+    // row's entries past column 31 -- the pad column, the next row, after row 31 the dinv area --
+    // and the clamped rows only feed values that are never stored)
+    const C aij = lds_c<C>(own + j * SZ);
+    const C lij = lane > j ? cscale(aij, inv) : mkc<C>(0, 0);
+    sts_c_if(lane >= j, own + j * SZ, lane == j ? mkc<C>(ljj, (T)0) : lij);
     if (lane == 0) dinv[j] = inv;
     __syncwarp();
     // D[i][k] -= L[i][j] conj(L[k][j]),  j < k <= i: eight columns at a time, all sixteen loads
@@ -126,25 +136,25 @@ __device__ __noinline__ void diag_tile(cx<T>* tile, int K, uint32_t sD, T* dinv,
     for (int k0 = j + 1; k0 < CT; k0 += 8) {
       C lk[8], t[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        lk[u] = k0 + u < CT ? lds_c<C>(sD + (uint32_t)((k0 + u) * LD + j) * SZ) : mkc<C>(0, 0);
+      for (int u = 0; u < 8; ++u) lk[u] = lds_c<C>(sD + (uint32_t)(min(k0 + u, CT - 1) * LD + j) * SZ);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = k0 + u <= lane ? lds_c<C>(own + (k0 + u) * SZ) : mkc<C>(0, 0);
+      for (int u = 0; u < 8; ++u) t[u] = lds_c<C>(own + (k0 + u) * SZ);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         t[u].x -= lij.x * lk[u].x + lij.y * lk[u].y;
         t[u].y -= lij.y * lk[u].x - lij.x * lk[u].y;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (k0 + u <= lane) sts_c(own + (k0 + u) * SZ, t[u]);
+      for (int u = 0; u < 8; ++u) sts_c_if(k0 + u <= lane, own + (k0 + u) * SZ, t[u]);
     }
     __syncwarp();
   }
   C* out = tile + (int64_t)lane * K;
 #pragma unroll 8
-  for (int j = 0; j < CT; ++j)
-    if (j <= lane) out[j] = lds_c<C>(sD + (uint32_t)(lane * LD + j) * SZ);
+  for (int j = 0; j < CT; ++j) {
+    const C v = lds_c<C>(sD + (uint32_t)(lane * LD + j) * SZ);
+    if (j <= lane) out[j] = v;
+  }
 }
 
 // A (packed lower, K(K+1)/2 per frequency) + ridge I -> full-layout lower L = chol(A).
