@@ -38,15 +38,20 @@ __host__ __device__ constexpr int chol_panel_offset() {
   return (int)(((sizeof(cx<T>) * CT * (CT + 1) + sizeof(T) * (CT + 2)) + 15) / 16 * 16);
 }
 
-// four consecutive complex values from 16-byte aligned shared memory
-__device__ __forceinline__ void load4(const float2* p, float2 (&v)[4]) {
-  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
-  v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w); v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+// two consecutive complex values from 16-byte aligned shared memory (one 16-byte load for float)
+__device__ __forceinline__ void ld2(const float2* p, float2& a, float2& b) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  a = make_float2(v.x, v.y);
+  b = make_float2(v.z, v.w);
 }
-__device__ __forceinline__ void load4(const double2* p, double2 (&v)[4]) {
-#pragma unroll
-  for (int r = 0; r < 4; ++r) v[r] = p[r];
+__device__ __forceinline__ void ld2(const double2* p, double2& a, double2& b) {
+  a = p[0];
+  b = p[1];
 }
+// panel row position: inside each 32-row group, rows 4c + q (c = 0..7, q = 0..3) are stored as
+// [q = 0,1 of c = 0..7][q = 2,3 of c = 0..7], so four consecutive rows are two aligned pairs and the
+// same pair of eight consecutive c is 128 contiguous bytes (float)
+__device__ __forceinline__ int ppos(int r) { return (r & ~31) | (((r >> 1) & 1) << 4) | (((r >> 2) & 7) << 1) | (r & 1); }
 
 // acc += a * conj(b) on 2-wide FP32 (FFMA2) / FP64 pairs: acc += a * b.x + (a.y, -a.x) * b.y
 template <typename C>
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
   const int64_t npk = (int64_t)Kv * (Kv + 1) / 2;
   const C* Sp = S + (int64_t)p * npk;
   C* L = Lall + (int64_t)p * K * K;
-  const int PR = (K - CT + 63) / 64 * 64;  // panel row stride: K - CT rows rounded up to the 64-row blocks
+  const int PR = K - CT;  // panel row stride (k-major panel, rows pair-interleaved within 32-row groups)
   long long* prof = (blockIdx.x == 0 && threadIdx.x == 0) ? g_chol_prof : nullptr;
   if (prof) prof[0] = clock64();
 
@@ -216,42 +221,55 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
   auto diag = [&](int kbx) {
     diag_tile<T>(L + (int64_t)(kbx * CT) * K + kbx * CT, K, sD, dinv, lane, info, p);
   };
-  // ---- one warp's 8-row x 64-column strip of the trailing update A22 -= P P^H:
-  // 64 x 64 block pair (bi, bj), rows ty * 4.. of the pair with ty = 2 tp + lane / 16 ----
-  auto strip = [&](int r0, int R, int bi, int bj, int tp) {
-    const int ty = 2 * tp + (lane >> 4), tx = lane & 15;
-    const int i0 = bi * 64 + ty * 4, j0 = bj * 64 + tx * 4;  // trailing-local rows / cols
-    C acc[4][4], tgt[4][4];
+  // ---- one warp's 32 x 32 tile (ti, tj), ti >= tj, of the trailing update A22 -= P P^H: lane
+  // (ry, cx) = (lane / 8, lane % 8) owns rows 8 ry.. 8 ry + 7 and columns 4 cx.. 4 cx + 3 (8 x 4
+  // complex accumulators, two 2-wide FMAs per complex multiply-add); per k the eight lanes of a
+  // quarter-warp read one broadcast 16-byte pair of the row operand and eight consecutive pairs
+  // of the column operand (the pair-interleaved panel layout, ppos), so every shared load is one
+  // wavefront; the targets are read-modified-written once, coalesced, after the k loop ----
+  auto tile_upd = [&](int r0, int ti, int tj) {
+    const int ry = lane >> 3, cx = lane & 7;
+    C acc[8][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {  // targets load while the products accumulate from zero
-        const int i = i0 + r, j = j0 + q;
-        tgt[r][q] = (i < R && j <= i) ? L[(int64_t)(r0 + i) * K + r0 + j] : mkc<C>(0, 0);
-        acc[r][q] = mkc<C>(0, 0);
-      }
-    if (i0 < R && j0 <= i0 + 3) {
-#pragma unroll 4
-      for (int k = 0; k < CT; ++k) {
-        // rows past R read panel slack: they only feed outputs that are never stored
-        C zi[4], zs[4], zj[4];
-        load4(PT + k * PR + i0, zi);
-        load4(PT + k * PR + j0, zj);
+      for (int q = 0; q < 4; ++q) acc[r][q] = mkc<C>(0, 0);
+    const C* pi = PT + ti * CT + 4 * ry;
+    const C* pj = PT + tj * CT + 2 * cx;
+#pragma unroll 2
+    for (int k = 0; k < CT; ++k) {
+      C zi[8], zj[4];
+      ld2(pi + k * PR, zi[0], zi[1]);            // rows 8 ry + 0, 1
+      ld2(pi + k * PR + 16, zi[2], zi[3]);       //            2, 3
+      ld2(pi + k * PR + 2, zi[4], zi[5]);        //            4, 5
+      ld2(pi + k * PR + 18, zi[6], zi[7]);       //            6, 7
+      ld2(pj + k * PR, zj[0], zj[1]);            // columns 4 cx + 0, 1
+      ld2(pj + k * PR + 16, zj[2], zj[3]);       //                2, 3
+      // acc += zi conj(zj) = zi * zj.x + swap(zi) * (zj.y, -zj.y): the swap is an operand swizzle of
+      // the 2-wide FMA, so a complex multiply-add is two FFMA2 and the sign vector costs one op per zj
+      C zn[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) zs[r] = mkc<C>(zi[r].y, -zi[r].x);
+      for (int q = 0; q < 4; ++q) zn[q] = mkc<C>(zj[q].y, -zj[q].y);
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < 8; ++r)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) cmac_conj2(acc[r][q], zi[r], zs[r], -zj[q].x, -zj[q].y);
-      }
+        for (int q = 0; q < 4; ++q) {
+          acc[r][q] = vfma(zi[r], vsplat<C>(zj[q].x), acc[r][q]);
+          acc[r][q] = vfma(vswap(zi[r]), zn[q], acc[r][q]);
+        }
     }
+    const int j0 = tj * CT + 4 * cx;
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < 8; ++r) {
+      const int i = ti * CT + 8 * ry + r;
+      C* dst = L + (int64_t)(r0 + i) * K + r0 + j0;
+      C t[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int i = i0 + r, j = j0 + q;
-        if (i < R && j <= i) L[(int64_t)(r0 + i) * K + r0 + j] = cadd(tgt[r][q], acc[r][q]);
-      }
+      for (int q = 0; q < 4; ++q) t[q] = j0 + q <= i ? dst[q] : mkc<C>(0, 0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j0 + q <= i) dst[q] = csub(t[q], acc[r][q]);
+    }
   };
   constexpr int NW = NT / 32;
   __shared__ int ctr;
@@ -283,32 +301,31 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
 #pragma unroll
       for (int j = 0; j < CT; ++j) {
         row[j] = x[j];
-        PT[j * PR + rr] = x[j];
+        PT[j * PR + ppos(rr)] = x[j];
       }
     }
     if (tid == 0) ctr = 0;
     __syncthreads();
     if (prof && kb < 16) prof[3 + 4 * kb] = clock64();
-    // ---- lookahead: A. the first 64 trailing columns (next diagonal tile + next panel) ----
-    const int nb64 = (R + 63) / 64;
-    for (int sidx = warp; sidx < nb64 * 8; sidx += NW) strip(r0, R, sidx >> 3, 0, sidx & 7);
+    // ---- lookahead: A. the first trailing tile column (next diagonal tile + next panel) ----
+    const int nbr = R / CT;
+    for (int t = warp; t < nbr; t += NW) tile_upd(r0, t, 0);
     __syncthreads();
     if (prof && kb < 16) prof[4 + 4 * kb] = clock64();
     // ---- B. warp 0 factors the next diagonal tile while the other warps take the rest of the
-    // trailing update (64 x 64 block pairs with bj >= 1, 8 strips each, dynamic); warp 0 joins ----
+    // trailing update (tiles (ti, tj), 1 <= tj <= ti, dynamic); warp 0 joins ----
     if (warp == 0) diag(kb + 1);
     if (prof && kb < 16) prof[5 + 4 * kb] = clock64();
-    const int nB = 8 * (nb64 * (nb64 - 1) / 2);
+    const int nB = (nbr - 1) * nbr / 2;
     for (;;) {
-      int sidx = 0;
-      if (lane == 0) sidx = atomicAdd(&ctr, 1);
-      sidx = __shfl_sync(0xffffffffu, sidx, 0);
-      if (sidx >= nB) break;
-      const int q = sidx >> 3;
+      int q = 0;
+      if (lane == 0) q = atomicAdd(&ctr, 1);
+      q = __shfl_sync(0xffffffffu, q, 0);
+      if (q >= nB) break;
       int b = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
       while (b * (b + 1) / 2 > q) --b;
       while ((b + 1) * (b + 2) / 2 <= q) ++b;
-      strip(r0, R, b + 1, q - b * (b + 1) / 2 + 1, sidx & 7);
+      tile_upd(r0, b + 1, q - b * (b + 1) / 2 + 1);
     }
     __syncthreads();
     if (prof && kb < 16) prof[6 + 4 * kb] = clock64();
@@ -700,7 +717,7 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
   }
   (void)nb;
   const size_t smem = (dtype_hist == OCSC_F64 ? (size_t)chol_panel_offset<double>() : (size_t)chol_panel_offset<float>()) +
-                      cs * (size_t)CT * ((K - CT + 63) / 64 * 64);  // L_kk + 1/L_jj + panel with slack
+                      cs * (size_t)CT * (K - CT);  // L_kk + 1/L_jj + panel
   if (smem > 227 * 1024) return fail(OCSC_EARG, "history_factor: panel exceeds shared memory for this K/dtype");
   // float: 512 threads (one CTA per SM) from K = 384; up to K = 288, 128-thread CTAs, three per SM (measured
   // at K = 256: 19.0 ms with 128, 20.8 with 256, 30.3 with 512 threads); OCSC_CHOL_NT overrides
