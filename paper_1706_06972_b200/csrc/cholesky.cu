@@ -289,14 +289,16 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
       for (int j = 0; j < CT; ++j) x[j] = row[j];
       static_for<0, CT>([&](auto J) {
         constexpr int j = decltype(J)::value;
-        C acc[4] = {x[j], mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};  // four partial sums: short chains
-        static_for<0, j>([&](auto Kk) {  // acc -= x_k conj(L_jk)
+        // acc -= x_k conj(L_jk) = x_k (-l.x) + swap(x_k) (-l.y, l.y): two 2-wide FMAs (the swap and
+        // the signs are FFMA2 operand modifiers); two partial sums keep the chains short
+        C acc[2] = {x[j], mkc<C>(0, 0)};
+        static_for<0, j>([&](auto Kk) {
           constexpr int k = decltype(Kk)::value;
           const C l = lds_c<C>(sD + (uint32_t)((j * LD + k) * sizeof(C)));
-          acc[k & 3].x -= x[k].x * l.x + x[k].y * l.y;
-          acc[k & 3].y -= x[k].y * l.x - x[k].x * l.y;
+          acc[k & 1] = vfma(x[k], vsplat<C>(-l.x), acc[k & 1]);
+          acc[k & 1] = vfma(vswap(x[k]), mkc<C>(-l.y, l.y), acc[k & 1]);
         });
-        x[j] = cscale(cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3])), dinv[j]);
+        x[j] = cscale(vadd(acc[0], acc[1]), dinv[j]);
       });
 #pragma unroll
       for (int j = 0; j < CT; ++j) {
