@@ -229,6 +229,14 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
   // wavefront; the targets are read-modified-written once, coalesced, after the k loop ----
   auto tile_upd = [&](int r0, int ti, int tj) {
     const int ry = lane >> 3, cx = lane & 7;
+    const int j0 = tj * CT + 4 * cx;
+    // the targets come from DRAM (the factors of the frequencies in flight exceed L2): ask for
+    // them now, read them after the k loop
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const C* t = L + (int64_t)(r0 + ti * CT + 8 * ry + r) * K + r0 + j0;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(t));
+    }
     C acc[8][4];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -258,7 +266,6 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
           acc[r][q] = vfma(vswap(zi[r]), zn[q], acc[r][q]);
         }
     }
-    const int j0 = tj * CT + 4 * cx;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int i = ti * CT + 8 * ry + r;
@@ -309,25 +316,32 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
     if (tid == 0) ctr = 0;
     __syncthreads();
     if (prof && kb < 16) prof[3 + 4 * kb] = clock64();
-    // ---- lookahead: A. the first trailing tile column (next diagonal tile + next panel) ----
+    // ---- trailing update, one dynamic queue of 32 x 32 tiles: first the next tile column (tiles
+    // (ti, 0): the next diagonal tile and panel -- the lookahead), then the rest (tiles (ti, tj),
+    // 1 <= tj <= ti).  The warp that finishes tile (0, 0) factors the next diagonal tile at once
+    // and then rejoins the queue; the end-of-step barrier orders everything for the next panel ----
     const int nbr = R / CT;
-    for (int t = warp; t < nbr; t += NW) tile_upd(r0, t, 0);
-    __syncthreads();
+    const int nT = nbr * (nbr + 1) / 2;
     if (prof && kb < 16) prof[4 + 4 * kb] = clock64();
-    // ---- B. warp 0 factors the next diagonal tile while the other warps take the rest of the
-    // trailing update (tiles (ti, tj), 1 <= tj <= ti, dynamic); warp 0 joins ----
-    if (warp == 0) diag(kb + 1);
-    if (prof && kb < 16) prof[5 + 4 * kb] = clock64();
-    const int nB = (nbr - 1) * nbr / 2;
     for (;;) {
       int q = 0;
       if (lane == 0) q = atomicAdd(&ctr, 1);
       q = __shfl_sync(0xffffffffu, q, 0);
-      if (q >= nB) break;
-      int b = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
-      while (b * (b + 1) / 2 > q) --b;
-      while ((b + 1) * (b + 2) / 2 <= q) ++b;
-      tile_upd(r0, b + 1, q - b * (b + 1) / 2 + 1);
+      if (q >= nT) break;
+      if (q < nbr) {
+        tile_upd(r0, q, 0);
+        if (q == 0) {
+          __syncwarp();
+          diag(kb + 1);
+          if (prof && kb < 16) prof[5 + 4 * kb] = clock64();
+        }
+      } else {
+        const int qb = q - nbr;
+        int b = (int)((sqrtf(8.0f * qb + 1.0f) - 1.0f) * 0.5f);
+        while (b * (b + 1) / 2 > qb) --b;
+        while ((b + 1) * (b + 2) / 2 <= qb) ++b;
+        tile_upd(r0, b + 1, qb - b * (b + 1) / 2 + 1);
+      }
     }
     __syncthreads();
     if (prof && kb < 16) prof[6 + 4 * kb] = clock64();
