@@ -23,8 +23,8 @@ using sfft::static_for;
 constexpr int CT = 32;  // tile edge
 
 // optional phase stamps of CTA 0 (development aid): [0] start, [1] after the expansion, [2] after
-// diag(0), then per step kb: [3+4kb] panel done, [4+4kb] strips A done, [5+4kb] warp 0's diagonal
-// done, [6+4kb] step done (clock64)
+// diag(0), then per step kb: [3+4kb] panel done, [4+4kb] trailing queue start, [5+4kb] next
+// diagonal tile factored, [6+4kb] step done (clock64)
 __device__ long long* g_chol_prof = nullptr;
 
 template <typename C>
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
         if (q == 0) {
           __syncwarp();
           diag(kb + 1);
-          if (prof && kb < 16) prof[5 + 4 * kb] = clock64();
+          if (blockIdx.x == 0 && lane == 0 && g_chol_prof && kb < 16) g_chol_prof[5 + 4 * kb] = clock64();
         }
       } else {
         const int qb = q - nbr;

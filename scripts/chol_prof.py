@@ -34,8 +34,8 @@ for K in [int(a) for a in sys.argv[1:]] or [256, 512]:
     prev = t[2]
     for kb in range(nb - 1):
         a, b_, c, d = t[3 + 4 * kb: 7 + 4 * kb]
-        print(f"  kb={kb:2d} R={K - 32 * (kb + 1):3d}: panel {a - prev:7d}  stripsA {b_ - a:7d}  diag(w0) {c - b_:7d}  "
-              f"stripsB {d - b_:7d}  step {d - prev:7d}")
+        print(f"  kb={kb:2d} R={K - 32 * (kb + 1):3d}: panel {a - prev:7d}  next diagonal done {c - b_:7d}  "
+              f"trailing {d - b_:7d}  step {d - prev:7d}")
         prev = d
     del z, x, h
     torch.cuda.empty_cache()
