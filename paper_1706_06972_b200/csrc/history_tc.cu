@@ -108,9 +108,38 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
   const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TB >> 3) << 17) | ((uint32_t)(TB >> 4) << 24);
   const uint32_t idesc_neg = idesc | (1u << 13);  // negate A
 
+  // the epilogue read-modify-writes this block of S (DRAM-resident): ask L2 for its rows now, so
+  // the staging and the MMAs run while they arrive (128-byte lines; a row of the block is
+  // TB complex = 1 KB (float) / 2 KB (double) of the packed triangle)
+  {
+    const int64_t npk_ = (int64_t)K * (K + 1) / 2;
+    constexpr int LINES = TB * (int)sizeof(cx<Th>) / 128;  // lines per block row
+    for (int e = tid; e < TB * LINES; e += 256) {
+      const int rr = e / LINES, ln = e - rr * LINES, row = I * TB + rr, col = J * TB + ln * (128 / (int)sizeof(cx<Th>));
+      if (row < K && col <= row)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(S + (int64_t)p * npk_ + packed_index(row, col)));
+    }
+  }
   float2 cacc = make_float2(0.f, 0.f);
   uint32_t phase[2] = {0, 0};
   const int nchunk = (B + TKC - 1) / TKC;
+  // raw code values of a chunk, loaded one chunk ahead (the loads of chunk ch + 1 are in flight
+  // while chunk ch is converted, staged and issued)
+  float2 rvi[TKC / 2], rvj[TKC / 2];
+  auto load_raw = [&](int ch) {
+#pragma unroll
+    for (int s4 = 0; s4 < TKC / 2; ++s4) {
+      const int b = ch * TKC + thalf * (TKC / 2) + s4;
+      rvi[s4] = make_float2(0.f, 0.f);
+      rvj[s4] = make_float2(0.f, 0.f);
+      if (b < B) {
+        const int64_t base = (int64_t)b * z_sb + (int64_t)p * z_sp;
+        if (ri < K) rvi[s4] = z[base + (int64_t)ri * z_sk];
+        if (!diag && rj < K) rvj[s4] = z[base + (int64_t)rj * z_sk];
+      }
+    }
+  };
+  load_raw(0);
   for (int ch = 0; ch < nchunk; ++ch) {
     const int buf = ch & 1;
     if (ch >= 2) {  // the MMAs of chunk ch-2 read this buffer: wait for their commit
@@ -127,16 +156,11 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
 #pragma unroll
       for (int s4 = 0; s4 < TKC / 2; ++s4) {
         const int b = b0 + thalf * (TKC / 2) + s4;
-        float2 vi = make_float2(0.f, 0.f), vj = make_float2(0.f, 0.f);
-        if (b < B) {
-          const int64_t base = (int64_t)b * z_sb + (int64_t)p * z_sp;
-          if (ri < K) vi = z[base + (int64_t)ri * z_sk];
-          if (!diag && rj < K) vj = z[base + (int64_t)rj * z_sk];
-          if (diag && ri < K) {  // cross term c_i += conj(x_b) z_bi on CUDA cores
-            const float2 xb = x[(int64_t)b * x_sb + (int64_t)p * x_sp];
-            cacc.x += xb.x * vi.x + xb.y * vi.y;
-            cacc.y += xb.x * vi.y - xb.y * vi.x;
-          }
+        const float2 vi = rvi[s4], vj = rvj[s4];
+        if (diag && b < B && ri < K) {  // cross term c_i += conj(x_b) z_bi on CUDA cores
+          const float2 xb = x[(int64_t)b * x_sb + (int64_t)p * x_sp];
+          cacc.x += xb.x * vi.x + xb.y * vi.y;
+          cacc.y += xb.x * vi.y - xb.y * vi.x;
         }
         xh[s4] = to_tf32(vi.x);
         xl[s4] = to_tf32(vi.x - __uint_as_float(xh[s4]));
@@ -147,6 +171,7 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
         jyh[s4] = to_tf32(vj.y);
         jyl[s4] = to_tf32(vj.y - __uint_as_float(jyh[s4]));
       }
+      if (ch + 1 < nchunk) load_raw(ch + 1);
       const uint32_t off = thalf * (TB * 4) + trow * 4;  // word offset of the k-unit inside a tile
       auto st4 = [&](int tile, const uint32_t (&v)[4]) {
         *reinterpret_cast<uint4*>(Tb + tile * TILE_WORDS + off) = make_uint4(v[0], v[1], v[2], v[3]);
