@@ -479,6 +479,9 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
   const double2* Ap = inv_in + (int64_t)p * npk;
   for (int64_t e = tid; e < npk; e += nt) cp_async<16>(A + e, Ap + e);  // all in flight at once
   cp_async_commit();
+  if (S)  // the final phase read-modify-writes this frequency's S: bring it into L2 meanwhile
+    for (int64_t l = tid; l < (npk * 16 + 127) / 128; l += nt)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(S + (int64_t)p * npk) + l * 128));
   for (int e = tid; e < K * nb; e += nt) {
     const int k = e / nb, j = e - k * nb;
     const auto v = z[j * zb + k * zk + p * zp];
@@ -583,6 +586,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
   for (int i = warp; i < K; i += nw)
     for (int j = lane; j <= i; j += 32) {  // out[i][j] = A^-1[i][j] - sum_m X[i][m] conj(W[j][m])
+      C sv = Sp ? Sp[packed_index(i, j)] : make_double2(0, 0);  // (issued first: its latency overlaps)
       C acc = A[packed_index(i, j)];
       for (int m = 0; m < nb; ++m) {
         const C x = X[i * nbp + m], w = Wm[j * nbp + m];
@@ -591,7 +595,6 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
       }
       o[packed_index(i, j)] = ccast<To>(acc);
       if (Sp) {  // S_p[i][j] += sum_m U[i][m] conj(U[j][m])
-        C sv = Sp[packed_index(i, j)];
         for (int m = 0; m < nb; ++m) {
           const C ui = U[i * nbp + m], uj = U[j * nbp + m];
           sv.x += ui.x * uj.x + ui.y * uj.y;
