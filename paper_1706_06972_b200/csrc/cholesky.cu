@@ -34,8 +34,9 @@ __device__ __forceinline__ C* tile_ptr(C* L, int K, int ib, int jb) {
 
 template <typename T>
 __host__ __device__ constexpr int chol_panel_offset() {
-  // L_kk [CT][CT+1] complex + 1/L_jj [CT] real, rounded up to 16 bytes
-  return (int)(((sizeof(cx<T>) * CT * (CT + 1) + sizeof(T) * (CT + 2)) + 15) / 16 * 16);
+  // L_kk [CT + 8][CT+1] complex (8 padding rows read by the diagonal factor's unrolled groups) +
+  // 1/L_jj [CT] real, rounded up to 16 bytes
+  return (int)(((sizeof(cx<T>) * (CT + 8) * (CT + 1) + sizeof(T) * (CT + 2)) + 15) / 16 * 16);
 }
 
 // two consecutive complex values from 16-byte aligned shared memory (one 16-byte load for float)
@@ -95,12 +96,13 @@ __device__ __forceinline__ void sts_c_if(bool c, uint32_t a, double2 v) {
 }
 
 // Cholesky of one CT x CT diagonal tile by one warp (lane = row), in place in shared memory
-// (sD: [CT][CT + 1] complex), the lower triangle read from and written back to `tile` (global,
+// (sD: [CT + 8][CT + 1] complex, the last 8 rows padding), the lower triangle read from and written back to `tile` (global,
 // row stride K); 1 / L_jj into dinv.  Right-looking, one column per step: every lane reads the
 // pivot (broadcast), the rows below scale their entry of column j, then update their row of the
 // trailing triangle from the column (broadcast reads).  Rolled loops keep the routine small: it
-// runs once per tile column on the critical path, beside the trailing update of the other warps
-// (a register-resident, fully unrolled variant measured 2x slower: spills and code size).
+// runs once per tile column on the critical path, beside the trailing update of the other warps.
+// (A register-resident, fully unrolled variant is faster alone -- 13.6 k against 21.4 k cycles per
+// tile, scripts/diag_bench.cu -- but spills inside this kernel's 128-register budget.)
 template <typename T>
 __device__ __noinline__ void diag_tile(cx<T>* tile, int K, uint32_t sD, T* dinv, int lane, int32_t* info, int p) {
   using C = cx<T>;
@@ -128,8 +130,8 @@ __device__ __noinline__ void diag_tile(cx<T>* tile, int K, uint32_t sD, T* dinv,
     }
     const uint32_t own = sD + (uint32_t)(lane * LD) * SZ;
     // (loads are unconditional and stores predicated: no branches around the shared-memory asm; a
-    // row's entries past column 31 -- the pad column, the next row, after row 31 the dinv area --
-    // and the clamped rows only feed values that are never stored)
+    // row's entries past column 31 -- the pad column, the next row -- and the rows past 31 -- the
+    // tile's 8 padding rows -- only feed values that are never stored)
     const C aij = lds_c<C>(own + j * SZ);
     const C lij = lane > j ? cscale(aij, inv) : mkc<C>(0, 0);
     sts_c_if(lane >= j, own + j * SZ, lane == j ? mkc<C>(ljj, (T)0) : lij);
@@ -137,20 +139,23 @@ __device__ __noinline__ void diag_tile(cx<T>* tile, int K, uint32_t sD, T* dinv,
     __syncwarp();
     // D[i][k] -= L[i][j] conj(L[k][j]),  j < k <= i: eight columns at a time, all sixteen loads
     // issued before the first store (the shared-memory asm keeps program order)
+    // (t -= lij conj(lk) as two 2-wide FMAs: t + lij (-lk.x) + swap(lij) (-lk.y, lk.y); addresses are
+    // a per-group base plus immediates)
 #pragma unroll 1
     for (int k0 = j + 1; k0 < CT; k0 += 8) {
+      const uint32_t colk = sD + (uint32_t)(k0 * LD + j) * SZ, rowk = own + k0 * SZ;
       C lk[8], t[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) lk[u] = lds_c<C>(sD + (uint32_t)(min(k0 + u, CT - 1) * LD + j) * SZ);
+      for (int u = 0; u < 8; ++u) lk[u] = lds_c<C>(colk + u * LD * SZ);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = lds_c<C>(own + (k0 + u) * SZ);
+      for (int u = 0; u < 8; ++u) t[u] = lds_c<C>(rowk + u * SZ);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        t[u].x -= lij.x * lk[u].x + lij.y * lk[u].y;
-        t[u].y -= lij.y * lk[u].x - lij.x * lk[u].y;
+        t[u] = vfma(lij, vsplat<C>(-lk[u].x), t[u]);
+        t[u] = vfma(vswap(lij), mkc<C>(-lk[u].y, lk[u].y), t[u]);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) sts_c_if(k0 + u <= lane, own + (k0 + u) * SZ, t[u]);
+      for (int u = 0; u < 8; ++u) sts_c_if(k0 + u <= lane, rowk + u * SZ, t[u]);
     }
     __syncwarp();
   }
@@ -181,7 +186,7 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int LD = CT + 1;
   C* D = reinterpret_cast<C*>(smem_raw);  // L_kk [CT][LD]
-  T* dinv = reinterpret_cast<T*>(D + CT * LD);   // 1 / L_jj [CT]
+  T* dinv = reinterpret_cast<T*>(D + (CT + 8) * LD);  // 1 / L_jj [CT] (after the padded tile)
   C* PT = reinterpret_cast<C*>(smem_raw + chol_panel_offset<T>());  // panel, k-major: PT[k][r]
   const uint32_t sD = (uint32_t)__cvta_generic_to_shared(D);
   const int nb = K / CT;
@@ -278,7 +283,6 @@ __global__ void __launch_bounds__(NT, (sizeof(T) == 8 || NT >= 512) ? 1 : (NT >=
         if (j0 + q <= i) dst[q] = csub(t[q], acc[r][q]);
     }
   };
-  constexpr int NW = NT / 32;
   __shared__ int ctr;
 
   if (warp == 0) diag(0);
