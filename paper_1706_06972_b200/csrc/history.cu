@@ -458,8 +458,11 @@ static size_t csize(int dtype) { return dtype == OCSC_F64 ? 16 : 8; }
 // Low-rank refresh of a packed Hermitian inverse (Woodbury):
 //   (A + U U^H)^-1 = A^-1 - W (I + U^H W)^-1 W^H,  W = A^-1 U,  U = the nb new code spectra (K x nb)
 // One CTA per frequency; A^-1 (packed, f64) is staged in shared memory, the nb x nb capacitance
-// matrix is inverted by one thread (nb is a mini-batch remainder, <= 32).  Lets the trainer
-// invert S + (most of the batch) while the rest of the batch is still being coded.
+// matrix is inverted by one warp (nb is a mini-batch remainder, <= 16).  Lets the trainer
+// invert S + (most of the batch) while the rest of the batch is still being coded.  Shared
+// memory: A^-1, U in the codes' own precision, W, the capacitance and one row of X = W C^-1 per
+// warp (formed where the output phase needs it): K = 100 with nb <= 11 stays under 113 KB, so two
+// CTAs share an SM (config 1: nb = 9, config 2: nb = 10).
 template <typename Tz, typename To>
 __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const double2* __restrict__ inv_in,
                                                          const typename Cx<Tz>::type* __restrict__ z, int64_t zb,
@@ -471,11 +474,13 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
   const int p = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const int64_t npk = (int64_t)K * (K + 1) / 2;
   const int nbp = nb | 1;  // odd row pitch (complex): lanes along K hit distinct bank groups
+  using CZ = typename Cx<Tz>::type;
   C* A = reinterpret_cast<C*>(smraw);  // packed A^-1
-  C* U = A + npk;                      // [K][nbp]
-  C* Wm = U + K * nbp;                 // [K][nbp]  W = A^-1 U
-  C* X = Wm + K * nbp;                 // [K][nbp]  X = W Cinv
-  C* Cm = X + K * nbp;                 // [nb][nb] capacitance, inverted in place
+  C* Wm = A + npk;                     // [K][nbp]  W = A^-1 U
+  C* Cm = Wm + K * nbp;                // [nb][nb] capacitance, inverted in place
+  C* Xr = Cm + nb * nb;                // [16 warps][16] the output phase's row of X = W Cinv
+  CZ* U = reinterpret_cast<CZ*>(Xr + 16 * 16);  // [K][nbp] the new codes, own precision
+  auto up = [](CZ v) { return make_double2((double)v.x, (double)v.y); };
   const double2* Ap = inv_in + (int64_t)p * npk;
   for (int64_t e = tid; e < npk; e += nt) cp_async<16>(A + e, Ap + e);  // all in flight at once
   cp_async_commit();
@@ -484,8 +489,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
       asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(S + (int64_t)p * npk) + l * 128));
   for (int e = tid; e < K * nb; e += nt) {
     const int k = e / nb, j = e - k * nb;
-    const auto v = z[j * zb + k * zk + p * zp];
-    U[k * nbp + j] = make_double2((double)v.x, (double)v.y);
+    U[k * nbp + j] = z[j * zb + k * zk + p * zp];
   }
   cp_async_wait<0>();
   __syncthreads();
@@ -497,19 +501,19 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
     const C* row = A + packed_index(t, 0);
     int k = 0;
     for (; k + 1 <= t; k += 2) {
-      cfma(a0, row[k], U[k * nbp + j]);
-      cfma(a1, row[k + 1], U[(k + 1) * nbp + j]);
+      cfma(a0, row[k], up(U[k * nbp + j]));
+      cfma(a1, row[k + 1], up(U[(k + 1) * nbp + j]));
     }
-    if (k <= t) cfma(a0, row[k], U[k * nbp + j]);
+    if (k <= t) cfma(a0, row[k], up(U[k * nbp + j]));
     int i = t + 1;
     int64_t q = packed_index(i, t);  // packed (i, t): advances by i + 1 per row
     for (; i + 1 < K; i += 2) {
-      cfma(a0, cconj(A[q]), U[i * nbp + j]);
+      cfma(a0, cconj(A[q]), up(U[i * nbp + j]));
       q += i + 1;
-      cfma(a1, cconj(A[q]), U[(i + 1) * nbp + j]);
+      cfma(a1, cconj(A[q]), up(U[(i + 1) * nbp + j]));
       q += i + 2;
     }
-    if (i < K) cfma(a0, cconj(A[q]), U[i * nbp + j]);
+    if (i < K) cfma(a0, cconj(A[q]), up(U[i * nbp + j]));
     Wm[t * nbp + j] = make_double2(a0.x + a1.x, a0.y + a1.y);
   }
   __syncthreads();
@@ -519,7 +523,7 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
       const int a = e / nb, b = e - a * nb;
       double ax = 0, ay = 0;
       for (int k = lane; k < K; k += 32) {
-        const C u = U[k * nbp + a], w = Wm[k * nbp + b];
+        const C u = up(U[k * nbp + a]), w = Wm[k * nbp + b];
         ax += u.x * w.x + u.y * w.y;  // conj(u) w
         ay += u.x * w.y - u.y * w.x;
       }
@@ -562,19 +566,12 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
     }
   }
   __syncthreads();
-  for (int e = tid; e < K * nb; e += nt) {  // X = W Cinv
-    const int i = e / nb, j = e - i * nb;
-    C acc = make_double2(0, 0);
-    for (int m = 0; m < nb; ++m) cfma(acc, Wm[i * nbp + m], Cm[m * nb + j]);
-    X[i * nbp + j] = acc;
-  }
-  __syncthreads();
   if (S) {  // fold the same samples into the history sums: c_p += sum_b conj(x_b) z_b
     for (int k = tid; k < K; k += nt) {
       C acc = cvec[(int64_t)p * K + k];
       for (int m = 0; m < nb; ++m) {
         const auto xv = x[m * xb + p * xp];
-        const C u = U[k * nbp + m];
+        const C u = up(U[k * nbp + m]);
         acc.x += (double)xv.x * u.x + (double)xv.y * u.y;
         acc.y += (double)xv.x * u.y - (double)xv.y * u.x;
       }
@@ -584,30 +581,41 @@ __global__ void __launch_bounds__(512, 2) k_hist_woodbury(int K, int nb, const d
   double2* Sp = S ? S + (int64_t)p * npk : nullptr;
   typename Cx<To>::type* o = out + (int64_t)p * npk;
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  for (int i = warp; i < K; i += nw)
+  C* xr = Xr + warp * 16;
+  for (int i = warp; i < K; i += nw) {
+    if (lane < nb) {  // row i of X = W Cinv
+      C acc = make_double2(0, 0);
+      for (int m = 0; m < nb; ++m) cfma(acc, Wm[i * nbp + m], Cm[m * nb + lane]);
+      xr[lane] = acc;
+    }
+    __syncwarp();
     for (int j = lane; j <= i; j += 32) {  // out[i][j] = A^-1[i][j] - sum_m X[i][m] conj(W[j][m])
       C sv = Sp ? Sp[packed_index(i, j)] : make_double2(0, 0);  // (issued first: its latency overlaps)
       C acc = A[packed_index(i, j)];
       for (int m = 0; m < nb; ++m) {
-        const C x = X[i * nbp + m], w = Wm[j * nbp + m];
+        const C x = xr[m], w = Wm[j * nbp + m];
         acc.x -= x.x * w.x + x.y * w.y;
         acc.y -= x.y * w.x - x.x * w.y;
       }
       o[packed_index(i, j)] = ccast<To>(acc);
       if (Sp) {  // S_p[i][j] += sum_m U[i][m] conj(U[j][m])
         for (int m = 0; m < nb; ++m) {
-          const C ui = U[i * nbp + m], uj = U[j * nbp + m];
+          const C ui = up(U[i * nbp + m]), uj = up(U[j * nbp + m]);
           sv.x += ui.x * uj.x + ui.y * uj.y;
           sv.y += ui.y * uj.x - ui.x * uj.y;
         }
         Sp[packed_index(i, j)] = sv;
       }
     }
+    __syncwarp();  // xr is rewritten for the next row
+  }
 }
 
-extern "C" size_t ocsc_history_woodbury_smem(int K, int nb) {
-  return sizeof(double2) * ((size_t)K * (K + 1) / 2 + 3 * (size_t)K * (nb | 1) + (size_t)nb * nb);
+static size_t woodbury_smem(int K, int nb, size_t zsize) {
+  return sizeof(double2) * ((size_t)K * (K + 1) / 2 + (size_t)K * (nb | 1) + (size_t)nb * nb + 16 * 16) +
+         zsize * (size_t)K * (nb | 1);
 }
+extern "C" size_t ocsc_history_woodbury_smem(int K, int nb) { return woodbury_smem(K, nb, 16); }
 
 extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfreq, int nb, const void* inv_in,
                                      const void* z, int64_t z_sb, int64_t z_sk, int64_t z_sp, void* out,
@@ -618,7 +626,7 @@ extern "C" int ocsc_history_woodbury(int dtype_z, int dtype_out, int K, int nfre
   cudaStream_t s = as_stream(stream);
   OCSC_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
   if (nfreq == 0) return OCSC_OK;
-  const size_t sm = ocsc_history_woodbury_smem(K, nb);
+  const size_t sm = woodbury_smem(K, nb, dtype_z == OCSC_F32 ? 8 : 16);
   if (sm > 227 * 1024) return fail(OCSC_EARG, "history_woodbury: K too large for the shared-memory inverse");
 #define OCSC_WB(TZ, TO)                                                                                        \
   do {                                                                                                         \

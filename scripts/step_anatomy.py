@@ -1,7 +1,7 @@
-"""Anatomy of one config-1 training step (dev aid): trainer marks (CUDA events) relative to the
-step start, with the divergence check on (the API default) and off.
+"""Anatomy of one training step of a BASELINE config (dev aid): trainer marks (CUDA events)
+relative to the step start, with the divergence check on (the API default) and off.
 
-python scripts/step_anatomy.py
+python scripts/step_anatomy.py [config]   (1: 42x42 K=100 B=50; 2: 100x100 K=100 B=10)
 """
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -9,12 +9,14 @@ import numpy as np, torch
 import paper_1706_06972_b200 as ob
 from paper_1706_06972_b200.workloads import CONFIGS, synth_images
 
-c = CONFIGS[1]
-B = 50
+cid = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+c = CONFIGS[cid]
+B = c["B"]
 X = torch.as_tensor(synth_images(8 * B, c["dims0"], c["grid"], c["K0"], seed=1).reshape(8, B, -1).astype(np.float32)).cuda()
 for check in (True, False):
     tr = ob.OnlineTrainer(ob.SignalShape(c["grid"], (11, 11)),
-                          ob.TrainConfig(n_filters=100, dtype="float32", batch_size=B, stop_tol=0.0, rho_dict=1.0))
+                          ob.TrainConfig(n_filters=c["K"], beta=c["beta"], dtype="float32", batch_size=B, stop_tol=0.0,
+                                         rho_dict=1.0))
     for m in range(3):
         tr.partial_fit(X[m], check=check)
     torch.cuda.synchronize()
