@@ -223,8 +223,10 @@ def test_overlap_entry_points_validate_on_the_host():
     assert lib.ocsc_history_woodbury(4, 8, 40, 3, 17, None, None, 0, 0, 0, None, None, None, 0, 0, None, None,
                                      None) == -1                       # nb <= 16
     assert lib.ocsc_history_invert_claim(8, 8, 120, 3, None, 1.0, 1.0, None, None, None, 4, None) == -1
-    assert lib.ocsc_history_woodbury_smem(100, 5) == 16 * (5050 + 3 * 100 * 5 + 25)
-    assert lib.ocsc_history_woodbury_smem(100, 10) == 16 * (5050 + 3 * 100 * 11 + 100)   # odd pitch
+    # A^-1 packed + W (K x nb, odd pitch) + capacitance nb x nb + a 16x16 scratch, all double2,
+    # plus the codes staged in their own precision (16 bytes per complex128 entry here)
+    assert lib.ocsc_history_woodbury_smem(100, 5) == 16 * (5050 + 100 * 5 + 25 + 256) + 16 * 100 * 5
+    assert lib.ocsc_history_woodbury_smem(100, 10) == 16 * (5050 + 100 * 11 + 100 + 256) + 16 * 100 * 11
     # plane-resident stream kernel: one CTA per (sample, filter group), at most one wave of 148 SMs
     ctas = lib.ocsc_code_stream_plane_ctas(4, 100, 100, 100, 10)
     assert 0 < ctas <= 148 and ctas % 10 == 0
