@@ -199,8 +199,8 @@ template <typename C, class G>
 __device__ __forceinline__ void row_stage1_inv_pre(C* S, const C* tws, int nr, int tid) {
   static_assert(G::RA == 2 && G::RB % 2 == 1, "pair fusion needs RA = 2");
   constexpr int NR = Derived<G>::NR, PR = Derived<G>::PR, RB = G::RB, TPR = RB / 2 + 1;
-  for (int e = tid; e < nr * TPR; e += blockDim.x) {
-    const int i = e / TPR, n2 = e - i * TPR;
+  for (int e = tid; e < nr * TPR; e += blockDim.x) {  // lanes -> rows: distinct bank pairs
+    const int n2 = e / nr, i = e - n2 * nr;
     C* row = S + i * PR;
     if (n2 == 0) {  // bins 0 (partner: the X[NR] slot) and RB = NR / 2 (its own partner)
       const C a0 = row[0], b0 = row[NR], a1 = row[RB];
@@ -577,7 +577,48 @@ struct PlaneArgs {
   int first;
 };
 
+__host__ __device__ constexpr int ceil_div_c(int a, int b) { return (a + b - 1) / b; }
 constexpr int PLANE_NT = 512;  // one CTA per SM: plane + state + partial in shared memory
+
+// The 25-point stage 2 of a Good-Thomas A x 25 line transform, split across threads as a 5 x 5
+// Cooley-Tukey transform so that a plane pass has ~1000 small tasks instead of ~200 long ones
+// (the 25-point register FFT kept only 6 warps busy).  With y[m] = line[(25 k1 + A m) mod N],
+// m = 5 m1 + m2 and output bin k2 = a + 5 b:
+//   Y[a + 5 b] = sum_m2 W5^{m2 b} W25^{m2 a} sum_m1 y[5 m1 + m2] W5^{m1 a}.
+// Stage a (task k1, m2): the inner 5-point DFT over m1, times W25^{m2 a}, back into the slots of
+// y[5 a + m2] (in place: each task owns its five slots).  Stage b (task k1, a): the outer 5-point
+// DFT over the slots 5 a + m2 -> Y[a + 5 b], whose natural-order position is
+// (25 tB k1 + A tA (a + 5 b)) mod N (the Good-Thomas output map of Pfa::out_pos).
+template <int A>
+struct S25 {
+  using P = Pfa<A, 25>;
+  static constexpr int N = P::N;
+  template <typename C, bool INV>
+  __device__ static __forceinline__ void stage_a(C* line, int stride, int k1, int m2, const C* tw25) {
+    const int base = (25 * k1 + A * m2) % N;
+    C v[5];
+    sfft::static_for<0, 5>([&](auto I) { v[I.value] = line[P::template wrap<5 * A * I.value>(base) * stride]; });
+    fft<C, 5, INV>(v);
+    sfft::static_for<1, 5>([&](auto I) {
+      const C t = tw25[m2 * I.value];  // e^{-2 pi i m2 a / 25}
+      v[I.value] = INV ? cmulc2(t, v[I.value]) : cmul2(t, v[I.value]);
+    });
+    sfft::static_for<0, 5>([&](auto I) { line[P::template wrap<5 * A * I.value>(base) * stride] = v[I.value]; });
+  }
+  template <typename C, bool INV>
+  __device__ static __forceinline__ void stage_b(const C* line, int stride, int k1, int a, C (&v)[5]) {
+    const int base = (25 * k1 + 5 * A * a) % N;
+    sfft::static_for<0, 5>([&](auto I) { v[I.value] = line[P::template wrap<A * I.value>(base) * stride]; });
+    fft<C, 5, INV>(v);
+  }
+  // natural-order position of output Y[a + 5 b] of task (k1, a)
+  struct Out {
+    int base;
+    __device__ __forceinline__ Out(int k1, int a) : base((25 * P::tB * k1 + A * P::tA * a) % N) {}
+    template <int B5>
+    __device__ __forceinline__ int at() const { return P::template wrap<5 * A * P::tA * B5>(base); }
+  };
+};
 
 // debug: clock64 stamps of CTA (0, 0) over its first 4 planes (scripts/plane_prof.py)
 __device__ long long* g_plane_prof = nullptr;
@@ -589,15 +630,19 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   using C = cx<T>;
   using D = Derived<G>;
   constexpr int H = G::H, W = G::W, NR = D::NR, WH = D::WH, PR = D::PR, NF = D::NF, NT = PLANE_NT;
-  static_assert(H * G::RA <= NT && WH * G::CA <= NT, "stage-2 tasks must fit one pass");
+  constexpr int CA = G::CA, RA = G::RA;
+  static_assert(G::CB == 25 && G::RB == 25, "k_plane splits the 25-point stage 2 as 5 x 5");
+  static_assert(RA == 2, "the forward row pass fuses the Hermitian post-processing (RA = 2)");
+  using SC = S25<CA>;
+  using SR = S25<RA>;
   extern __shared__ __align__(16) unsigned char smraw[];
   C* SA = reinterpret_cast<C*>(smraw);  // [H][PR] plane
-  C* SB = SA + H * PR;                  // [H][PR] second plane: stage-2 passes run out of place
-  C* WB = SB + H * PR;                  // [H][NR] state plane (pairs)
-  C* PT = WB + H * NR;                  // [NF] the group's synthesis partial
+  C* SB = SA + H * PR;                  // [H][PR] second plane: stage-b passes run out of place
+  C* PT = SB + H * PR;                  // [NF] the group's synthesis partial
   C* GS = PT + NF;                      // [NF] the sample's g, loaded once for all the group's planes
   __shared__ double scratch[4 * 32];
   __shared__ C tws[NR + 1];  // e^{-2 pi i k / W}, k <= NR
+  __shared__ C tw25[17];     // e^{-2 pi i j / 25}, j <= 16 (= 4 * 4)
   const int b = blockIdx.y, grp = blockIdx.x;
   if (*a.fl.all_done || a.fl.done[b]) return;
   const int tid = threadIdx.x;
@@ -608,61 +653,106 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
     GS[f] = gb[f];
   }
   for (int i = tid; i <= NR; i += NT) tws[i] = a.tw[i];
+  if (tid < 17) {
+    double sn, cs;
+    sincospi(-2.0 * tid / 25.0, &sn, &cs);
+    tw25[tid] = mkc<C>((T)cs, (T)sn);
+  }
   C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};
   bool nonfinite = false;
   const C ip2 = mkc<C>(a.invP, a.invP);
   long long* prof = (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ? g_plane_prof : nullptr;
   static_assert(sizeof(C) == 8, "k_plane is the float path");
+  // column tasks: lanes -> consecutive columns c (conflict-free, D/g loads coalesced);
+  // row tasks: lanes -> consecutive rows i (row pitch PR = 51 complex: 16 distinct bank pairs)
+  constexpr int NCA = 5 * CA * WH, NRA = 5 * RA * H;
+  constexpr int NWV = (H * NR + NT - 1) / NT;  // state pairs per thread
+  __syncthreads();
   for (int k = k0; k < k1; ++k) {
     PLANE_STAMP(0)
     C* wpl = reinterpret_cast<C*>(a.w + ((int64_t)b * a.K + k) * H * W);  // H x NR pairs
     const C* dk = a.Wh + (int64_t)k * NF;
-    if (!a.first) {  // 16-byte copies (two complex; H * NR is even)
-      for (int e = 2 * tid; e < H * NR; e += 2 * NT) cp_async<16>(WB + e, wpl + e);
-      cp_async_commit();
+    // this thread's state pairs e = tid + j NT of the update below, requested now into registers
+    // (their latency hides under the inverse passes; no shared-memory staging of w)
+    C wv[NWV];
+#pragma unroll
+    for (int j = 0; j < NWV; ++j) {
+      const int e = tid + j * NT;
+      wv[j] = (!a.first && e < H * NR) ? wpl[e] : mkc<C>(0, 0);
     }
-    // (a) inverse input conj(D_k) g: g from shared memory (loaded once per CTA), D_k from L2
-    // (a shared-memory prefetch of D_k instead of g measured slower)
-    for (int f = tid; f < NF; f += NT) {
-      const int u = f / WH, v = f - u * WH;
-      SA[u * PR + v] = cmulc2(dk[f], GS[f]);
+    PLANE_STAMP(1)
+    // (a) inverse input conj(D_k) g formed as column IFFT stage 1 loads it (g from shared memory,
+    // loaded once per CTA; D_k from L2), (b) column IFFT (length H along u, WH columns)
+    #pragma unroll
+    for (int j_ = 0; j_ < ceil_div_c(G::CB * WH, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= G::CB * WH) break;
+      const int n2 = e / WH, c = e - n2 * WH;
+      using P = Pfa<CA, G::CB>;
+      const int base = (CA * n2) % H;
+      C v[CA];
+      sfft::static_for<0, CA>([&](auto I) {
+        const int u = P::template wrap<G::CB * I.value>(base);
+        v[I.value] = cmulc2(dk[u * WH + c], GS[u * WH + c]);
+      });
+      fft<C, CA, true>(v);
+      sfft::static_for<0, CA>([&](auto I) { SA[P::template wrap<G::CB * I.value>(base) * PR + c] = v[I.value]; });
     }
     __syncthreads();
-    PLANE_STAMP(1)
-    // (b) column IFFT (length H along u, WH columns)
-    for (int e = tid; e < G::CB * WH; e += NT) {
-      const int n2 = e / WH, c = e - n2 * WH;
-      stage1<C, G::CA, G::CB, true>(SA + c, PR, n2);
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(NCA, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= NCA) break;
+      const int c = e % WH, q = e / WH, q1 = q % CA, m2 = q / CA;
+      SC::template stage_a<C, true>(SA + c, PR, q1, m2, tw25);
     }
     __syncthreads();
     PLANE_STAMP(2)
-    {
-      const int c = tid % WH, q1 = tid / WH;
-      if (q1 < G::CA) {
-        C v[G::CB];
-        stage2_load<C, G::CA, G::CB, true>(SA + c, PR, q1, v);
-        const OutRow<G::CA, G::CB> o(q1);
-        sfft::static_for<0, G::CB>([&](auto K2) { SB[o.template at<K2.value>() * PR + c] = v[K2.value]; });
-      }
-      __syncthreads();
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(NCA, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= NCA) break;
+      const int c = e % WH, q = e / WH, q1 = q % CA, a5 = q / CA;
+      C v[5];
+      SC::template stage_b<C, true>(SA + c, PR, q1, a5, v);
+      const typename SC::Out o(q1, a5);
+      sfft::static_for<0, 5>([&](auto B5) { SB[o.template at<B5.value>() * PR + c] = v[B5.value]; });
     }
+    __syncthreads();
     PLANE_STAMP(3)
     // (c) Hermitian pre-processing of every row fused into (d) row IFFT stage 1
     row_stage1_inv_pre<C, G>(SB, tws, H, tid);
     PLANE_STAMP(4)
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(NRA, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= NRA) break;
+      const int i = e % H, q = e / H, q1 = q % RA, m2 = q / RA;
+      SR::template stage_a<C, true>(SB + i * PR, 1, q1, m2, tw25);
+    }
+    __syncthreads();
     PLANE_STAMP(5)
-    row_stage2_oop<C, G, true>(SB, SA, H, tid);
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(NRA, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= NRA) break;
+      const int i = e % H, q = e / H, q1 = q % RA, a5 = q / RA;
+      C v[5];
+      SR::template stage_b<C, true>(SB + i * PR, 1, q1, a5, v);
+      const typename SR::Out o(q1, a5);
+      sfft::static_for<0, 5>([&](auto B5) { SA[i * PR + o.template at<B5.value>()] = v[B5.value]; });
+    }
+    __syncthreads();
     PLANE_STAMP(6)
     // (e) update w (pairs), norms, t' packed
-    if (!a.first) {
-      cp_async_wait<0>();
-      __syncthreads();
-    }
     PLANE_STAMP(7)
-    for (int e = tid; e < H * NR; e += NT) {
+#pragma unroll
+    for (int j = 0; j < NWV; ++j) {
+      const int e = tid + j * NT;
+      if (e >= H * NR) break;
       const int i = e / NR, n = e - i * NR;
       const C z = SA[i * PR + n];
-      const C wo = a.first ? mkc<C>(0, 0) : WB[e];
+      const C wo = wv[j];
       const C go = mkc<C>(clip(wo.x, a.kappa), clip(wo.y, a.kappa));
       const C uo = vsub(wo, go);
       const C wn = vfma(z, ip2, uo);
@@ -679,42 +769,93 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
     }
     __syncthreads();
     PLANE_STAMP(8)
-    // (f) row FFT of t', (g) post-processing in place (pairs k, NR-k; X[NR] into the pad slot)
-    for (int e = tid; e < H * G::RB; e += NT) {
-      const int i = e / G::RB, n2 = e - i * G::RB;
-      stage1<C, G::RA, G::RB, false>(SA + i * PR, 1, n2);
+    // (f) row FFT of t': stage 1 (2-point), then the split 25-point stage
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(H * G::RB, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= H * G::RB) break;
+      const int i = e % H, n2 = e / H;
+      stage1<C, RA, G::RB, false>(SA + i * PR, 1, n2);
     }
     __syncthreads();
     PLANE_STAMP(9)
-    // (g) post-processing fused into row stage 2: SB = forward half spectrum rows
-    row_stage2_fwd_post<C, G>(SA, SB, tws, H, tid);
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(NRA, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= NRA) break;
+      const int i = e % H, q = e / H, q1 = q % RA, m2 = q / RA;
+      SR::template stage_a<C, false>(SA + i * PR, 1, q1, m2, tw25);
+    }
+    __syncthreads();
     PLANE_STAMP(10)
+    // (g) stage b with the Hermitian post-processing fused into its stores (SA -> SB = forward
+    // half-spectrum rows): bin k2 pairs with bin 25 - k2 of the same k1, i.e. outer task a with
+    // task 5 - a, so a thread runs task 0 alone or the pair (1, 4) / (2, 3)
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(3 * RA * H, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= 3 * RA * H) break;
+      const int i = e % H, q = e / H, q1 = q % RA, s = q / RA;
+      const C* src = SA + i * PR;
+      C* row = SB + i * PR;
+      C u[5];
+      SR::template stage_b<C, false>(src, 1, q1, s, u);
+      const typename SR::Out ou(q1, s);
+      if (s == 0) {
+        sfft::static_for<0, 5>([&](auto B5) {
+          constexpr int bb = B5.value, bp = (5 - bb) % 5;
+          const int kk = ou.template at<bb>();
+          row[kk] = herm_post(u[bb], u[bp], tws[kk]);
+        });
+        if (q1 == 0) row[NR] = herm_post(u[0], u[0], tws[NR]);
+      } else {
+        C w[5];
+        SR::template stage_b<C, false>(src, 1, q1, 5 - s, w);
+        const typename SR::Out ow(q1, 5 - s);
+        sfft::static_for<0, 5>([&](auto B5) {
+          constexpr int bb = B5.value;
+          const int ku = ou.template at<bb>(), kw = ow.template at<bb>();
+          row[ku] = herm_post(u[bb], w[4 - bb], tws[ku]);
+          row[kw] = herm_post(w[bb], u[4 - bb], tws[kw]);
+        });
+      }
+    }
+    __syncthreads();
     PLANE_STAMP(11)
-    // (h) column FFT
-    for (int e = tid; e < G::CB * WH; e += NT) {
+    // (h) column FFT: stage 1 in place, stage a in place, stage b with (i) the synthesis partial
+    // fused into its stores: PT[f] += D_k[f] T_k[f] (every f is one output of one task: no race)
+    #pragma unroll
+    for (int j_ = 0; j_ < ceil_div_c(G::CB * WH, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= G::CB * WH) break;
       const int n2 = e / WH, c = e - n2 * WH;
-      stage1<C, G::CA, G::CB, false>(SB + c, PR, n2);
+      stage1<C, CA, G::CB, false>(SB + c, PR, n2);
     }
     __syncthreads();
     PLANE_STAMP(12)
-    {
-      const int c = tid % WH, q1 = tid / WH;
-      if (q1 < G::CA) {
-        C v[G::CB];
-        stage2_load<C, G::CA, G::CB, false>(SB + c, PR, q1, v);
-        const OutRow<G::CA, G::CB> o(q1);
-        sfft::static_for<0, G::CB>([&](auto K2) { SA[o.template at<K2.value>() * PR + c] = v[K2.value]; });
-      }
-      __syncthreads();
+    #pragma unroll 1
+    for (int j_ = 0; j_ < ceil_div_c(NCA, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= NCA) break;
+      const int c = e % WH, q = e / WH, q1 = q % CA, m2 = q / CA;
+      SC::template stage_a<C, false>(SB + c, PR, q1, m2, tw25);
     }
+    __syncthreads();
     PLANE_STAMP(13)
-    // (i) synthesis partial: PT[f] += D_k[f] T_k[f] (each thread revisits the same f: no race)
-#pragma unroll 4
-    for (int f = tid; f < NF; f += NT) {
-      const int u = f / WH, v = f - u * WH;
-      PT[f] = vfma_c(dk[f], SA[u * PR + v], PT[f]);
+    #pragma unroll
+    for (int j_ = 0; j_ < ceil_div_c(NCA, NT); ++j_) {
+      const int e = tid + j_ * NT;
+      if (e >= NCA) break;
+      const int c = e % WH, q = e / WH, q1 = q % CA, a5 = q / CA;
+      C v[5];
+      SC::template stage_b<C, false>(SB + c, PR, q1, a5, v);
+      const typename SC::Out o(q1, a5);
+      sfft::static_for<0, 5>([&](auto B5) {
+        const int f = o.template at<B5.value>() * WH + c;
+        PT[f] = vfma_c(dk[f], v[B5.value], PT[f]);
+      });
     }
-    __syncthreads();  // SA / WB are rewritten by the next plane
+    __syncthreads();  // SA / SB are rewritten by the next plane
     PLANE_STAMP(14)
   }
   C* part = a.part + ((int64_t)b * a.groups + grp) * NF;
@@ -852,7 +993,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   }
   PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
                      (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
-  const size_t plane_smem = ((size_t)H * (2 * D::PR + D::NR) + 2 * NF) * sizeof(cx<T>);
+  const size_t plane_smem = ((size_t)H * 2 * D::PR + 2 * NF) * sizeof(cx<T>);
   if constexpr (G::PLANE)
     OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
   int rc = OCSC_OK, chunk = 0;

@@ -37,9 +37,9 @@ infer_codes_stream(xh, tr.Wh, tr.den, shape, cc, buf, B, poll=0)
 torch.cuda.synchronize()
 _lib.call("ocsc_debug_plane_profile", None)
 t = pb.cpu().numpy().reshape(4, 16).astype(np.int64)
-names = ["conj(D)g", "col stage1 inv", "col stage2 inv", "hermitian pre", "row stage1 inv", "row stage2 inv",
-         "w wait", "update", "row stage1 fwd", "row stage2 fwd", "post", "col stage1 fwd", "col stage2 fwd",
-         "partial"]
+names = ["w prefetch issue", "col inv s1(cdg)+a", "col inv b", "herm pre+row s1", "row inv a", "row inv b",
+         "w wait", "update", "row fwd s1", "row fwd a", "row fwd b+post", "col fwd s1", "col fwd a",
+         "col fwd b+partial"]
 d = np.diff(t[:, :15], axis=1)
 print("cycles per phase (median over the CTA's first 4 planes):")
 for i, n in enumerate(names):
