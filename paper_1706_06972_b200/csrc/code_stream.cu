@@ -57,7 +57,7 @@ template <typename T> struct SGeo<T, 266, 266> {
   static constexpr bool PLANE = false;
   static constexpr int H = 266, W = 266, RA = 7, RB = 19, CA = 14, CB = 19;
   static constexpr int R = 16, NTR = 128;
-  static constexpr int L = 8, NTC = 128;
+  static constexpr int L = 8, NTC = 160;  // stage 1: 19 x 8 = 152 tasks in one round
 };
 
 template <class G> struct Derived {
