@@ -739,22 +739,24 @@ extern "C" int ocsc_history_factor(int dtype_hist, int K, int nfreq, const void*
   const size_t smem = (dtype_hist == OCSC_F64 ? (size_t)chol_panel_offset<double>() : (size_t)chol_panel_offset<float>()) +
                       cs * (size_t)CT * (K - CT);  // L_kk + 1/L_jj + panel
   if (smem > 227 * 1024) return fail(OCSC_EARG, "history_factor: panel exceeds shared memory for this K/dtype");
+  size_t smem_req = smem;  // dev knob: request more shared memory (fewer CTAs per SM, a smaller L2 working set)
+  if (const char* e = getenv("OCSC_CHOL_MINSMEM")) smem_req = std::max(smem, (size_t)atol(e));
   // float: 512 threads (one CTA per SM) from K = 384; up to K = 288, 128-thread CTAs, three per SM (measured
   // at K = 256: 19.0 ms with 128, 20.8 with 256, 30.3 with 512 threads); OCSC_CHOL_NT overrides
   int nt = dtype_hist == OCSC_F32 ? (K >= 384 ? 512 : (K <= 288 ? 128 : 256)) : 256;
   if (const char* e = getenv("OCSC_CHOL_NT")) nt = atoi(e);
   if (dtype_hist == OCSC_F32 && nt == 512) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<float, 512><<<nfreq, 512, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_req));
+    k_chol_blocked<float, 512><<<nfreq, 512, smem_req, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
   } else if (dtype_hist == OCSC_F32 && nt == 256) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<float, 256><<<nfreq, 256, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_req));
+    k_chol_blocked<float, 256><<<nfreq, 256, smem_req, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
   } else if (dtype_hist == OCSC_F32) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<float, 128><<<nfreq, 128, smem, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<float, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_req));
+    k_chol_blocked<float, 128><<<nfreq, 128, smem_req, s>>>(K, Kv, (const float2*)S, (float)ridge, (float2*)L, info);
   } else if (dtype_hist == OCSC_F64) {
-    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<double, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_chol_blocked<double, 256><<<nfreq, 256, smem, s>>>(K, Kv, (const double2*)S, ridge, (double2*)L, info);
+    OCSC_CUDA(cudaFuncSetAttribute(k_chol_blocked<double, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_req));
+    k_chol_blocked<double, 256><<<nfreq, 256, smem_req, s>>>(K, Kv, (const double2*)S, ridge, (double2*)L, info);
   } else {
     return fail(OCSC_EARG, "dtype must be 4 or 8");
   }

@@ -276,34 +276,52 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   C* spec = a.spec + ((int64_t)b * rows + r0) * WH;
   T* w = a.w + ((int64_t)b * rows + r0) * W;
 
-  // 0. prefetch this block's state rows (contiguous) into WB; consumed by the update
+  // 0. this block's state rows (contiguous) into WB, consumed by the update, and 1. its spectrum
+  // rows into SA (the row pitch equals WH: one contiguous block).  float: two TMA bulk copies
+  // issued by one thread (no per-thread copy instructions, no bank conflicts on the shared-memory
+  // side); double: cp.async / plain copies
   C* WB = SA + R * PR;
-  if (!a.first) {
-    const C* wsrc = reinterpret_cast<const C*>(w);
-    if constexpr (sizeof(C) == 8) {  // 16-byte copies (two complex)
-      const int n = nr * NR;
-      for (int e = 2 * tid; e < n; e += 2 * G::NTR) {
-        if (e + 1 < n) cp_async<16>(WB + e, wsrc + e);
-        else cp_async<8>(WB + e, wsrc + e);
-      }
-    } else {
-      for (int e = tid; e < nr * NR; e += G::NTR) cp_async<sizeof(C)>(WB + e, wsrc + e);
+  constexpr bool BULK = PR == WH && sizeof(C) == 8;
+  __shared__ __align__(8) uint64_t mb_bulk[2];
+  const uint32_t wbytes = (uint32_t)(nr * NR * sizeof(C)), sbytes = (uint32_t)(nr * WH * sizeof(C));
+  const bool bulk = BULK && (wbytes % 16 == 0) && (sbytes % 16 == 0) && ((uintptr_t)w % 16 == 0) &&
+                    ((uintptr_t)spec % 16 == 0);
+  if (bulk) {
+    if (tid == 0) {
+      bulk_mbar_init(&mb_bulk[0]);
+      bulk_mbar_init(&mb_bulk[1]);
+      bulk_g2s(SA, spec, sbytes, &mb_bulk[0]);
+      if (!a.first) bulk_g2s(WB, w, wbytes, &mb_bulk[1]);
     }
-    cp_async_commit();
-  }
-  // 1. spectrum rows -> SA (the row pitch equals WH: one contiguous block)
-  if constexpr (PR == WH && sizeof(C) == 8) {
-    const int n = nr * WH;
-    for (int e = 2 * tid; e < n; e += 2 * G::NTR) {
-      if (e + 1 < n) cp_async<16>(SA + e, spec + e);
-      else cp_async<8>(SA + e, spec + e);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
+    __syncthreads();  // barriers initialised before anyone waits on them
+    bulk_wait(&mb_bulk[0], 0);
   } else {
-    for (int e = tid; e < nr * WH; e += G::NTR) {
-      const int i = e / WH, k = e - i * WH;
-      SA[i * PR + k] = spec[(int64_t)i * WH + k];
+    if (!a.first) {
+      const C* wsrc = reinterpret_cast<const C*>(w);
+      if constexpr (sizeof(C) == 8) {  // 16-byte copies (two complex)
+        const int n = nr * NR;
+        for (int e = 2 * tid; e < n; e += 2 * G::NTR) {
+          if (e + 1 < n) cp_async<16>(WB + e, wsrc + e);
+          else cp_async<8>(WB + e, wsrc + e);
+        }
+      } else {
+        for (int e = tid; e < nr * NR; e += G::NTR) cp_async<sizeof(C)>(WB + e, wsrc + e);
+      }
+      cp_async_commit();
+    }
+    if constexpr (PR == WH && sizeof(C) == 8) {
+      const int n = nr * WH;
+      for (int e = 2 * tid; e < n; e += 2 * G::NTR) {
+        if (e + 1 < n) cp_async<16>(SA + e, spec + e);
+        else cp_async<8>(SA + e, spec + e);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+    } else {
+      for (int e = tid; e < nr * WH; e += G::NTR) {
+        const int i = e / WH, k = e - i * WH;
+        SA[i * PR + k] = spec[(int64_t)i * WH + k];
+      }
     }
   }
   __syncthreads();
@@ -334,8 +352,12 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   C sl[4] = {mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0), mkc<C>(0, 0)};  // per-thread partial norms
   bool nonfinite = false;
   if (!a.first) {
-    cp_async_wait<0>();
-    __syncthreads();
+    if (bulk) {
+      bulk_wait(&mb_bulk[1], 0);
+    } else {
+      cp_async_wait<0>();
+      __syncthreads();
+    }
   }
   const C ip2 = mkc<C>(a.invP, a.invP);
   RowWalk<NR, G::NTR> uw(tid);

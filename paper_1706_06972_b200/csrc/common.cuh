@@ -146,6 +146,33 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// ------------------------------------------------------- bulk copies (TMA) --
+// One thread moves a contiguous global block into shared memory with cp.async.bulk (16-byte
+// aligned addresses, size a multiple of 16); completion is counted on an mbarrier that every
+// consumer waits on (one phase per barrier here: each is used once per CTA).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_mbar_init(uint64_t* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(m)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// issue (one thread): expect `bytes` on m, then copy
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(m))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait(uint64_t* m, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(m)), "r"(phase)
+        : "memory");
+}
+
 // ------------------------------------------------------------ reductions --
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
