@@ -150,7 +150,7 @@ template <typename C, class G, bool INV>
 __device__ __forceinline__ void row_stage2(C* SA, int nr, int tid) {
   constexpr int PR = Derived<G>::PR;
   const bool act = tid < nr * G::RA;
-  const int i = tid / G::RA, k1 = tid - (tid / G::RA) * G::RA;
+  const int k1 = tid / nr, i = tid - k1 * nr;  // lanes -> rows
   C v[G::RB];
   if (act) stage2_load<C, G::RA, G::RB, INV>(SA + i * PR, 1, k1, v);
   __syncthreads();
@@ -241,6 +241,26 @@ __device__ __forceinline__ void row_stage2_fwd_post(const C* src, C* dst, const 
     if (k1 == 0) row[NR] = herm_post(v[0], v[0], tws[NR]);
   }
   __syncthreads();
+}
+
+// stage-1 task e of a row pass -> (row i, task n2): 16 consecutive n2 of one row per half-warp
+// (positions step by RA: distinct bank pairs), the RB - 16 remaining tasks of every row after
+// them with lanes over rows
+template <int RB>
+__device__ __forceinline__ void row_task1(int e, int nr, int& i, int& n2) {
+  if constexpr (RB >= 16) {
+    if (e < nr * 16) {
+      i = e >> 4;
+      n2 = e & 15;
+    } else {
+      const int j = e - nr * 16;
+      n2 = 16 + j / nr;
+      i = j - (n2 - 16) * nr;
+    }
+  } else {
+    i = e / RB;
+    n2 = e - i * RB;
+  }
 }
 
 // ----------------------------------------------------------------- row pass --
@@ -342,7 +362,8 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   __syncthreads();
   // 3. inverse FFT_NR in place: stage 1, then stage 2 through registers (one round of tasks)
   for (int e = tid; e < nr * G::RB; e += G::NTR) {
-    const int i = e / G::RB, n2 = e - i * G::RB;
+    int i, n2;
+    row_task1<G::RB>(e, nr, i, n2);
     stage1<C, G::RA, G::RB, true>(SA + i * PR, 1, n2);
   }
   __syncthreads();
@@ -390,7 +411,8 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
   }
   // 5. forward FFT_NR of t' in place
   for (int e = tid; e < nr * G::RB; e += G::NTR) {
-    const int i = e / G::RB, n2 = e - i * G::RB;
+    int i, n2;
+    row_task1<G::RB>(e, nr, i, n2);
     stage1<C, G::RA, G::RB, false>(SA + i * PR, 1, n2);
   }
   __syncthreads();
