@@ -144,13 +144,54 @@ struct OutRow {
   __device__ __forceinline__ int at() const { return Pfa<A, B_>::template wrap<A * Pfa<A, B_>::tA * K2>(base); }
 };
 
+// stage-1 task e of a row pass -> (row i, task n2): 16 consecutive n2 of one row per half-warp
+// (positions step by RA: distinct bank pairs), the RB - 16 remaining tasks of every row after
+// them with lanes over rows
+template <int RB>
+__device__ __forceinline__ void row_task1(int e, int nr, int& i, int& n2) {
+  if constexpr (RB >= 16) {
+    if (e < nr * 16) {
+      i = e >> 4;
+      n2 = e & 15;
+    } else {
+      const int j = e - nr * 16;
+      n2 = 16 + j / nr;
+      i = j - (n2 - 16) * nr;
+    }
+  } else {
+    i = e / RB;
+    n2 = e - i * RB;
+  }
+}
+
+// stage-2 task t of a row pass -> (row i, task k1): each half-warp takes 8 rows x two consecutive
+// k1 (positions of k1 + 1 are an odd number of bank pairs away from those of k1, the 8 rows an even
+// number apart: 16 distinct bank pairs); an odd RA's last k1 runs with lanes over rows
+template <int RA>
+__device__ __forceinline__ void row_task2(int t, int nr, int& i, int& k1) {
+  constexpr int P = RA / 2;
+  const int npair = (nr & 7) == 0 ? (nr >> 3) * P * 16 : 0;
+  if (t < npair) {
+    const int h = t >> 4, l = t & 15, rbk = h / P, pi = h - rbk * P;
+    i = 8 * rbk + (l & 7);
+    k1 = 2 * pi + (l >> 3);
+  } else if (npair > 0) {
+    i = t - npair;
+    k1 = RA - 1;
+  } else {
+    k1 = t / nr;
+    i = t - k1 * nr;
+  }
+}
+
 // stage 2 of the row transform in place: every task loads its B-line into registers, the CTA
 // syncs, then the outputs land in natural order (tasks <= threads, one round); ends synced.
 template <typename C, class G, bool INV>
 __device__ __forceinline__ void row_stage2(C* SA, int nr, int tid) {
   constexpr int PR = Derived<G>::PR;
   const bool act = tid < nr * G::RA;
-  const int k1 = tid / nr, i = tid - k1 * nr;  // lanes -> rows
+  int i, k1;
+  row_task2<G::RA>(tid, nr, i, k1);
   C v[G::RB];
   if (act) stage2_load<C, G::RA, G::RB, INV>(SA + i * PR, 1, k1, v);
   __syncthreads();
@@ -241,26 +282,6 @@ __device__ __forceinline__ void row_stage2_fwd_post(const C* src, C* dst, const 
     if (k1 == 0) row[NR] = herm_post(v[0], v[0], tws[NR]);
   }
   __syncthreads();
-}
-
-// stage-1 task e of a row pass -> (row i, task n2): 16 consecutive n2 of one row per half-warp
-// (positions step by RA: distinct bank pairs), the RB - 16 remaining tasks of every row after
-// them with lanes over rows
-template <int RB>
-__device__ __forceinline__ void row_task1(int e, int nr, int& i, int& n2) {
-  if constexpr (RB >= 16) {
-    if (e < nr * 16) {
-      i = e >> 4;
-      n2 = e & 15;
-    } else {
-      const int j = e - nr * 16;
-      n2 = 16 + j / nr;
-      i = j - (n2 - 16) * nr;
-    }
-  } else {
-    i = e / RB;
-    n2 = e - i * RB;
-  }
 }
 
 // ----------------------------------------------------------------- row pass --
