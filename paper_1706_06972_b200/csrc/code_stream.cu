@@ -366,8 +366,38 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
     }
   }
   __syncthreads();
-  // 2. Hermitian pre-processing (pairs k, NR-k): Z = (X_k + X*_{NR-k}) + i e^{+i 2pi k/W}(X_k - X*_{NR-k})
-  {
+  // 2. Hermitian pre-processing (pairs k, NR-k): Z = (X_k + X*_{NR-k}) + i e^{+i 2pi k/W}(X_k - X*_{NR-k}),
+  // 3. inverse FFT_NR in place: stage 1, then stage 2 through registers (one round of tasks)
+  if constexpr (G::RA % 2 == 1) {
+    // odd RA (266: 7 x 19): the pre-processing pairs position p with NR - p, and the stage-1 task
+    // n2 (positions p(n1, n2) = (RB n1 + RA n2) mod NR) with task RB - n2 (positions NR - p(-n1, n2)),
+    // so one thread forms both tasks' inputs from the same 2 RA loads and runs both transforms
+    // (task 0 is its own partner; its p = 0 pairs with the Nyquist bin X[NR])
+    using P = Pfa<G::RA, G::RB>;
+    constexpr int RA = G::RA, RB = G::RB, NT1 = RB / 2 + 1;
+    for (int e = tid; e < nr * NT1; e += G::NTR) {
+      const int n2 = e / nr, i = e - n2 * nr;  // lanes over rows
+      C* row = SA + i * PR;
+      const int base = (RA * n2) % NR;
+      int pos[RA];
+      C u[RA], v[RA];
+      sfft::static_for<0, RA>([&](auto I) {
+        pos[I.value] = P::template wrap<RB * I.value>(base);
+        const C x = row[pos[I.value]], y = row[NR - pos[I.value]];
+        u[I.value] = herm_pre(x, y, tws[pos[I.value]]);
+        v[I.value] = herm_pre(y, x, tws[NR - pos[I.value]]);
+      });
+      fft<C, RA, true>(u);
+      sfft::static_for<0, RA>([&](auto I) { row[pos[I.value]] = u[I.value]; });
+      if (n2 != 0) {  // task RB - n2: its n1-th input sits at NR - p((RA - n1) % RA, n2)
+        C w[RA];
+        sfft::static_for<0, RA>([&](auto I) { w[I.value] = v[(RA - I.value) % RA]; });
+        fft<C, RA, true>(w);
+        sfft::static_for<0, RA>([&](auto I) { row[NR - pos[(RA - I.value) % RA]] = w[I.value]; });
+      }
+    }
+    __syncthreads();
+  } else {
     constexpr int NP = NR / 2 + 1;
     RowWalk<NP, G::NTR> rw(tid);
     for (int e = tid; e < nr * NP; e += G::NTR, rw.advance()) {
@@ -379,15 +409,14 @@ __global__ void __launch_bounds__(G::NTR) k_rows(RowArgs<T, G> a) {
       row[k] = z1;
       if (k != 0 && k2 != k) row[k2] = z2;
     }
+    __syncthreads();
+    for (int e = tid; e < nr * G::RB; e += G::NTR) {
+      int i, n2;
+      row_task1<G::RB>(e, nr, i, n2);
+      stage1<C, G::RA, G::RB, true>(SA + i * PR, 1, n2);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // 3. inverse FFT_NR in place: stage 1, then stage 2 through registers (one round of tasks)
-  for (int e = tid; e < nr * G::RB; e += G::NTR) {
-    int i, n2;
-    row_task1<G::RB>(e, nr, i, n2);
-    stage1<C, G::RA, G::RB, true>(SA + i * PR, 1, n2);
-  }
-  __syncthreads();
   row_stage2<C, G, true>(SA, nr, tid);
   // 4. update: c = (Re z[n], Im z[n]) = (c[2n], c[2n+1]); w' = S(w) + c/P; norms; t' packed into SA
   // (x, y) pairs run as 2-wide arithmetic; Gamma = clip(w) by min/max, U = w - Gamma
