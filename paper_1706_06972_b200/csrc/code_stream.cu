@@ -669,6 +669,11 @@ struct PlaneArgs {
   int32_t* bad;
   Flags fl;
   int first;
+  // the stopping test runs in the last CTA to finish (ticket counter; no k_decide launch)
+  int32_t* flags;       // (2 B + 3): done, bad, all_done, iteration count, ticket
+  int32_t* iters;
+  int32_t* status;
+  double tol;
 };
 
 __host__ __device__ constexpr int ceil_div_c(int a, int b) { return (a + b - 1) / b; }
@@ -738,8 +743,28 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
   __shared__ C tws[NR + 1];  // e^{-2 pi i k / W}, k <= NR
   __shared__ C tw25[17];     // e^{-2 pi i j / 25}, j <= 16 (= 4 * 4)
   const int b = blockIdx.y, grp = blockIdx.x;
-  if (*a.fl.all_done || a.fl.done[b]) return;
+  if (*a.fl.all_done) return;  // (every CTA sees the same flag: no ticket is taken this launch)
   const int tid = threadIdx.x;
+  __shared__ int s_last;
+  // this CTA's ticket; the last one runs the stopping test of the iteration
+  auto ticket = [&]() {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();  // the norms' atomics above are visible before the ticket
+      const int t = atomicAdd(a.flags + 2 * a.B + 2, 1);
+      s_last = t == (int)(gridDim.x * gridDim.y) - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      if (tid == 0) a.flags[2 * a.B + 2] = 0;
+      decide_block(a.B, a.tol, a.acc, a.flags, a.iters, a.status);
+    }
+  };
+  if (a.fl.done[b]) {
+    ticket();
+    return;
+  }
   const int k0 = grp * a.kper, k1 = min(a.K, k0 + a.kper);
   const C* gb = a.g + (int64_t)b * NF;
   for (int f = tid; f < NF; f += NT) {
@@ -962,6 +987,7 @@ __global__ void __launch_bounds__(PLANE_NT, 1) k_plane(PlaneArgs<T, G> a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) atomicAdd(a.acc + 4 * b + j, sn[j]);
   }
+  ticket();
 }
 
 // final pass: u = S(w) in place
@@ -1004,7 +1030,7 @@ size_t stream_layout(int dtype, int H, int W, int K, int B, int groups, StreamWo
   char* part = take((size_t)B * groups * nf * s);
   char* g = take((size_t)B * nf * s);
   char* acc = take((size_t)B * 4 * sizeof(double));
-  char* flags = take((size_t)(2 * B + 2) * sizeof(int32_t));
+  char* flags = take((size_t)(2 * B + 3) * sizeof(int32_t));  // + the plane kernel's ticket
   if (w) {
     w->part = part; w->g = g; w->acc = (double*)acc; w->flags = (int32_t*)flags;
   }
@@ -1057,7 +1083,7 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
   const cx<T>* tw = twiddles<T>(W);
   if (!tw) return fail(OCSC_ECUDA, "code_stream: twiddle table allocation failed");
   OCSC_CUDA(cudaMemsetAsync(sw.acc, 0, sizeof(double) * 4 * B, s));
-  OCSC_CUDA(cudaMemsetAsync(sw.flags, 0, sizeof(int32_t) * (2 * B + 2), s));
+  OCSC_CUDA(cudaMemsetAsync(sw.flags, 0, sizeof(int32_t) * (2 * B + 3), s));
   OCSC_CUDA(cudaMemsetAsync(iters, 0, sizeof(int32_t) * B, s));
   OCSC_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * B, s));
   if (B == 0 || max_iters <= 0) {
@@ -1086,7 +1112,8 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
     OCSC_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
   }
   PlaneArgs<T, G> pa{K, B, groups, kper, (T)(beta / rho), (T)(1.0 / ((double)H * W)), (T*)u, (const cx<T>*)Wh,
-                     (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1};
+                     (const cx<T>*)sw.g, (cx<T>*)sw.part, tw, sw.acc, sw.flags + B, fl, 1, sw.flags, iters, status,
+                     rel_tol};
   const size_t plane_smem = ((size_t)H * 2 * D::PR + 2 * NF) * sizeof(cx<T>);
   if constexpr (G::PLANE)
     OCSC_CUDA(cudaFuncSetAttribute(k_plane<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plane_smem));
@@ -1098,9 +1125,8 @@ int run(int K, int B, const void* xh, const void* Wh, const void* den, double be
       k_gsum<T><<<ggrid, 256, 0, s>>>(B, NF, groups, (const cx<T>*)xh, (const T*)den,
                                       it > 1 ? (const cx<T>*)sw.part : nullptr, (cx<T>*)sw.g, fl);
       pa.first = it == 1;
-      k_plane<T, G><<<dim3(groups, B), PLANE_NT, plane_smem, s>>>(pa);
-      k_decide<<<1, 256, 0, s>>>(B, rel_tol, sw.acc, sw.flags, iters, status);
-      count_launches(3);
+      k_plane<T, G><<<dim3(groups, B), PLANE_NT, plane_smem, s>>>(pa);  // (its last CTA decides)
+      count_launches(2);
     } else {
     if (it > 1) {
       k_cols_f<T, G><<<cgrid, G::NTC, colf_smem, s>>>(ca);  // groups == 1: writes g itself

@@ -220,4 +220,43 @@ __host__ __device__ __forceinline__ int64_t packed_index(int i, int j) {  // j <
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// the per-sample stopping test of one code-ADMM iteration (coding.py:105-118) by one CTA: k_decide,
+// or the last CTA of the plane-resident stream kernel.  flags = (done[B], bad[B], all_done,
+// iteration count, ...); acc = (B, 4) squared norms, zeroed for the next iteration
+__device__ __forceinline__ void decide_block(int B, double tol, double* acc, int32_t* flags, int32_t* iters,
+                                             int32_t* status) {
+  int32_t* done = flags;
+  int32_t* bad = flags + B;
+  int32_t* all_done = flags + 2 * B;
+  int32_t* itc = flags + 2 * B + 1;
+  if (*all_done) return;
+  __shared__ int it_s;
+  __syncthreads();
+  if (threadIdx.x == 0) it_s = ++(*itc);
+  __syncthreads();
+  const int it = it_s;
+  int mine = 1;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (!done[b]) {
+      iters[b] = it;
+      if (bad[b]) {
+        done[b] = 1;
+        status[b] = 2;
+      } else {
+        const double num = sqrt(acc[4 * b]), den = sqrt(acc[4 * b + 1]);
+        const double gap = sqrt(acc[4 * b + 2]), dual = sqrt(acc[4 * b + 3]);
+        const double gap_scale = fmax(fmax(den, dual), 1e-12);
+        if (num <= tol * fmax(den, 1e-12) && gap <= tol * gap_scale) {
+          done[b] = 1;
+          status[b] = 1;
+        }
+      }
+      acc[4 * b] = acc[4 * b + 1] = acc[4 * b + 2] = acc[4 * b + 3] = 0.0;
+    }
+    mine &= done[b];
+  }
+  const int all = __syncthreads_and(mine);
+  if (threadIdx.x == 0 && all) *all_done = 1;
+}
+
 }  // namespace ocsc
