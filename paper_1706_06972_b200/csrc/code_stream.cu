@@ -202,19 +202,6 @@ __device__ __forceinline__ void row_stage2(C* SA, int nr, int tid) {
   __syncthreads();
 }
 
-// stage 2 of the row transform out of place (src -> dst, natural order); ends synced
-template <typename C, class G, bool INV>
-__device__ __forceinline__ void row_stage2_oop(const C* src, C* dst, int nr, int tid) {
-  constexpr int PR = Derived<G>::PR;
-  for (int e = tid; e < nr * G::RA; e += blockDim.x) {
-    const int i = e / G::RA, k1 = e - i * G::RA;
-    C v[G::RB];
-    stage2_load<C, G::RA, G::RB, INV>(src + i * PR, 1, k1, v);
-    const OutRow<G::RA, G::RB> o(k1);
-    sfft::static_for<0, G::RB>([&](auto K2) { dst[i * PR + o.template at<K2.value>()] = v[K2.value]; });
-  }
-  __syncthreads();
-}
 
 // Rows with RA = 2 (W = 100): the Hermitian pre-/post-processing that maps a half spectrum to
 // the packed NR-point complex transform pairs bin k with bin NR - k.  Stage-1 task n2 touches
@@ -262,27 +249,6 @@ __device__ __forceinline__ void row_stage1_inv_pre(C* S, const C* tws, int nr, i
   __syncthreads();
 }
 
-// forward row stage 2 out of place (src -> dst) with the post-processing fused in: dst rows hold
-// the half spectrum X[0..NR] in natural order; ends synced
-template <typename C, class G>
-__device__ __forceinline__ void row_stage2_fwd_post(const C* src, C* dst, const C* tws, int nr, int tid) {
-  static_assert(G::RA == 2, "pair fusion needs RA = 2");
-  constexpr int NR = Derived<G>::NR, PR = Derived<G>::PR, RB = G::RB;
-  for (int e = tid; e < nr * G::RA; e += blockDim.x) {
-    const int i = e / G::RA, k1 = e - i * G::RA;
-    C v[RB];
-    stage2_load<C, G::RA, RB, false>(src + i * PR, 1, k1, v);
-    const OutRow<G::RA, RB> o(k1);
-    C* row = dst + i * PR;
-    sfft::static_for<0, RB>([&](auto K2) {
-      constexpr int k2 = K2.value, kp = (RB - k2) % RB;  // bin NR - k of bin k
-      const int k = o.template at<k2>();
-      row[k] = herm_post(v[k2], v[kp], tws[k]);
-    });
-    if (k1 == 0) row[NR] = herm_post(v[0], v[0], tws[NR]);
-  }
-  __syncthreads();
-}
 
 // ----------------------------------------------------------------- row pass --
 template <typename T, class G>
