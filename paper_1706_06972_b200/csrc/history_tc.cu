@@ -240,22 +240,23 @@ __global__ void __launch_bounds__(256) k_hist_accum_tc(int K, int B, const float
     for (int q = 0; q < 32; ++q) E[part * (TB * 33) + r * 33 + q] = __uint_as_float(v[q]);
     __syncthreads();
     const int col = J * TB + c0 + lane;
-    // lanes = 32 consecutive columns of one row; each warp's 16 rows go in batches of 8 whose
-    // loads are all in flight before the first add
+    // lanes = 32 consecutive columns of one row; NB of a warp's 16 rows have their loads in
+    // flight before the first add (float: all 16)
+    constexpr int NB = sizeof(Th) == 4 ? 16 : 8;  // rows in flight per warp (double: 8 keeps two CTAs per SM)
 #pragma unroll 1
-    for (int rb = 0; rb < TB / 8; rb += 8) {
-      cx<Th> cur[8];
-      int64_t at[8];
-      bool ok[8];
+    for (int rb = 0; rb < TB / 8; rb += NB) {
+      cx<Th> cur[NB];
+      int64_t at[NB];
+      bool ok[NB];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NB; ++u) {
         const int rr = warp + 8 * (rb + u), row = I * TB + rr;
         ok[u] = row < K && col <= row && col < K;
         at[u] = (int64_t)p * npk + packed_index(row, col);
         if (ok[u]) cur[u] = S[at[u]];
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < NB; ++u) {
         const int rr = warp + 8 * (rb + u);
         if (ok[u]) {
           const float vr = E[rr * 33 + lane], vi = E[TB * 33 + rr * 33 + lane];
