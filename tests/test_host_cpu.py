@@ -243,7 +243,7 @@ def test_committed_launch_list_and_traffic_table_agree():
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = subprocess.run([sys.executable, os.path.join(root, "scripts", "traffic_from_launches.py"),
-                          os.path.join(root, "profiles", "r2_bench_launches.csv")], capture_output=True, text=True,
+                          os.path.join(root, "profiles", "r2_bench_launches_s3.csv")], capture_output=True, text=True,
                          check=True).stdout
     assert "k_code_fused" in out
     t = json.load(open(os.path.join(root, "profiles", "traffic.json")))
