@@ -13,9 +13,11 @@
 //            row FFT of t' -> back into the same spectrum rows.   HBM: spectrum r+w, w r+w.
 //   k_cols_f (per L columns x K-group of one sample): forward column FFT of every plane,
 //            times D_k, summed over the group in registers -> one partial per group.
-//   k_g      g = (X - sum of partials) / den per frequency.
+//   k_gsum   g = (X - sum of partials) / den per frequency.
 //   k_cols_i (per L columns x K-group): conj(D_k) g -> inverse column FFT -> spectrum.
 //   k_decide the per-sample stopping test (code.cu), which freezes converged samples.
+//   k_plane  (float 100 x 100, config 2): the whole iteration of a (sample, filter) plane on
+//            chip, one CTA per (sample, filter group); its last CTA takes the stopping test.
 //
 // Per iteration and sample that is 6 passes over K*P reals (spectrum written and read twice,
 // w read and written once) where the cuFFT path needs 10+ (and 5 kernels per 266-point
@@ -619,7 +621,7 @@ __global__ void __launch_bounds__(G::NTC) k_cols_i(ColArgs<T, G> a) {
 // ------------------------------------------------------------ plane-resident --
 // For grids whose half-spectrum plane fits one CTA's shared memory (100 x 100: 41 KB) the whole
 // iteration of a (sample, filter) plane stays on chip: conj(D_k) g -> column IFFT -> row IFFT ->
-// update of w (row-major, prefetched by cp.async) -> row FFT of t' -> column FFT -> times D_k,
+// update of w (row-major, requested into registers at the plane's start) -> row FFT of t' -> column FFT -> times D_k,
 // summed in registers over the CTA's filter group.  HBM per plane and iteration: w read + write
 // and the group partial (vs six passes over the spectrum for the row/column kernels).
 template <typename T, class G>
