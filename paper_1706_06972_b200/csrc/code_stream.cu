@@ -621,9 +621,10 @@ __global__ void __launch_bounds__(G::NTC) k_cols_i(ColArgs<T, G> a) {
 // ------------------------------------------------------------ plane-resident --
 // For grids whose half-spectrum plane fits one CTA's shared memory (100 x 100: 41 KB) the whole
 // iteration of a (sample, filter) plane stays on chip: conj(D_k) g -> column IFFT -> row IFFT ->
-// update of w (row-major, requested into registers at the plane's start) -> row FFT of t' -> column FFT -> times D_k,
-// summed in registers over the CTA's filter group.  HBM per plane and iteration: w read + write
-// and the group partial (vs six passes over the spectrum for the row/column kernels).
+// update of w (row-major, requested into registers at the plane's start) -> row FFT of t' ->
+// column FFT -> times D_k, accumulated over the CTA's filter group into a shared-memory partial.
+// HBM per plane and iteration: w read + write and the group partial (vs six passes over the
+// spectrum for the row/column kernels).
 template <typename T, class G>
 struct PlaneArgs {
   int K, B, groups, kper;
