@@ -5,7 +5,8 @@ reference at 1e-9 on the config-3 grid by tests/test_config_parity_gpu.py).  Pri
 checkpoint, the max relative objective error over the mini-batches so far and the relative
 Frobenius error of the final filters (north_star bars: 1e-4 and 1e-3).
 
-python scripts/drift_cfg3.py [n_samples]   (default 2,000 = the whole config-3 stream)
+python scripts/drift_cfg3.py [n_samples [config]]   (default 2,000 = the whole config-3 stream;
+config 2: 100x100, K = 100, B = 10, the float64 history and Gauss-Jordan inverse in both builds)
 """
 import os
 import sys
@@ -18,12 +19,15 @@ import paper_1706_06972_b200 as ob  # noqa: E402
 from paper_1706_06972_b200.workloads import CONFIGS, synth_images  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000
-c = CONFIGS[3]
+cid = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+c = CONFIGS[cid]
 B = c["B"]
 kw = dict(n_filters=c["K"], beta=c["beta"], rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0,
-          code_max_iters=300, code_rel_tol=1e-3, batch_size=B, stop_tol=0.0, history_solver="chol")
+          code_max_iters=300, code_rel_tol=1e-3, batch_size=B, stop_tol=0.0)
+if cid == 3:
+    kw["history_solver"] = "chol"
 shape = ob.SignalShape(c["grid"], (11, 11))
-t32 = ob.OnlineTrainer(shape, ob.TrainConfig(dtype="float32", history_dtype="float32", **kw))
+t32 = ob.OnlineTrainer(shape, ob.TrainConfig(dtype="float32", history_dtype="float32" if cid == 3 else "float64", **kw))
 t64 = ob.OnlineTrainer(shape, ob.TrainConfig(dtype="float64", history_dtype="float64", **kw))
 
 
