@@ -10,6 +10,7 @@ the product kernels of that configuration:
   cfg1  42x42,  K=100, B=50        fused cluster kernel + tail split + overlapped inverse (f32)
   cfg2  100x100, K=100, B=10       f32: plane-resident k_plane + inverse beside coding; f64: stream
   cfg3  266x266, K=32 (chol), B=4  streaming 266-point kernels + blocked Cholesky (c64 / c128)
+  cfg3  266x266, K=256, B=32       full size, float32 + complex64 history vs the float64 build
 
 Bars (north_star): float64 1e-9 relative; float32 objective trace 1e-4, filters 1e-3 relative
 Frobenius.  Reference semantics: coding.py:67-119, dictionary.py:73-114, 176-215,
@@ -141,3 +142,29 @@ def test_config3_grid_float64_cholesky_matches_reference(golden):
     g = golden("cfg3_mb")
     tr = _trainer(g, "float64", history_solver="chol")
     _run(g, tr, "stream", TOL64, TOL64, exact_iters=True)
+
+
+def test_config3_full_size_float32_against_float64():
+    """BASELINE config 3 at its full size (266x266, K = 256, B = 32: the 9.4 GB complex64 history and
+    the 128-wide blocked Cholesky of the product path) for two mini-batches against the float64 /
+    complex128 build of the same path, whose 266x266 kernels and Cholesky are pinned to the
+    reference above (test_config3_grid_float64_cholesky_matches_reference).  north_star float32 bars;
+    scripts/drift_cfg3.py runs the whole 2,000-sample stream (profiles/r2_drift_cfg3.txt)."""
+    from paper_1706_06972_b200.workloads import CONFIGS
+
+    c = CONFIGS[3]
+    shape = ob.SignalShape(c["grid"], (11, 11))
+    kw = dict(n_filters=c["K"], beta=c["beta"], rho_code=1.0, rho_dict=1.0, inner_iters=10, seed=0,
+              code_max_iters=300, code_rel_tol=1e-3, batch_size=c["B"], stop_tol=0.0, history_solver="chol")
+    t32 = ob.OnlineTrainer(shape, ob.TrainConfig(dtype="float32", history_dtype="float32", **kw))
+    t64 = ob.OnlineTrainer(shape, ob.TrainConfig(dtype="float64", history_dtype="float64", **kw))
+    X = synth_images(2 * c["B"], c["dims0"], c["grid"], c["K0"], seed=2024).reshape(2 * c["B"], -1)
+    for m in range(2):
+        xb = X[m * c["B"]:(m + 1) * c["B"]]
+        a = t32.partial_fit(xb)
+        b = t64.partial_fit(xb)
+        assert t32.last_path == "stream" and t64.last_path == "stream"
+        assert np.max(np.abs(a.objectives - b.objectives) / np.abs(b.objectives)) < TOL32_OBJ
+    assert rel(t32.final_filters(), t64.final_filters()) < TOL32_FILT
+    del t32, t64
+    torch.cuda.empty_cache()
